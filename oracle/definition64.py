@@ -1,0 +1,132 @@
+"""Float64 model of the rasterizer definition -- an independent PIN for taoracle.c.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Written separately from
+taoracle.c with whole-array linear algebra instead of the normative scalar
+sequence: matrices are built with numpy / scipy (quaternion -> matrix via
+scipy.spatial.transform.Rotation), the EWA covariance as J W Sigma W^T J^T
+(PAPER.md P:386-388 via [kerbl20233d]), compositing per pixel with cumulative
+products.  Real arithmetic in float64; its decisions (q <= 9, stop at T < 1e-4)
+can therefore differ from the fp32 oracle on pixels that straddle a threshold,
+which the pins count and bound instead of requiring equality.
+"""
+from __future__ import annotations
+
+import numpy as np
+from scipy.spatial.transform import Rotation
+
+MARGIN_REL = 1.0 + 2.0 ** -10
+MARGIN_ABS = 2.0 ** -10
+
+
+def unproject(scene, d_min=0.0):
+    """a1 in float64: returns pos (n,3), cov (n,3,3), alpha (n,), ids (n,), feat (n,C) float64."""
+    P, S, A, F = [], [], [], []
+    for v in scene.views:
+        cam = v.cam
+        H, W = cam.H, cam.W
+        d = v.disparity.astype(np.float64)
+        keep = np.isfinite(d) & (d > d_min)
+        if v.mask is not None:
+            keep &= v.mask != 0
+        op = (v.opacity.astype(np.float64) if v.opacity is not None
+              else np.full((H, W), scene.default_opacity))
+        keep &= ~np.isnan(op)
+        ys, xs = np.nonzero(keep)                       # row-major order
+        fx, fy = np.float64(np.float32(cam.fx)), np.float64(np.float32(cam.fy))
+        cx, cy = np.float64(np.float32(cam.cx)), np.float64(np.float32(cam.cy))
+        B = np.float64(np.float32(v.baseline))
+        R = cam.R.astype(np.float32).astype(np.float64)
+        t = cam.t.astype(np.float32).astype(np.float64)
+        z = fx * B / d[ys, xs]
+        Xc = np.stack([(xs - cx) / fx * z, (ys - cy) / fy * z, z], axis=1)
+        P.append((Xc - t) @ R)                          # R^T (X_c - t) as row vectors
+        if v.scale is not None:
+            s = v.scale[ys, xs].astype(np.float64)
+        else:
+            s = np.full((len(xs), 3), np.float64(np.float32(scene.default_scale)))
+        if v.quat is not None:
+            q = v.quat[ys, xs].astype(np.float64)       # (w, x, y, z)
+            Rq = Rotation.from_quat(q[:, [1, 2, 3, 0]]).as_matrix()
+        else:
+            Rq = np.broadcast_to(np.eye(3), (len(xs), 3, 3))
+        S.append(Rq @ (s[:, :, None] ** 2 * np.swapaxes(Rq, 1, 2)))
+        A.append(np.clip(op[ys, xs], 0.0, 1.0))
+        F.append(v.feat[ys, xs].astype(np.float64))
+    pos = np.concatenate(P)
+    return dict(pos=pos, cov=np.concatenate(S), alpha=np.concatenate(A), feat=np.concatenate(F),
+                ids=np.arange(len(pos)))
+
+
+def project(g, cam, dilation=0.3, cull_sigma=3.0, z_near=0.01):
+    """a2 in float64 -> visible, mean (n,2), cov2 (n,2,2), rect (n,4), depth (n,)."""
+    fx, fy = np.float64(np.float32(cam.fx)), np.float64(np.float32(cam.fy))
+    cx, cy = np.float64(np.float32(cam.cx)), np.float64(np.float32(cam.cy))
+    R = cam.R.astype(np.float32).astype(np.float64)
+    t = cam.t.astype(np.float32).astype(np.float64)
+    X = g["pos"] @ R.T + t
+    x, y, z = X[:, 0], X[:, 1], X[:, 2]
+    ok = z > z_near
+    zs = np.where(ok, z, 1.0)
+    mean = np.stack([fx * x / zs + cx, fy * y / zs + cy], axis=1)
+    n = len(z)
+    J = np.zeros((n, 2, 3))
+    J[:, 0, 0] = fx / zs
+    J[:, 0, 2] = -fx * x / zs ** 2
+    J[:, 1, 1] = fy / zs
+    J[:, 1, 2] = -fy * y / zs ** 2
+    T = J @ R
+    cov2 = T @ g["cov"] @ np.swapaxes(T, 1, 2) + dilation * np.eye(2)
+    det = np.linalg.det(cov2)
+    ok &= det > 0
+    h = cull_sigma * np.sqrt(np.stack([cov2[:, 0, 0], cov2[:, 1, 1]], axis=1)) * MARGIN_REL + MARGIN_ABS
+    lo = np.ceil(mean - h)
+    hi = np.floor(mean + h)
+    lim = np.array([cam.W - 1, cam.H - 1], np.float64)
+    ok &= np.all(lo <= lim, axis=1) & np.all(hi >= 0, axis=1)
+    lo = np.clip(lo, 0, lim)
+    hi = np.clip(hi, 0, lim)
+    ok &= np.all(lo <= hi, axis=1)
+    rect = np.stack([lo[:, 0], hi[:, 0], lo[:, 1], hi[:, 1]], axis=1).astype(np.int64)
+    return dict(visible=ok, mean=mean, cov2=cov2, rect=rect, depth=z)
+
+
+def composite(g, pr, H, W, alpha_max=0.99, alpha_min=1.0 / 255.0, t_eps=1e-4, cull_sigma=3.0):
+    """a6 brute force in float64: every pixel over all visible Gaussians by (depth, id)."""
+    vis = np.nonzero(pr["visible"])[0]
+    # R12: the depth order key is the camera depth as an fp32 number, ties by id
+    zkey = pr["depth"][vis].astype(np.float32)
+    order = vis[np.lexsort((g["ids"][vis], zkey))]
+    mean = pr["mean"][order]
+    conic = np.linalg.inv(pr["cov2"][order])
+    rect = pr["rect"][order]
+    al = g["alpha"][order]
+    feat = g["feat"][order]
+    C = feat.shape[1]
+    F = np.zeros((H, W, C))
+    A = np.zeros((H, W))
+    NC = np.zeros((H, W), np.int64)
+    for py in range(H):
+        rowmask = (rect[:, 2] <= py) & (py <= rect[:, 3])
+        idx = np.nonzero(rowmask)[0]
+        if len(idx) == 0:
+            continue
+        for px in range(W):
+            sel = idx[(rect[idx, 0] <= px) & (px <= rect[idx, 1])]
+            if len(sel) == 0:
+                continue
+            d = np.array([px, py], np.float64) - mean[sel]
+            q = np.einsum("ni,nij,nj->n", d, conic[sel], d)
+            a = np.minimum(alpha_max, al[sel] * np.exp(-0.5 * q))
+            use = (q <= cull_sigma ** 2) & (a >= alpha_min)
+            sel, a = sel[use], a[use]
+            if len(sel) == 0:
+                continue
+            Tn = np.cumprod(1.0 - a)
+            stop = np.nonzero(Tn < t_eps)[0]
+            m = stop[0] if len(stop) else len(a)
+            Tb = np.concatenate([[1.0], Tn[:m]])
+            w = a[:m] * Tb[:m]
+            F[py, px] = w @ feat[sel[:m]]
+            A[py, px] = 1.0 - Tb[m]
+            NC[py, px] = m
+    return F, A, NC

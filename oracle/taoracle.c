@@ -1,0 +1,427 @@
+/*
+ * oracle/taoracle.c -- CPU ORACLE for the latent-Gaussian rasterizer hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load this library.  The product path
+ * (paper_2405_14866_b200/, libtaloha.so) never links, imports or calls it, and the
+ * two share no code, headers or constants generators.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, cited "P:<line>"):
+ *   a1  lift foreground pixels to latent Gaussians {x, f, s, alpha}, R = I unless a
+ *       rotation map is given ("four properties ... rotation ... identity",
+ *       P:376 "3D positions x ... unprojected from depth maps", "foreground
+ *       pixels ... lifted to pixel-aligned Gaussian points", P:358 disparity ->
+ *       depth; z = fx*B/d is DESIGN.md reading R2);
+ *   a2  project each Gaussian to the target camera Pi_novel with the EWA 2D
+ *       covariance (the rasterizer of [kerbl20233d]);
+ *   a3-a5  bin to 16x16 tiles and order each tile's list by (depth, id)
+ *       (the [kerbl20233d] tile/sort scheme);
+ *   a6  front-to-back alpha compositing of the C-channel latent feature into
+ *       F_novel and accumulated alpha ("F_novel = R_G({G}, Pi_novel)").
+ * Every constant the paper leaves to [kerbl20233d] is a DESIGN.md reading (R7-R13).
+ *
+ * Arithmetic: plain IEEE fp32, one operation at a time, in the normative order
+ * written in DESIGN.md "Normative arithmetic" (built with -ffp-contract=off
+ * -fno-fast-math, so every `a*b+c` below is two roundings and fmaf() is the only
+ * fused operation).  Decisions that turn floats into integers (cull, pixel/tile
+ * rectangles, depth order, q <= 9, alpha' >= 1/255, the T < 1e-4 stop) are taken
+ * in this fp32 sequence -- the kernel's precision -- so tile lists, order and T/A
+ * can be compared bit-exactly.  oracle/definition64.py is an
+ * independent float64 model of the same definition that pins this file.
+ *
+ * Deliberately slow: qsort for the tile order, one pixel at a time for compositing.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct { float fx, fy, cx, cy; } tao_intr;          /* pixels */
+typedef struct { float R[9]; float t[3]; } tao_extr;        /* world->camera, R row-major */
+typedef struct {
+    float dilation;        /* R7: added to the diagonal of Sigma' (px^2), default 0.3 */
+    float alpha_max;       /* R9: alpha' clamp, default 0.99 */
+    float alpha_min;       /* R9: skip alpha' < 1/255 */
+    float t_eps;           /* R10: stop before T would drop below 1e-4 */
+    float cull_sigma;      /* R8: q <= cull_sigma^2 and the 3-sigma box */
+    float z_near;          /* R14: cull z <= 0.01 m */
+    float d_min;           /* a1: lift iff d > d_min */
+    float default_scale;   /* a1: isotropic scale when no scale map */
+    float default_opacity; /* a1: opacity when no opacity map */
+} tao_params;
+
+#define TAO_TILE 16
+
+/* ------------------------------------------------------------------ helpers */
+
+static float f16_to_f32(uint16_t h) {
+    uint32_t sign = (uint32_t)(h >> 15) << 31;
+    uint32_t ex = (h >> 10) & 0x1f, man = h & 0x3ff, bits;
+    if (ex == 0) {
+        if (man == 0) {
+            bits = sign;
+        } else { /* subnormal half: renormalise */
+            int e = -1;
+            do { e++; man <<= 1; } while ((man & 0x400) == 0);
+            bits = sign | ((uint32_t)(127 - 15 - e) << 23) | ((man & 0x3ff) << 13);
+        }
+    } else if (ex == 31) {
+        bits = sign | 0x7f800000u | (man << 13);
+    } else {
+        bits = sign | ((ex + 127 - 15) << 23) | (man << 13);
+    }
+    float f;
+    memcpy(&f, &bits, 4);
+    return f;
+}
+
+static float feat_at(const void* feat, int feat_bytes, int C, int64_t g, int c) {
+    if (feat_bytes == 2) return f16_to_f32(((const uint16_t*)feat)[g * C + c]);
+    return ((const float*)feat)[g * C + c];
+}
+
+static uint32_t float_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+
+/* dot3(a, b) = fma(a2, b2, fma(a1, b1, a0*b0))  (DESIGN.md normative dot product) */
+static float dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
+    return fmaf(a2, b2, fmaf(a1, b1, a0 * b0));
+}
+
+/*
+ * exp_det -- DESIGN.md reading R13.  exp(x) for x <= 0 by a fixed fp32 sequence:
+ * k = rint(x*log2 e); Cody-Waite reduction r = x - k*ln2 (hi/lo split); degree-7
+ * Taylor polynomial in Horner form with fmaf; scale by 2^k (exact).  Pinned in
+ * tests/test_oracle_pins.py against float64 exp over [-4.5, 0] (<= 2 ulp).
+ */
+float tao_exp_det(float x) {
+    if (x < -80.0f) x = -80.0f;
+    float k = rintf(x * 1.44269502162933349609375f);          /* float(log2 e) */
+    float r = fmaf(-k, 0.693145751953125f, x);                  /* ln2 hi */
+    r = fmaf(-k, 1.428606765330187045037746429443359375e-06f, r); /* ln2 lo */
+    float p = 1.98412698412698412698e-4f;                       /* 1/5040 */
+    p = fmaf(p, r, 1.38888888888888888889e-3f);                 /* 1/720 */
+    p = fmaf(p, r, 8.33333333333333333333e-3f);                 /* 1/120 */
+    p = fmaf(p, r, 4.16666666666666666667e-2f);                 /* 1/24 */
+    p = fmaf(p, r, 1.66666666666666666667e-1f);                 /* 1/6 */
+    p = fmaf(p, r, 0.5f);
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
+    uint32_t sb = (uint32_t)((int)k + 127) << 23;
+    float s;
+    memcpy(&s, &sb, 4);
+    return p * s;
+}
+
+/* ------------------------------------------------------------ a1 unproject */
+/*
+ * One source view, pixels row-major.  Appends the lifted Gaussians of this view to
+ * the output arrays starting at index 0 of each given pointer and returns how many.
+ * ids are id0, id0+1, ... (running index over views, DESIGN.md a1).
+ *   pos[n][3]  world position;   alpha[n];   cov6[n][6] = (s00,s01,s02,s11,s12,s22)
+ *   ids[n];   feat_out[n][C] same element type as feat (bytes copied).
+ */
+int64_t tao_unproject_view(int H, int W, const float* disp, const uint8_t* mask,
+                           const tao_intr* K, const tao_extr* RT, float baseline,
+                           const float* scale, const float* quat, const float* opacity,
+                           const void* feat, int C, int feat_bytes, const tao_params* p,
+                           int64_t id0, float* pos, float* alpha, float* cov6, int64_t* ids,
+                           void* feat_out) {
+    int64_t n = 0;
+    const float* R = RT->R;
+    const float* t = RT->t;
+    for (int y = 0; y < H; y++) {
+        for (int x = 0; x < W; x++) {
+            int64_t pix = (int64_t)y * W + x;
+            float d = disp[pix];
+            if (mask && mask[pix] == 0) continue;               /* foreground only */
+            if (!isfinite(d) || !(d > p->d_min)) continue;      /* invalid disparity: skipped */
+            float a = opacity ? opacity[pix] : p->default_opacity;
+            if (isnan(a)) continue;
+            a = fminf(fmaxf(a, 0.0f), 1.0f);
+
+            /* depth from disparity (R2: z = fx*B/d) and camera-space point */
+            float z = (K->fx * baseline) / d;
+            float xc = (((float)x - K->cx) / K->fx) * z;
+            float yc = (((float)y - K->cy) / K->fy) * z;
+            float zc = z;
+            /* world point X_w = R^T (X_c - t) */
+            float p0 = xc - t[0], p1 = yc - t[1], p2 = zc - t[2];
+            float w0 = dot3(R[0], R[3], R[6], p0, p1, p2);
+            float w1 = dot3(R[1], R[4], R[7], p0, p1, p2);
+            float w2 = dot3(R[2], R[5], R[8], p0, p1, p2);
+
+            /* scale (R5) and rotation (identity; R4: optional quaternion map) */
+            float s0, s1, s2;
+            if (scale) { s0 = scale[pix * 3 + 0]; s1 = scale[pix * 3 + 1]; s2 = scale[pix * 3 + 2]; }
+            else { s0 = s1 = s2 = p->default_scale; }
+            float qw = 1.0f, qx = 0.0f, qy = 0.0f, qz = 0.0f;
+            if (quat) {
+                float aw = quat[pix * 4 + 0], ax = quat[pix * 4 + 1];
+                float ay = quat[pix * 4 + 2], az = quat[pix * 4 + 3];
+                float n2 = fmaf(az, az, fmaf(ay, ay, fmaf(ax, ax, aw * aw)));
+                if (n2 > 0.0f && isfinite(n2)) {
+                    float nn = sqrtf(n2);
+                    qw = aw / nn; qx = ax / nn; qy = ay / nn; qz = az / nn;
+                }
+            }
+            float xx = qx * qx, yy = qy * qy, zz = qz * qz;
+            float xy = qx * qy, xz = qx * qz, yz = qy * qz;
+            float wx = qw * qx, wy = qw * qy, wz = qw * qz;
+            float Rq[9];
+            Rq[0] = 1.0f - 2.0f * (yy + zz); Rq[1] = 2.0f * (xy - wz);        Rq[2] = 2.0f * (xz + wy);
+            Rq[3] = 2.0f * (xy + wz);        Rq[4] = 1.0f - 2.0f * (xx + zz); Rq[5] = 2.0f * (yz - wx);
+            Rq[6] = 2.0f * (xz - wy);        Rq[7] = 2.0f * (yz + wx);        Rq[8] = 1.0f - 2.0f * (xx + yy);
+            float ss[3] = {s0 * s0, s1 * s1, s2 * s2};
+            float M[9];   /* M = Rq diag(s^2) */
+            for (int i = 0; i < 3; i++)
+                for (int k = 0; k < 3; k++) M[i * 3 + k] = Rq[i * 3 + k] * ss[k];
+            /* Sigma_w = Rq diag(s^2) Rq^T, upper triangle */
+            static const int IJ[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+            for (int e = 0; e < 6; e++) {
+                int i = IJ[e][0], j = IJ[e][1];
+                cov6[n * 6 + e] = dot3(M[i * 3 + 0], M[i * 3 + 1], M[i * 3 + 2],
+                                       Rq[j * 3 + 0], Rq[j * 3 + 1], Rq[j * 3 + 2]);
+            }
+            pos[n * 3 + 0] = w0; pos[n * 3 + 1] = w1; pos[n * 3 + 2] = w2;
+            alpha[n] = a;
+            ids[n] = id0 + n;
+            memcpy((char*)feat_out + n * (int64_t)C * feat_bytes,
+                   (const char*)feat + pix * (int64_t)C * feat_bytes, (size_t)C * feat_bytes);
+            n++;
+        }
+    }
+    return n;
+}
+
+/* -------------------------------------------------------------- a2 project */
+/*
+ * EWA projection of n Gaussians into the target camera (H x W pixels).
+ * Outputs per Gaussian: visible (0/1); mean2[2] pixel centre; conic[3] =
+ * (ca, cb2, cc) with q = ca dx^2 + cb2 dx dy + cc dy^2; cov2d[3] = (a, b, c) of
+ * Sigma' + dilation*I; rect[4] = pixel box (x0, x1, y0, y1) inclusive; depth key
+ * dkey = bits(z) of the camera-space centre depth (R12).
+ */
+void tao_project(int64_t n, const float* pos, const float* cov6, const tao_intr* K,
+                 const tao_extr* RT, int H, int W, const tao_params* p, int32_t* visible,
+                 float* mean2, float* conic, float* cov2d, int32_t* rect, uint32_t* dkey) {
+    const float* R = RT->R;
+    const float* t = RT->t;
+    for (int64_t g = 0; g < n; g++) {
+        visible[g] = 0;
+        dkey[g] = 0;
+        rect[g * 4 + 0] = 1; rect[g * 4 + 1] = 0; rect[g * 4 + 2] = 1; rect[g * 4 + 3] = 0;
+        float w0 = pos[g * 3 + 0], w1 = pos[g * 3 + 1], w2 = pos[g * 3 + 2];
+        float X = dot3(R[0], R[1], R[2], w0, w1, w2) + t[0];
+        float Y = dot3(R[3], R[4], R[5], w0, w1, w2) + t[1];
+        float Z = dot3(R[6], R[7], R[8], w0, w1, w2) + t[2];
+        if (!(Z > p->z_near)) continue;                                   /* R14 */
+        float u = X / Z, v = Y / Z;
+        float mx = fmaf(K->fx, u, K->cx);
+        float my = fmaf(K->fy, v, K->cy);
+        /* EWA: J = d(pixel)/d(X_c) at X (2x3, J01 = J10 = 0); T = J R */
+        float J00 = K->fx / Z, J11 = K->fy / Z;
+        float J02 = -(J00 * u), J12 = -(J11 * v);
+        float T0[3], T1[3];
+        for (int j = 0; j < 3; j++) {
+            T0[j] = fmaf(J02, R[6 + j], J00 * R[0 + j]);
+            T1[j] = fmaf(J12, R[6 + j], J11 * R[3 + j]);
+        }
+        const float* s = cov6 + g * 6;
+        float S[9] = {s[0], s[1], s[2], s[1], s[3], s[4], s[2], s[4], s[5]};
+        float M0[3], M1[3];   /* M = T Sigma_w */
+        for (int j = 0; j < 3; j++) {
+            M0[j] = dot3(T0[0], T0[1], T0[2], S[0 + j], S[3 + j], S[6 + j]);
+            M1[j] = dot3(T1[0], T1[1], T1[2], S[0 + j], S[3 + j], S[6 + j]);
+        }
+        /* Sigma' = M T^T (+ dilation on the diagonal, R7) */
+        float a = dot3(M0[0], M0[1], M0[2], T0[0], T0[1], T0[2]) + p->dilation;
+        float b = dot3(M0[0], M0[1], M0[2], T1[0], T1[1], T1[2]);
+        float c = dot3(M1[0], M1[1], M1[2], T1[0], T1[1], T1[2]) + p->dilation;
+        float det = fmaf(a, c, -(b * b));
+        if (!(det > 0.0f)) continue;
+        float ca = c / det;
+        float cb = (-b) / det;
+        float cc = a / det;
+        /* 3-sigma box with rounding margin (R8), clipped to the image (R18) */
+        float hx = fmaf(p->cull_sigma * sqrtf(a), 1.0009765625f, 0.0009765625f);
+        float hy = fmaf(p->cull_sigma * sqrtf(c), 1.0009765625f, 0.0009765625f);
+        float fx0 = ceilf(mx - hx), fx1 = floorf(mx + hx);
+        float fy0 = ceilf(my - hy), fy1 = floorf(my + hy);
+        if (!(fx0 <= (float)(W - 1)) || !(fx1 >= 0.0f) || !(fy0 <= (float)(H - 1)) || !(fy1 >= 0.0f))
+            continue;
+        int x0 = fx0 < 0.0f ? 0 : (int)fx0;
+        int x1 = fx1 > (float)(W - 1) ? W - 1 : (int)fx1;
+        int y0 = fy0 < 0.0f ? 0 : (int)fy0;
+        int y1 = fy1 > (float)(H - 1) ? H - 1 : (int)fy1;
+        if (x0 > x1 || y0 > y1) continue;
+        visible[g] = 1;
+        mean2[g * 2 + 0] = mx; mean2[g * 2 + 1] = my;
+        conic[g * 3 + 0] = ca; conic[g * 3 + 1] = cb + cb; conic[g * 3 + 2] = cc;
+        cov2d[g * 3 + 0] = a; cov2d[g * 3 + 1] = b; cov2d[g * 3 + 2] = c;
+        rect[g * 4 + 0] = x0; rect[g * 4 + 1] = x1; rect[g * 4 + 2] = y0; rect[g * 4 + 3] = y1;
+        dkey[g] = float_bits(Z);
+    }
+}
+
+/* ----------------------------------------------------- a3-a5 tile lists */
+
+typedef struct { uint32_t tile, dkey; int64_t id, g; } tao_entry;
+
+static int entry_cmp(const void* pa, const void* pb) {
+    const tao_entry* a = (const tao_entry*)pa;
+    const tao_entry* b = (const tao_entry*)pb;
+    if (a->tile != b->tile) return a->tile < b->tile ? -1 : 1;
+    if (a->dkey != b->dkey) return a->dkey < b->dkey ? -1 : 1;
+    if (a->id != b->id) return a->id < b->id ? -1 : 1;
+    return 0;
+}
+
+/* K = number of (tile, Gaussian) pairs: each visible Gaussian covers the tiles of its pixel box */
+int64_t tao_count_entries(int64_t n, const int32_t* visible, const int32_t* rect) {
+    int64_t K = 0;
+    for (int64_t g = 0; g < n; g++) {
+        if (!visible[g]) continue;
+        int64_t tw = rect[g * 4 + 1] / TAO_TILE - rect[g * 4 + 0] / TAO_TILE + 1;
+        int64_t th = rect[g * 4 + 3] / TAO_TILE - rect[g * 4 + 2] / TAO_TILE + 1;
+        K += tw * th;
+    }
+    return K;
+}
+
+/*
+ * Per-tile lists ordered by (tile, dkey, id): ranges[T][2] = [start, end) into list;
+ * list[K] = array index g of the Gaussian.  Tiles are row-major, T = ceil(W/16)*ceil(H/16).
+ * Returns K.
+ */
+int64_t tao_tile_lists(int64_t n, const int32_t* visible, const int32_t* rect, const uint32_t* dkey,
+                       const int64_t* ids, int H, int W, uint32_t* ranges, int64_t* list) {
+    int TX = (W + TAO_TILE - 1) / TAO_TILE, TY = (H + TAO_TILE - 1) / TAO_TILE;
+    int64_t K = tao_count_entries(n, visible, rect);
+    tao_entry* e = (tao_entry*)malloc(sizeof(tao_entry) * (size_t)(K > 0 ? K : 1));
+    int64_t k = 0;
+    for (int64_t g = 0; g < n; g++) {
+        if (!visible[g]) continue;
+        for (int ty = rect[g * 4 + 2] / TAO_TILE; ty <= rect[g * 4 + 3] / TAO_TILE; ty++)
+            for (int tx = rect[g * 4 + 0] / TAO_TILE; tx <= rect[g * 4 + 1] / TAO_TILE; tx++) {
+                e[k].tile = (uint32_t)(ty * TX + tx);
+                e[k].dkey = dkey[g];
+                e[k].id = ids[g];
+                e[k].g = g;
+                k++;
+            }
+    }
+    qsort(e, (size_t)K, sizeof(tao_entry), entry_cmp);
+    for (int t = 0; t < TX * TY; t++) { ranges[2 * t] = 0; ranges[2 * t + 1] = 0; }
+    for (int64_t i = 0; i < K; i++) {
+        uint32_t t = e[i].tile;
+        if (i == 0 || e[i - 1].tile != t) ranges[2 * t] = (uint32_t)i;
+        ranges[2 * t + 1] = (uint32_t)(i + 1);
+        list[i] = e[i].g;
+    }
+    free(e);
+    return K;
+}
+
+/* ------------------------------------------------------------ a6 composite */
+
+/* Front-to-back compositing of one pixel over a sequence of Gaussians (DESIGN.md a6). */
+static void composite_pixel(int px, int py, int C, int64_t count, const int64_t* seq,
+                            const float* alpha, const float* mean2, const float* conic,
+                            const int32_t* rect, const void* feat, int feat_bytes,
+                            const tao_params* p, float* F, float* A, int32_t* n_contrib,
+                            int32_t* n_eval) {
+    float T = 1.0f;
+    float qmax = p->cull_sigma * p->cull_sigma;
+    int32_t nc = 0, ne = 0;
+    for (int c = 0; c < C; c++) F[c] = 0.0f;
+    for (int64_t j = 0; j < count; j++) {
+        int64_t g = seq[j];
+        ne++;
+        const int32_t* r = rect + g * 4;
+        if (px < r[0] || px > r[1] || py < r[2] || py > r[3]) continue;   /* R8 box */
+        float dx = (float)px - mean2[g * 2 + 0];
+        float dy = (float)py - mean2[g * 2 + 1];
+        float q = fmaf(fmaf(conic[g * 3 + 0], dx, conic[g * 3 + 1] * dy), dx,
+                       (conic[g * 3 + 2] * dy) * dy);
+        if (!(q <= qmax)) continue;                                         /* 3 sigma */
+        float e = tao_exp_det(-0.5f * q);
+        float a = fminf(p->alpha_max, alpha[g] * e);                        /* R9 */
+        if (a < p->alpha_min) continue;
+        float Tn = T * (1.0f - a);
+        if (Tn < p->t_eps) break;                                           /* R10 */
+        float w = a * T;
+        for (int c = 0; c < C; c++) F[c] = F[c] + feat_at(feat, feat_bytes, C, g, c) * w;
+        T = Tn;
+        nc++;
+    }
+    *A = 1.0f - T;                                                          /* R11 */
+    if (n_contrib) *n_contrib = nc;
+    if (n_eval) *n_eval = ne;
+}
+
+/*
+ * Tiled compositing: each pixel walks its tile's (dkey, id)-ordered list.
+ * tiles: indices of the tiles to render (NULL = all).  F[H*W*C] (HWC), A[H*W];
+ * n_contrib / n_eval [H*W] optional.  Pixels of tiles not rendered are untouched.
+ */
+void tao_composite_tiles(int H, int W, int C, int feat_bytes, const float* alpha,
+                         const float* mean2, const float* conic, const int32_t* rect,
+                         const void* feat, const uint32_t* ranges, const int64_t* list,
+                         const tao_params* p, const int32_t* tiles, int64_t n_tiles, float* F,
+                         float* A, int32_t* n_contrib, int32_t* n_eval) {
+    int TX = (W + TAO_TILE - 1) / TAO_TILE, TY = (H + TAO_TILE - 1) / TAO_TILE;
+    if (!tiles) n_tiles = (int64_t)TX * TY;
+    for (int64_t k = 0; k < n_tiles; k++) {
+        int t = tiles ? tiles[k] : (int)k;
+        int tx = t % TX, ty = t / TX;
+        uint32_t s = ranges[2 * t], e = ranges[2 * t + 1];
+        for (int py = ty * TAO_TILE; py < ty * TAO_TILE + TAO_TILE && py < H; py++)
+            for (int px = tx * TAO_TILE; px < tx * TAO_TILE + TAO_TILE && px < W; px++) {
+                int64_t pix = (int64_t)py * W + px;
+                composite_pixel(px, py, C, (int64_t)(e - s), list + s, alpha, mean2, conic, rect,
+                                feat, feat_bytes, p, F + pix * C, A + pix,
+                                n_contrib ? n_contrib + pix : NULL, n_eval ? n_eval + pix : NULL);
+            }
+    }
+}
+
+typedef struct { uint32_t dkey; int64_t id, g; } tao_depth;
+
+static int depth_cmp(const void* pa, const void* pb) {
+    const tao_depth* a = (const tao_depth*)pa;
+    const tao_depth* b = (const tao_depth*)pb;
+    if (a->dkey != b->dkey) return a->dkey < b->dkey ? -1 : 1;
+    if (a->id != b->id) return a->id < b->id ? -1 : 1;
+    return 0;
+}
+
+/*
+ * Brute force: no tiles.  Every pixel walks ALL visible Gaussians in global (dkey, id)
+ * order with the same inclusion predicate.  rows [y0, y1) only (row bands bound time).
+ */
+void tao_composite_bruteforce(int H, int W, int C, int feat_bytes, int64_t n,
+                              const int32_t* visible, const uint32_t* dkey, const int64_t* ids,
+                              const float* alpha, const float* mean2, const float* conic,
+                              const int32_t* rect, const void* feat, const tao_params* p,
+                              int y0, int y1, float* F, float* A, int32_t* n_contrib) {
+    int64_t m = 0;
+    tao_depth* d = (tao_depth*)malloc(sizeof(tao_depth) * (size_t)(n > 0 ? n : 1));
+    for (int64_t g = 0; g < n; g++)
+        if (visible[g]) { d[m].dkey = dkey[g]; d[m].id = ids[g]; d[m].g = g; m++; }
+    qsort(d, (size_t)m, sizeof(tao_depth), depth_cmp);
+    int64_t* seq = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+    for (int64_t i = 0; i < m; i++) seq[i] = d[i].g;
+    free(d);
+    for (int py = y0; py < y1 && py < H; py++)
+        for (int px = 0; px < W; px++) {
+            int64_t pix = (int64_t)py * W + px;
+            composite_pixel(px, py, C, m, seq, alpha, mean2, conic, rect, feat, feat_bytes, p,
+                            F + pix * C, A + pix, n_contrib ? n_contrib + pix : NULL, NULL);
+        }
+    free(seq);
+}
+
+/* vectorised exp_det for the pins */
+void tao_exp_det_array(int64_t n, const float* x, float* y) {
+    for (int64_t i = 0; i < n; i++) y[i] = tao_exp_det(x[i]);
+}

@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""bench.py -- target views/s of the latent-Gaussian rasterizer on B200 (BASELINE.json metric).
+
+Step (one pass of the whole hot path) = one frame of the c4 workload
+(BASELINE.json configs[3]): ta_unproject of the 4 x 1024^2 source views (1.67M Gaussians, C = 32,
+fp16-stored features) on rank 0, NCCL broadcast of the Gaussian set when N > 1, then
+ta_rasterize of this rank's share of the 32 parallax targets (1024^2, HWC fp32 + alpha).
+`value` = 32 views x steps / max-over-ranks device time (strong scaling: 32 views per frame
+regardless of N).  Inputs are resident in HBM before the timed region and larger than L2
+(423 MB of source maps, 187 MB Gaussian set, 16.9M tile entries per view).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun each rank drives one GPU; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "target views/sec and ms/view, 1024² 32-ch features, 1/2/4/8 B200; HBM roofline %"
+HBM_FALLBACK_GBS = 6650.0
+SM_CLOCK_MAX_MHZ = 1965.0
+FP32_LANES_PER_SM = 128          # B200: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / guide unit counts)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "sm_max_mhz": SM_CLOCK_MAX_MHZ}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.proc = None
+        self.dev = device_index
+
+    def start(self):
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.dev).uuid)
+            sel = ["--id=" + (uuid if uuid.startswith("GPU-") else "GPU-" + uuid)]
+        except Exception:
+            sel = ["-i", str(self.dev)]
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", *sel, "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) leg
+def oracle_crop_view(scene_g, cam, crop=256):
+    """One bounded sample of the per-view work on the CPU oracle: the central crop x crop window of a
+    1024^2 target (1/16 of its pixels) -- project all Gaussians, build the window's tile lists,
+    composite every window pixel.  Returns seconds."""
+    import oracle
+    import synthgen as sg
+    x0 = (cam.W - crop) // 2
+    y0 = (cam.H - crop) // 2
+    cc = sg.crop_camera(cam, x0, y0, crop, crop)
+    t0 = time.perf_counter()
+    oracle.rasterize(scene_g, cc)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_value(g, cam, steps=1, crop=256):
+    ts = [oracle_crop_view(g, cam, crop) for _ in range(steps)]
+    frac = (crop * crop) / float(cam.W * cam.H)
+    t = statistics.mean(ts)
+    return 1.0 / (t / frac), t, frac
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import synthgen as sg
+    import oracle
+    s = sg.make_config("c3")
+    g = oracle.unproject(s)
+    cam = sg.make_targets("c4")[0]
+    for _ in range(args.warmup):
+        oracle_crop_view(g, cam)
+    ts = [oracle_crop_view(g, cam) for _ in range(args.steps)]
+    frac = 256 * 256 / float(cam.W * cam.H)
+    t = statistics.mean(ts)
+    value = frac / t
+    sample = ("oracle/taoracle.c single-threaded: per step the central 256x256 window (1/16 of the pixels) of a "
+              "c4 1024^2 target -- EWA projection of all 1.67M Gaussians, (tile, depth, id) lists of the window, "
+              "compositing of its 65,536 pixels; value = (1/16) / step seconds; unprojection (per frame, "
+              "<1% of the oracle's per-view time) excluded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "ms_per_view": t * 1e3 / frac,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload_config(None, None),
+            "cpu_baseline": {"value": value, "unit": "views/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(n, K):
+    return {"workload": "c4: BASELINE.json configs[3] -- c3 Gaussian set (4 x 1024^2 sources, C=32 fp16-stored) "
+                        "rendered to 32 parallax targets 1024^2 per frame",
+            "views_per_step": 32, "target": "1024x1024", "C": 32, "feat_storage": "f16", "sources": "4x1024x1024",
+            "n_gaussians": n, "entries_per_view": K,
+            "l2": "no flush: inputs larger than L2 (423 MB source maps, 187 MB Gaussian set, "
+                  "~68 MB tile lists + 138 MB output per view)",
+            "parallelism": "target views sharded over ranks; Gaussian set NCCL-broadcast from rank 0"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synthgen as sg
+    import paper_2405_14866_b200 as tb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    n_views = args.views
+    targets = sg.make_targets("c4", n_targets=n_views)
+    mine = list(range(rank * n_views // world, (rank + 1) * n_views // world))
+    ctx = tb.Context(local)
+    C_, H, W = 32, 1024, 1024
+    cap = 4 * 1024 * 1024
+    g = tb.GaussianBuffers(cap, C_, "f16", device=dev)
+    params_sync = tb.default_params()
+    params = tb.default_params(flags=tb.TA_FLAG_ASYNC)
+
+    scene = None
+    views = keep = None
+    if rank == 0:
+        scene = sg.make_config("c3")
+        views, keep = tb.views_to_device(scene.views, device=dev)
+    cams = []
+    for j in mine:
+        K, R, t = sg.cam_arrays(targets[j])
+        cams.append((tb.intrinsics(K), tb.extrinsics(R, t)))
+    outs = [(torch.empty((H, W, C_), dtype=torch.float32, device=dev),
+             torch.empty((H, W), dtype=torch.float32, device=dev)) for _ in mine]
+
+    def broadcast():
+        if world == 1:
+            return
+        dist.broadcast(g.n_dev, 0)
+        n = int(g.n_dev.item())
+        dist.broadcast(g.pos_alpha[:n], 0)
+        dist.broadcast(g.cov[:n], 0)
+        dist.broadcast(g.feat[:n], 0)
+
+    def step(p):
+        if rank == 0:
+            ctx.unproject(views, params_sync, g, stream)
+        broadcast()
+        for (Ki, Ri), (F, A) in zip(cams, outs):
+            ctx.rasterize(g, -1, Ki, Ri, H, W, p, F, A, stream)
+
+    # sizing pass (synchronous): learn K per view, reserve for async steps
+    step(params_sync)
+    torch.cuda.synchronize()
+    kmax = 0
+    for (Ki, Ri), (F, A) in zip(cams, outs):
+        ctx.rasterize(g, -1, Ki, Ri, H, W, params_sync, F, A, stream)
+        kmax = max(kmax, ctx.debug_last().K)
+    n_g = g.n
+    ctx.reserve(cap, int(kmax * 1.05) + 4096, H, W)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(params)
+    torch.cuda.synchronize()
+    barrier()
+    assert not ctx.check_overflow(), "reserved tile-entry capacity overflowed"
+
+    # ---------------- timed region (device time, CUDA events on the launching stream)
+    if not args.no_stage_events:
+        ctx.profile(True)
+        ctx.profile_read(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(params)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    launches = int(sum_over_ranks(ctx.launches - launches0))
+    ms = max_over_ranks(ms_local)
+    prof = ctx.profile_read(reset=True) if not args.no_stage_events else None
+    ctx.profile(False)
+    overflow = ctx.check_overflow()
+    value = n_views * args.steps / (ms / 1e3)
+
+    line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "ms_per_view": ms / (args.steps * n_views),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded synthgen rig: ellipsoid upper body, log-normal scales, random rotations)",
+            "config": workload_config(n_g, kmax), "gpu_launches": launches, "clocks": clk,
+            "overflow": overflow}
+
+    # ---------------- roofline of the dominant kernel (rank 0's live stage events)
+    if prof is not None and rank == 0:
+        stages = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
+        line["stages_ms_per_call"] = {k: round(v, 4) for k, v in stages.items()}
+        share = {k: v[0] for k, v in prof.items()}
+        tot = sum(share.values())
+        line["stages_share"] = {k: round(v / tot, 4) for k, v in share.items()} if tot else {}
+        line["roofline"] = roofline(ctx, g, cams[0], outs[0], H, W, C_, stages, n_g, stream)
+
+    # ---------------- end to end through the C ABI with host buffers
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, ctx, g, views, keep, scene, cams, outs, H, W, C_, rank, world, stream,
+                          broadcast, max_over_ranks, sum_over_ranks, params, params_sync)
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        go = oracle.unproject(scene)
+        v, t, frac = cpu_baseline_value(go, targets[0])
+        line["cpu_baseline"] = {"value": v, "unit": "views/s", "cores": 1, "kind": "oracle",
+                                "sample": f"oracle/taoracle.c single-threaded on the central 256x256 window "
+                                          f"({frac:.4f} of the pixels) of c4 target 0: projection of all Gaussians + "
+                                          f"window tile lists + compositing, {t:.2f} s; value = fraction / seconds"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
+    """Algorithmic bytes / flops per launch over the live
+    per-launch time of each stage; the dominant stage is reported."""
+    import numpy as np
+    import torch
+    import paper_2405_14866_b200 as tb
+    from tests import _parity as P   # d2h helper only (no oracle use)
+    Ki, Ri = cam0
+    F, A = out0
+    pc = tb.default_params(flags=tb.TA_FLAG_DEBUG_COUNTS)
+    ctx.rasterize(g, -1, Ki, Ri, H, W, pc, F, A, stream)
+    torch.cuda.synchronize()
+    d = ctx.debug_last()
+    rec = P.d2h(d.records, 8 * d.n, np.uint32).reshape(-1, 8)
+    nvis = int(np.count_nonzero((rec[:, 6] & 0xffff) <= (rec[:, 6] >> 16)))
+    pairs = int(P.d2h(d.n_contrib, H * W, np.int32).astype(np.int64).sum())
+    K = int(d.K)
+    T = d.tiles_x * d.tiles_y
+    peaks, src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS))
+    mhz = float(peaks.get("sm_max_mhz", SM_CLOCK_MAX_MHZ))
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    fp32_tflops = sms * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
+    fb = 2 * C_
+    bytes_alg = {
+        "project": n_g * (48 + 32 + 8),
+        "sort": 16 * n_g * max(1, d.sort_passes),
+        "bin_count": 12 * nvis + 4 * T * d.P,
+        "bin_scan": 8 * T * d.P,
+        "bin_place": 12 * nvis + 4 * K + 4 * T * d.P,
+        "composite": 4 * K + nvis * (32 + fb) + 4 * H * W * (C_ + 1),
+    }
+    flops_comp = pairs * (2 * C_ + 12)
+    dom = max((k for k in bytes_alg), key=lambda k: stages.get(k, 0.0))
+    t = stages[dom] / 1e3
+    if dom == "composite":
+        hb = bytes_alg[dom] / t / 1e9
+        fl = flops_comp / t / 1e12
+        if fl / fp32_tflops >= hb / hbm:
+            r = {"bound": "alu", "achieved": fl, "peak": fp32_tflops, "unit": "TFLOP/s", "frac": fl / fp32_tflops,
+                 "peak_source": f"derived: {sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 x {mhz:.0f} MHz",
+                 "hbm_frac": hb / hbm}
+        else:
+            r = {"bound": "hbm", "achieved": hb, "peak": hbm, "unit": "GB/s", "frac": hb / hbm,
+                 "peak_source": src, "alu_frac": fl / fp32_tflops}
+    else:
+        hb = bytes_alg[dom] / t / 1e9
+        r = {"bound": "hbm", "achieved": hb, "peak": hbm, "unit": "GB/s", "frac": hb / hbm, "peak_source": src}
+    r.update({"kernel": dom, "traffic": None, "ms_per_launch": stages[dom],
+              "algorithmic_bytes_per_launch": bytes_alg[dom], "composited_pairs_per_view": pairs,
+              "visible_gaussians": nvis, "entries_per_view": K})
+    # whole-view roofline: all per-view algorithmic bytes vs the summed per-view stage time
+    view_ms = sum(v for k, v in stages.items() if k != "unproject")
+    b_view = n_g * 48 + nvis * fb + 16 * K + 4 * H * W * (C_ + 1)
+    r["view"] = {"ms": view_ms, "alg_bytes": b_view, "hbm_frac": b_view / (view_ms / 1e3) / 1e9 / hbm,
+                 "fp32_frac": flops_comp / (view_ms / 1e3) / 1e12 / fp32_tflops}
+    return r
+
+
+def e2e(args, ctx, g, views, keep, scene, cams, outs, H, W, C_, rank, world, stream, broadcast, max_over_ranks,
+        sum_over_ranks, params, params_sync):
+    """Same metric through the public API with HOST buffers: per step the source maps are copied
+    H2D from pinned memory and every rendered view (F + A) is copied D2H into pinned memory."""
+    import torch
+    h2d = 0
+    host_in = []
+    if rank == 0:
+        for dev_tensors in keep:
+            for t in dev_tensors:
+                if t is not None:
+                    host_in.append((t.cpu().pin_memory(), t))
+                    h2d += t.numel() * t.element_size()
+    host_out = [(torch.empty((H, W, C_), dtype=torch.float32).pin_memory(),
+                 torch.empty((H, W), dtype=torch.float32).pin_memory()) for _ in range(2)]
+    d2h = len(cams) * (H * W * C_ * 4 + H * W * 4)
+
+    def step():
+        for h, d in host_in:
+            d.copy_(h, non_blocking=True)
+        if rank == 0:
+            ctx.unproject(views, params_sync, g, stream)
+        broadcast()
+        for k, ((Ki, Ri), (F, A)) in enumerate(zip(cams, outs)):
+            ctx.rasterize(g, -1, Ki, Ri, H, W, params, F, A, stream)
+            hf, ha = host_out[k & 1]
+            hf.copy_(F, non_blocking=True)
+            ha.copy_(A, non_blocking=True)
+
+    steps = max(2, min(args.steps, 5))
+    step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    total_views = int(sum_over_ranks(len(cams)))
+    return {"value": total_views * steps / (ms / 1e3),
+            "unit": "views/s", "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
+            "d2h_bytes_per_step": int(sum_over_ranks(d2h)), "steps": steps,
+            "note": "source maps H2D from pinned host memory + ta_unproject + ta_rasterize + every view's "
+                    "F and A D2H into pinned host memory, per step"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--views", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stage-events", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

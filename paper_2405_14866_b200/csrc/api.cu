@@ -1,0 +1,568 @@
+// api.cu -- the C ABI of include/ta.h: validation, scratch management, kernel orchestration.
+#include <cmath>
+#include <cstdarg>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <algorithm>
+#include <vector>
+
+#include "../../include/ta.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace ta;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// Scans per rasterize call: depth-sort passes 0..3 use status regions / counters 0..3, the
+// tile-offset scan uses 4.
+constexpr int kScanSlots = 5;
+
+}  // namespace
+
+struct ta_context {
+    int device = 0;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    std::string err;
+    uint64_t launches = 0;
+    DevBuf cs, status, rec, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
+    uint64_t* pinned = nullptr;
+    uint32_t status_region = 0;   // words per scan slot
+    // last rasterize call
+    bool have_last = false;
+    int last_TX = 0, last_TY = 0, last_H = 0, last_W = 0;
+    uint32_t last_P = 0;
+    bool last_counts = false;
+    // stage profiling
+    bool profiling = false;
+    struct EvPair { cudaEvent_t a, b; int stage; };
+    std::vector<EvPair> pending, pool;
+    double prof_ms[TA_STAGE_COUNT] = {0};
+    uint64_t prof_calls[TA_STAGE_COUNT] = {0};
+};
+
+namespace {
+
+ta_status fail(ta_context* c, ta_status s, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return s;
+}
+
+ta_status cuda_fail(ta_context* c, cudaError_t e, const char* where) {
+    return fail(c, TA_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define TA_CUDA(ctx, expr)                                          \
+    do {                                                            \
+        cudaError_t _e = (expr);                                    \
+        if (_e != cudaSuccess) return cuda_fail((ctx), _e, #expr); \
+    } while (0)
+
+#define TA_LAUNCHED(ctx)                                                    \
+    do {                                                                    \
+        cudaError_t _e = cudaGetLastError();                                \
+        if (_e != cudaSuccess) return cuda_fail((ctx), _e, "kernel launch"); \
+        (ctx)->launches++;                                                  \
+    } while (0)
+
+ta_status grow(ta_context* c, DevBuf& b, size_t bytes) {
+    if (bytes <= b.bytes) return TA_OK;
+    if (b.p) {
+        cudaError_t e = cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        if (e != cudaSuccess) return cuda_fail(c, e, "cudaFree");
+    }
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        return fail(c, TA_ERR_OUT_OF_MEMORY, "cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
+    }
+    b.bytes = want;
+    return TA_OK;
+}
+
+bool finite_cam(const ta_intrinsics& K, const ta_extrinsics& RT, ta_context* c, ta_status* st) {
+    const float* v = &K.fx;
+    for (int i = 0; i < 4; i++)
+        if (!std::isfinite(v[i])) { *st = fail(c, TA_ERR_INVALID_ARG, "non-finite intrinsics"); return false; }
+    if (!(K.fx > 0.0f) || !(K.fy > 0.0f)) { *st = fail(c, TA_ERR_INVALID_ARG, "fx, fy must be > 0"); return false; }
+    for (int i = 0; i < 9; i++)
+        if (!std::isfinite(RT.R[i])) { *st = fail(c, TA_ERR_INVALID_ARG, "non-finite rotation"); return false; }
+    for (int i = 0; i < 3; i++)
+        if (!std::isfinite(RT.t[i])) { *st = fail(c, TA_ERR_INVALID_ARG, "non-finite translation"); return false; }
+    double worst = 0.0;
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) {
+            double d = 0.0;
+            for (int k = 0; k < 3; k++) d += (double)RT.R[i * 3 + k] * (double)RT.R[j * 3 + k];
+            worst = std::max(worst, std::fabs(d - (i == j ? 1.0 : 0.0)));
+        }
+    const float* R = RT.R;
+    const double det = (double)R[0] * ((double)R[4] * R[8] - (double)R[5] * R[7]) -
+                       (double)R[1] * ((double)R[3] * R[8] - (double)R[5] * R[6]) +
+                       (double)R[2] * ((double)R[3] * R[7] - (double)R[4] * R[6]);
+    if (worst > 1e-4 || det <= 0.0) {
+        *st = fail(c, TA_ERR_INVALID_ARG, "rotation not orthonormal (|R R^T - I| = %g, det %g)", worst, det);
+        return false;
+    }
+    return true;
+}
+
+bool supported_C(int C) { return C == 8 || C == 16 || C == 32 || C == 64; }
+
+// Stage timer: records an event pair around a stage when profiling is enabled.
+struct StageTimer {
+    ta_context* c;
+    cudaStream_t s;
+    ta_context::EvPair cur{};
+    bool on = false;
+    StageTimer(ta_context* c_, cudaStream_t s_) : c(c_), s(s_) {}
+    void begin(int stage) {
+        if (!c->profiling) return;
+        if (c->pool.empty()) {
+            ta_context::EvPair p{};
+            cudaEventCreate(&p.a);
+            cudaEventCreate(&p.b);
+            c->pool.push_back(p);
+        }
+        cur = c->pool.back();
+        c->pool.pop_back();
+        cur.stage = stage;
+        cudaEventRecord(cur.a, s);
+        on = true;
+    }
+    void end() {
+        if (!on) return;
+        cudaEventRecord(cur.b, s);
+        c->pending.push_back(cur);
+        on = false;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+void ta_default_params(ta_raster_params* p) {
+    if (!p) return;
+    p->dilation = 0.3f;
+    p->alpha_max = 0.99f;
+    p->alpha_min = 1.0f / 255.0f;
+    p->t_eps = 1e-4f;
+    p->cull_sigma = 3.0f;
+    p->z_near = 0.01f;
+    p->d_min = 0.0f;
+    p->default_scale = 0.0f;
+    p->default_opacity = 1.0f;
+    p->flags = 0u;
+}
+
+const char* ta_status_string(ta_status s) {
+    switch (s) {
+        case TA_OK: return "TA_OK";
+        case TA_ERR_INVALID_ARG: return "TA_ERR_INVALID_ARG";
+        case TA_ERR_UNSUPPORTED: return "TA_ERR_UNSUPPORTED";
+        case TA_ERR_CUDA: return "TA_ERR_CUDA";
+        case TA_ERR_OUT_OF_MEMORY: return "TA_ERR_OUT_OF_MEMORY";
+        case TA_ERR_CAPACITY: return "TA_ERR_CAPACITY";
+    }
+    return "TA_ERR_UNKNOWN";
+}
+
+const char* ta_last_error(const ta_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+const char* ta_build_info(void) {
+    return "taloha sm_100a (tcgen05-free SIMT compositing; look-back scans; warp-partition depth sort + binning)";
+}
+
+uint64_t ta_launch_count(const ta_context* ctx) { return ctx ? ctx->launches : 0; }
+
+ta_status ta_context_create(int32_t device, ta_context** out) {
+    if (!out) return TA_ERR_INVALID_ARG;
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) { cudaGetLastError(); return TA_ERR_CUDA; }
+    if (device < 0 || device >= ndev) return TA_ERR_INVALID_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return TA_ERR_CUDA;
+    ta_context* c = new ta_context();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    c->smem_optin = (size_t)optin;
+    ta_status st = grow(c, c->cs, sizeof(CallState));
+    if (st != TA_OK) { delete c; return st; }
+    if (cudaMemset(c->cs.p, 0, sizeof(CallState)) != cudaSuccess ||
+        cudaMallocHost(&c->pinned, 64) != cudaSuccess ||
+        cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess ||
+        cudaFuncSetAttribute(k_bin_place, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return TA_ERR_CUDA;
+    }
+    *out = c;
+    return TA_OK;
+}
+
+ta_status ta_context_destroy(ta_context* c) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
+                      &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto& p : c->pool) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    delete c;
+    return TA_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Binning geometry for an H x W target: tiles, difference-grid pitch, warps per block, P.
+ta_status bin_geometry(ta_context* c, int H, int W, BinGeom* bg, int* nwb) {
+    bg->TX = (W + kTile - 1) / kTile;
+    bg->TY = (H + kTile - 1) / kTile;
+    bg->GW = (bg->TX + 1) | 1;
+    bg->GS = (bg->TY + 1) * bg->GW;
+    const size_t per_warp = (size_t)bg->GS * 4;   // >= T*4 (k_bin_place's per-warp offsets)
+    const size_t budget = c->smem_optin > 4096 ? c->smem_optin - 1024 : 0;
+    int w = (int)std::min<size_t>(8, budget / per_warp);
+    if (w < 1) return fail(c, TA_ERR_UNSUPPORTED, "target of %d x %d tiles exceeds the binning shared-memory budget",
+                           bg->TX, bg->TY);
+    *nwb = w;
+    bg->P = (uint32_t)(c->num_sms * w);
+    return TA_OK;
+}
+
+ta_status reserve_gaussians(ta_context* c, int64_t cap) {
+    ta_status st;
+    const size_t n = (size_t)std::max<int64_t>(cap, 1);
+    if ((st = grow(c, c->rec, n * 32)) != TA_OK) return st;
+    if ((st = grow(c, c->keys0, n * 4)) != TA_OK) return st;
+    if ((st = grow(c, c->keys1, n * 4)) != TA_OK) return st;
+    if ((st = grow(c, c->vals0, n * 4)) != TA_OK) return st;
+    if ((st = grow(c, c->vals1, n * 4)) != TA_OK) return st;
+    const size_t parts = (n + kSortItemsPerWarp - 1) / kSortItemsPerWarp;
+    if ((st = grow(c, c->sort_hist, 256 * parts * 4 + 64)) != TA_OK) return st;
+    return TA_OK;
+}
+
+ta_status reserve_target(ta_context* c, const BinGeom& bg, int64_t cap) {
+    ta_status st;
+    const size_t T = (size_t)bg.TX * bg.TY;
+    const size_t bin_len = T * bg.P + 1;
+    if ((st = grow(c, c->bin_offs, bin_len * 4 + 64)) != TA_OK) return st;
+    const size_t parts = ((size_t)std::max<int64_t>(cap, 1) + kSortItemsPerWarp - 1) / kSortItemsPerWarp;
+    const uint32_t region = std::max(scan_tiles((uint32_t)(256 * parts)), scan_tiles((uint32_t)bin_len));
+    if (region > c->status_region || !c->status.p) {
+        if ((st = grow(c, c->status, (size_t)region * kScanSlots * 8)) != TA_OK) return st;
+        c->status_region = region;
+    }
+    return TA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, int32_t H, int32_t W) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (max_gaussians < 0 || max_entries < 0 || H <= 0 || W <= 0 || H > 32767 || W > 32767)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_reserve: bad sizes");
+    if (max_entries > 0xffffffffll) return fail(c, TA_ERR_CAPACITY, "more than 2^32-1 tile entries");
+    cudaSetDevice(c->device);
+    ta_status st;
+    if ((st = reserve_gaussians(c, max_gaussians)) != TA_OK) return st;
+    BinGeom bg;
+    int nwb;
+    if ((st = bin_geometry(c, H, W, &bg, &nwb)) != TA_OK) return st;
+    if ((st = reserve_target(c, bg, max_gaussians)) != TA_OK) return st;
+    if ((st = grow(c, c->list, (size_t)std::max<int64_t>(max_entries, 1) * 4)) != TA_OK) return st;
+    return TA_OK;
+}
+
+ta_status ta_unproject(ta_context* c, const ta_source_view* views, int32_t V, const ta_raster_params* p,
+                       ta_gaussians* out, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!views || !p || !out) return fail(c, TA_ERR_INVALID_ARG, "ta_unproject: NULL argument");
+    if (V < 1 || V > TA_MAX_VIEWS) return fail(c, TA_ERR_UNSUPPORTED, "ta_unproject: V = %d not in [1, %d]", V, TA_MAX_VIEWS);
+    if (!supported_C(out->C)) return fail(c, TA_ERR_UNSUPPORTED, "C = %d not in {8,16,32,64}", out->C);
+    if (out->feat_dtype != TA_F32 && out->feat_dtype != TA_F16) return fail(c, TA_ERR_UNSUPPORTED, "unknown dtype");
+    if (!out->pos_alpha || !out->cov || !out->feat || !out->n_dev)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_unproject: NULL output array");
+    if ((((uintptr_t)out->pos_alpha) | ((uintptr_t)out->cov) | ((uintptr_t)out->feat)) & 15)
+        return fail(c, TA_ERR_INVALID_ARG, "Gaussian arrays must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    ViewTable vt;
+    memset(&vt, 0, sizeof(vt));
+    vt.V = V;
+    vt.C = out->C;
+    vt.fbytes = out->feat_dtype == TA_F16 ? 2 : 4;
+    vt.d_min = p->d_min;
+    vt.default_scale = p->default_scale;
+    vt.default_opacity = p->default_opacity;
+    int64_t pixels = 0;
+    uint32_t blocks = 0;
+    for (int v = 0; v < V; v++) {
+        const ta_source_view& s = views[v];
+        if (s.H < 1 || s.W < 1 || s.H > 32767 || s.W > 32767)
+            return fail(c, TA_ERR_INVALID_ARG, "view %d: bad size %d x %d", v, s.H, s.W);
+        if (!s.disparity || !s.feat) return fail(c, TA_ERR_INVALID_ARG, "view %d: NULL disparity/feat", v);
+        if (!(s.baseline > 0.0f) || !std::isfinite(s.baseline))
+            return fail(c, TA_ERR_INVALID_ARG, "view %d: baseline must be > 0", v);
+        ta_status cst;
+        if (!finite_cam(s.K, s.RT, c, &cst)) return cst;
+        if (((uintptr_t)s.feat) & 15) return fail(c, TA_ERR_INVALID_ARG, "view %d: feat not 16-byte aligned", v);
+        ViewDesc& d = vt.v[v];
+        d.disp = s.disparity; d.mask = s.mask; d.scale = s.scale; d.quat = s.quat; d.opacity = s.opacity; d.feat = s.feat;
+        d.fx = s.K.fx; d.fy = s.K.fy; d.cx = s.K.cx; d.cy = s.K.cy;
+        memcpy(d.R, s.RT.R, sizeof(d.R));
+        memcpy(d.t, s.RT.t, sizeof(d.t));
+        d.baseline = s.baseline;
+        d.H = s.H; d.W = s.W;
+        d.blk_begin = blocks;
+        const int64_t HW = (int64_t)s.H * s.W;
+        const bool al = ((((uintptr_t)s.disparity) | ((uintptr_t)s.opacity) | ((uintptr_t)s.quat)) & 15) == 0 &&
+                        (((uintptr_t)s.mask) & 3) == 0;
+        d.vec4 = (HW % 4 == 0 && al) ? 1 : 0;
+        blocks += (uint32_t)((HW + kUnprojPix - 1) / kUnprojPix);
+        pixels += HW;
+    }
+    if (pixels > out->capacity)
+        return fail(c, TA_ERR_CAPACITY, "capacity %lld < %lld source pixels", (long long)out->capacity, (long long)pixels);
+    if (pixels >= (1ll << 31)) return fail(c, TA_ERR_CAPACITY, "more than 2^31 source pixels");
+    ta_status s2;
+    if ((s2 = grow(c, c->ucounts, ((size_t)blocks + 16) * 4)) != TA_OK) return s2;
+    const uint32_t tiles = scan_tiles(blocks);
+    if ((s2 = grow(c, c->ustatus, ((size_t)tiles + 8) * 8)) != TA_OK) return s2;
+    StageTimer tm(c, st);
+    tm.begin(TA_STAGE_UNPROJECT);
+    TA_CUDA(c, cudaMemsetAsync(c->ustatus.p, 0, ((size_t)tiles + 8) * 8, st));
+    k_unproject_count<<<blocks, kUnprojThreads, 0, st>>>(vt, (uint32_t*)c->ucounts.p);
+    TA_LAUNCHED(c);
+    unsigned long long* status = (unsigned long long*)c->ustatus.p;
+    launch_scan((uint32_t*)c->ucounts.p, nullptr, blocks, status, (uint32_t*)(status + tiles + 4),
+                (unsigned long long*)out->n_dev, st);
+    TA_LAUNCHED(c);
+    k_unproject_write<<<blocks, kUnprojThreads, 0, st>>>(vt, (const uint32_t*)c->ucounts.p, (float4*)out->pos_alpha,
+                                                         (float4*)out->cov, out->feat);
+    TA_LAUNCHED(c);
+    tm.end();
+    return TA_OK;
+}
+
+ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta_intrinsics* K,
+                       const ta_extrinsics* RT, int32_t H, int32_t W, const ta_raster_params* p, float* feat_out,
+                       float* alpha_out, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!g || !K || !RT || !p || !feat_out || !alpha_out) return fail(c, TA_ERR_INVALID_ARG, "ta_rasterize: NULL argument");
+    if (H < 1 || W < 1 || H > 32767 || W > 32767) return fail(c, TA_ERR_INVALID_ARG, "bad target size %d x %d", H, W);
+    if (!supported_C(g->C)) return fail(c, TA_ERR_UNSUPPORTED, "C = %d not in {8,16,32,64}", g->C);
+    if (g->feat_dtype != TA_F32 && g->feat_dtype != TA_F16) return fail(c, TA_ERR_UNSUPPORTED, "unknown dtype");
+    if (n < -1 || (n == -1 && !g->n_dev)) return fail(c, TA_ERR_INVALID_ARG, "n = -1 needs g->n_dev");
+    if (n > g->capacity) return fail(c, TA_ERR_INVALID_ARG, "n > capacity");
+    if (g->capacity >= (1ll << 31)) return fail(c, TA_ERR_CAPACITY, "capacity >= 2^31");
+    if ((n != 0) && (!g->pos_alpha || !g->cov || !g->feat)) return fail(c, TA_ERR_INVALID_ARG, "NULL Gaussian array");
+    if ((((uintptr_t)g->pos_alpha) | ((uintptr_t)g->cov) | ((uintptr_t)g->feat) | ((uintptr_t)feat_out)) & 15)
+        return fail(c, TA_ERR_INVALID_ARG, "Gaussian arrays / feat_out must be 16-byte aligned");
+    ta_status st;
+    if (!finite_cam(*K, *RT, c, &st)) return st;
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool async = (p->flags & TA_FLAG_ASYNC) != 0;
+    const bool counts = (p->flags & TA_FLAG_DEBUG_COUNTS) != 0;
+
+    BinGeom bg;
+    int nwb;
+    if ((st = bin_geometry(c, H, W, &bg, &nwb)) != TA_OK) return st;
+    const int64_t cap = n >= 0 ? n : g->capacity;
+    const int T = bg.TX * bg.TY;
+    const uint32_t bin_len = (uint32_t)T * bg.P + 1;
+    if (async) {
+        if (c->rec.bytes < (size_t)cap * 32 || c->bin_offs.bytes < (size_t)bin_len * 4 || !c->list.p)
+            return fail(c, TA_ERR_CAPACITY, "TA_FLAG_ASYNC needs ta_reserve() for this size first");
+    }
+    if ((st = reserve_gaussians(c, cap)) != TA_OK) return st;
+    if ((st = reserve_target(c, bg, cap)) != TA_OK) return st;
+    if (counts && (st = grow(c, c->ncontrib, (size_t)H * W * 4)) != TA_OK) return st;
+    if (!c->list.p && (st = grow(c, c->list, (size_t)std::max<int64_t>(cap, 1) * 16)) != TA_OK) return st;
+
+    TargetCam cam;
+    cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
+    memcpy(cam.R, RT->R, sizeof(cam.R));
+    memcpy(cam.t, RT->t, sizeof(cam.t));
+    cam.W = W; cam.H = H;
+    cam.Wm1f = (float)(W - 1);
+    cam.Hm1f = (float)(H - 1);
+    RasterConsts rc;
+    rc.dilation = p->dilation; rc.alpha_max = p->alpha_max; rc.alpha_min = p->alpha_min; rc.t_eps = p->t_eps;
+    rc.cull_sigma = p->cull_sigma; rc.z_near = p->z_near;
+    rc.q_max = p->cull_sigma * p->cull_sigma;
+
+    CallState* cs = (CallState*)c->cs.p;
+    unsigned long long* status = (unsigned long long*)c->status.p;
+    const uint32_t region = c->status_region;
+    const int n_status = (int)(region * kScanSlots);
+    uint32_t* k0 = (uint32_t*)c->keys0.p; uint32_t* k1 = (uint32_t*)c->keys1.p;
+    uint32_t* v0 = (uint32_t*)c->vals0.p; uint32_t* v1 = (uint32_t*)c->vals1.p;
+    uint32_t* hist = (uint32_t*)c->sort_hist.p;
+    uint32_t* offs = (uint32_t*)c->bin_offs.p;
+    uint4* rec = (uint4*)c->rec.p;
+
+    StageTimer tm(c, s);
+    tm.begin(TA_STAGE_PROJECT);
+    k_init<<<std::min(1024, (n_status + 255) / 256 + 1), 256, 0, s>>>(cs, status, n_status, n, g->n_dev, bin_len);
+    TA_LAUNCHED(c);
+    const int64_t cap_blocks = (cap + 255) / 256;
+    if (cap_blocks > 0) {
+        k_project<<<(unsigned)cap_blocks, 256, 0, s>>>((const float4*)g->pos_alpha, (const float4*)g->cov, cam, rc, cs,
+                                                       rec, k0, v0);
+        TA_LAUNCHED(c);
+    }
+    tm.end();
+    tm.begin(TA_STAGE_SORT);
+    const uint32_t parts_max = (uint32_t)((cap + kSortItemsPerWarp - 1) / kSortItemsPerWarp);
+    const uint32_t sort_blocks = (parts_max + kSortWarps - 1) / kSortWarps;
+    if (sort_blocks > 0) {
+        for (int pass = 0; pass < 4; pass++) {
+            k_sort_hist<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, pass, cs, hist);
+            TA_LAUNCHED(c);
+            launch_scan(hist, &cs->sort_len, 256 * parts_max, status + (size_t)pass * region, &cs->scan_counter[pass],
+                        &cs->sort_total, s);
+            TA_LAUNCHED(c);
+            k_sort_scatter<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs, hist);
+            TA_LAUNCHED(c);
+        }
+    }
+    tm.end();
+    const size_t smem_count = (size_t)nwb * bg.GS * 4;
+    const size_t smem_place = (size_t)nwb * T * 4;
+    tm.begin(TA_STAGE_BIN_COUNT);
+    k_bin_count<<<c->num_sms, nwb * 32, smem_count, s>>>(rec, v0, v1, cs, bg, offs);
+    TA_LAUNCHED(c);
+    tm.end();
+    tm.begin(TA_STAGE_BIN_SCAN);
+    launch_scan(offs, nullptr, bin_len, status + (size_t)4 * region, &cs->scan_counter[4], &cs->K, s);
+    TA_LAUNCHED(c);
+    if (!async) {
+        TA_CUDA(c, cudaMemcpyAsync(c->pinned, &cs->K, 8, cudaMemcpyDeviceToHost, s));
+        TA_CUDA(c, cudaStreamSynchronize(s));
+        const uint64_t Kh = c->pinned[0];
+        if (Kh > 0xffffffffull) return fail(c, TA_ERR_CAPACITY, "%llu tile entries exceed 2^32-1", (unsigned long long)Kh);
+        if (Kh * 4 > c->list.bytes && (st = grow(c, c->list, (size_t)(Kh + Kh / 8 + 1024) * 4)) != TA_OK) return st;
+    }
+    tm.end();
+    tm.begin(TA_STAGE_BIN_PLACE);
+    k_bin_place<<<c->num_sms, nwb * 32, smem_place, s>>>(rec, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
+                                                        (uint64_t)(c->list.bytes / 4));
+    TA_LAUNCHED(c);
+    tm.end();
+    tm.begin(TA_STAGE_COMPOSITE);
+    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, 0, rec, g->feat, (const uint32_t*)c->list.p,
+                                     offs, bg.P, bg.TX, W, H, rc, feat_out, alpha_out,
+                                     counts ? (int32_t*)c->ncontrib.p : nullptr, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "composite launch");
+    c->launches++;
+    tm.end();
+    c->have_last = true;
+    c->last_TX = bg.TX; c->last_TY = bg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;
+    c->last_counts = counts;
+    return TA_OK;
+}
+
+ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
+    if (!c || !out) return TA_ERR_INVALID_ARG;
+    if (!c->have_last) return fail(c, TA_ERR_INVALID_ARG, "no rasterize call yet");
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    CallState h;
+    TA_CUDA(c, cudaMemcpyAsync(&h, c->cs.p, sizeof(CallState), cudaMemcpyDeviceToHost, s));
+    TA_CUDA(c, cudaStreamSynchronize(s));
+    int passes = 0;
+    const uint32_t m = h.key_or ^ h.key_and;
+    if (h.n_visible && m) {
+        int lo = 0, hi = 31;
+        while (!((m >> lo) & 1u)) lo++;
+        while (!((m >> hi) & 1u)) hi--;
+        passes = (hi - lo) / 8 + 1;
+    }
+    out->n = h.n;
+    out->K = (int64_t)h.K;
+    out->P = (int32_t)c->last_P;
+    out->tiles_x = c->last_TX;
+    out->tiles_y = c->last_TY;
+    out->sort_passes = passes;
+    out->records = (const uint32_t*)c->rec.p;
+    out->depth_keys = (const uint32_t*)((passes & 1) ? c->keys1.p : c->keys0.p);
+    out->order = (const uint32_t*)((passes & 1) ? c->vals1.p : c->vals0.p);
+    out->tile_offsets = (const uint32_t*)c->bin_offs.p;
+    out->tile_list = (const uint32_t*)c->list.p;
+    out->n_contrib = c->last_counts ? (const int32_t*)c->ncontrib.p : nullptr;
+    return TA_OK;
+}
+
+ta_status ta_profile_enable(ta_context* c, int32_t enable) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    c->profiling = enable != 0;
+    return TA_OK;
+}
+
+ta_status ta_profile_read(ta_context* c, ta_profile* out, int32_t reset) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    TA_CUDA(c, cudaDeviceSynchronize());
+    for (auto& p : c->pending) {
+        float ms = 0.0f;
+        TA_CUDA(c, cudaEventElapsedTime(&ms, p.a, p.b));
+        c->prof_ms[p.stage] += ms;
+        c->prof_calls[p.stage] += 1;
+        c->pool.push_back(p);
+    }
+    c->pending.clear();
+    if (out) {
+        for (int i = 0; i < TA_STAGE_COUNT; i++) { out->ms[i] = c->prof_ms[i]; out->calls[i] = c->prof_calls[i]; }
+    }
+    if (reset) {
+        for (int i = 0; i < TA_STAGE_COUNT; i++) { c->prof_ms[i] = 0.0; c->prof_calls[i] = 0; }
+    }
+    return TA_OK;
+}
+
+ta_status ta_check_overflow(ta_context* c, void* stream, int32_t* overflowed) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    CallState h;
+    TA_CUDA(c, cudaMemcpyAsync(&h, c->cs.p, sizeof(CallState), cudaMemcpyDeviceToHost, s));
+    TA_CUDA(c, cudaStreamSynchronize(s));
+    const uint32_t zero = 0;
+    TA_CUDA(c, cudaMemcpy((char*)c->cs.p + offsetof(CallState, overflow), &zero, 4, cudaMemcpyHostToDevice));
+    if (overflowed) *overflowed = h.overflow ? 1 : 0;
+    return h.overflow ? fail(c, TA_ERR_CAPACITY, "tile-entry capacity overflowed in an async call") : TA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// common.cuh -- device-side building blocks shared by the rasterizer kernels (sm_100a).
+//
+// The fp32 arithmetic here is this library's own implementation of DESIGN.md "Normative
+// arithmetic": every rounding step is an explicit __f*_rn intrinsic so nvcc cannot contract
+// or reorder it; that is what makes tile lists, depth order and transmittance reproduce the
+// CPU oracle bit for bit (the oracle is a separate C file; the two share no code).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+namespace ta {
+
+constexpr int kTile = 16;
+constexpr uint32_t kCulledKey = 0xffffffffu;
+constexpr uint32_t kEmptyRect = 1u;     // x0 = 1, x1 = 0  -> empty box
+
+// ------------------------------------------------------------------ exact fp32 helpers
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
+
+// dot3(a, b) = fma(a2, b2, fma(a1, b1, a0*b0))
+__device__ __forceinline__ float dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
+    return ffma(a2, b2, ffma(a1, b1, fmul(a0, b0)));
+}
+
+// DESIGN.md R13 exp_det: exp(x), x <= 0, by a fixed fp32 sequence (Cody-Waite + degree-7 Taylor).
+__device__ __forceinline__ float exp_det(float x) {
+    x = fmaxf(x, -80.0f);
+    const float k = rintf(fmul(x, 1.44269502162933349609375f));
+    float r = ffma(-k, 0.693145751953125f, x);
+    r = ffma(-k, 1.428606765330187045037746429443359375e-06f, r);
+    float p = 1.98412698412698412698e-4f;
+    p = ffma(p, r, 1.38888888888888888889e-3f);
+    p = ffma(p, r, 8.33333333333333333333e-3f);
+    p = ffma(p, r, 4.16666666666666666667e-2f);
+    p = ffma(p, r, 1.66666666666666666667e-1f);
+    p = ffma(p, r, 0.5f);
+    p = ffma(p, r, 1.0f);
+    p = ffma(p, r, 1.0f);
+    const float s = __int_as_float(((int)k + 127) << 23);
+    return fmul(p, s);
+}
+
+// ------------------------------------------------------------------ memory-order helpers
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ------------------------------------------------------------------ per-call device state
+// One small struct of device scalars, reset by k_init at the start of every rasterize call.
+struct CallState {
+    unsigned long long K;          // tile entries (written by the bin-offset scan)
+    unsigned long long sort_total; // scratch totals of the sort scans
+    uint32_t n;                    // Gaussians of this call
+    uint32_t n_visible;
+    uint32_t key_or, key_and;      // OR / AND of visible depth keys -> varying bit range
+    uint32_t sort_parts;           // depth-sort partitions (warps): ceil(n / kSortItemsPerWarp)
+    uint32_t sort_len;             // 256 * sort_parts
+    uint32_t bin_len;              // T * P (+1 for the total)
+    uint32_t overflow;             // sticky: entries exceeded the list capacity (not reset by k_init)
+    uint32_t scan_counter[8];      // tile counters of the look-back scans (one per scan)
+};
+
+constexpr int kSortItemsPerWarp = 1024;   // depth sort: keys per warp partition
+constexpr int kSortWarps = 8;             // warps per block in the sort kernels
+
+// Number of LSD passes of 8 bits covering the varying bits of the visible depth keys.
+__device__ __forceinline__ int sort_passes(const CallState* cs) {
+    const uint32_t m = cs->key_or ^ cs->key_and;
+    if (cs->n_visible == 0 || m == 0) return 0;
+    const int lo = __ffs(m) - 1, hi = 31 - __clz(m);
+    return (hi - lo) / 8 + 1;
+}
+__device__ __forceinline__ int sort_shift(const CallState* cs, int pass) {
+    const uint32_t m = cs->key_or ^ cs->key_and;
+    return (__ffs(m) - 1) + 8 * pass;
+}
+
+}  // namespace ta

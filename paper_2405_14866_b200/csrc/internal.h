@@ -1,0 +1,84 @@
+// internal.h -- kernel parameter structs and kernel declarations shared by the .cu files.
+#pragma once
+#include <cstdint>
+#include "common.cuh"
+
+namespace ta {
+
+struct TargetCam {
+    float fx, fy, cx, cy;
+    float R[9];
+    float t[3];
+    int W, H;
+    float Wm1f, Hm1f;     // (float)(W-1), (float)(H-1): exact for W, H < 2^24
+};
+
+struct RasterConsts {
+    float dilation, alpha_max, alpha_min, t_eps, cull_sigma, z_near, q_max;
+};
+
+struct BinGeom {
+    int TX, TY;           // tiles per row / column
+    int GW, GS;           // difference-grid row pitch ((TX+1)|1) and size ((TY+1)*GW)
+    uint32_t P;           // binning partitions (warps)
+};
+
+struct ViewDesc {
+    const float* disp;
+    const uint8_t* mask;
+    const float* scale;
+    const float* quat;
+    const float* opacity;
+    const void* feat;
+    float fx, fy, cx, cy;
+    float R[9];
+    float t[3];
+    float baseline;
+    int H, W;
+    uint32_t blk_begin;   // first unprojection block of this view
+    int vec4;             // 1: H*W % 4 == 0 and all maps 16-byte aligned -> 128-bit loads
+};
+
+constexpr int kMaxViews = 16;
+struct ViewTable {
+    ViewDesc v[kMaxViews];
+    int V;
+    int C;
+    int fbytes;           // 2 (f16) or 4 (f32)
+    float d_min, default_scale, default_opacity;
+};
+
+constexpr int kUnprojThreads = 256;
+constexpr int kUnprojPix = 4 * kUnprojThreads;   // pixels per block
+
+// raster.cu
+__global__ void k_init(CallState* cs, unsigned long long* status, int n_status, int64_t n_host,
+                       const int64_t* n_dev, uint32_t bin_len);
+__global__ void k_project(const float4* pos_alpha, const float4* cov, TargetCam cam, RasterConsts rc,
+                          CallState* cs, uint4* rec, uint32_t* key0, uint32_t* val0);
+__global__ void k_sort_hist(const uint32_t* keys_a, const uint32_t* keys_b, int pass, const CallState* cs,
+                            uint32_t* hist);
+__global__ void k_sort_scatter(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int pass,
+                               const CallState* cs, const uint32_t* offs);
+__global__ void k_bin_count(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, const CallState* cs,
+                            BinGeom bg, uint32_t* counts);
+__global__ void k_bin_place(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, CallState* cs,
+                            BinGeom bg, const uint32_t* offs, uint32_t* list, uint64_t list_cap);
+
+// In-place exclusive scan of data[0 .. len) with len = *len_ptr (device) or len_max (len_ptr NULL);
+// status (>= len_max/4096 + 1 words) and *counter must be zero.
+void launch_scan(uint32_t* data, const uint32_t* len_ptr, uint32_t len_max, unsigned long long* status,
+                 uint32_t* counter, unsigned long long* total, cudaStream_t st);
+constexpr uint32_t scan_tiles(uint32_t len_max) { return len_max / 4096u + 1u; }
+
+// composite.cu
+cudaError_t launch_composite(int C, int fbytes, int tiles, int threads_smem_dummy, const uint4* rec,
+                             const void* feat, const uint32_t* list, const uint32_t* offs, uint32_t P, int TX,
+                             int W, int H, RasterConsts rc, float* F, float* A, int32_t* ncontrib,
+                             cudaStream_t st);
+
+// unproject.cu
+__global__ void k_unproject_count(ViewTable vt, uint32_t* counts);
+__global__ void k_unproject_write(ViewTable vt, const uint32_t* offs, float4* pos_alpha, float4* cov, void* feat);
+
+}  // namespace ta

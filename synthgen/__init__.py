@@ -283,3 +283,32 @@ def cam_arrays(cam: Camera):
 
 DEFAULT_PARAMS = dict(dilation=0.3, alpha_max=0.99, alpha_min=float(np.float32(1.0 / 255.0)),
                       t_eps=1e-4, cull_sigma=3.0, z_near=0.01, d_min=0.0)
+
+
+def make_targets(name: str, res: Optional[int] = None, target_hw: Optional[tuple] = None,
+                 n_targets: Optional[int] = None) -> List[Camera]:
+    """Target cameras of a config without synthesising the source maps (for ranks that only render)."""
+    if name == "c2":
+        r = res or 512
+        th, tw = target_hw or (r, r)
+        R, t = look_at([0.0, 0.0, 0.0], RIG_LOOK)
+        return [_pinhole(tw, th, FOCAL_SCALE, R, t)]
+    if name == "c3":
+        r = res or 1024
+        th, tw = target_hw or (r, r)
+        R, t = look_at(_arc_centre(), RIG_LOOK)
+        return [_pinhole(tw, th, FOCAL_SCALE, R, t)]
+    if name == "c4":
+        r = res or 1024
+        th, tw = target_hw or (r, r)
+        return _parallax_targets(n_targets or 32, tw, th)
+    if name == "c5":
+        r = res or 2048
+        th, tw = target_hw or (r, r)
+        return _parallax_targets(n_targets or 8, tw, th)
+    return make_config(name, res=res, target_hw=target_hw, n_targets=n_targets).targets
+
+
+def crop_camera(cam: Camera, x0: int, y0: int, w: int, h: int) -> Camera:
+    """The w x h window at (x0, y0) of `cam` as a camera of its own (same rays)."""
+    return Camera(fx=cam.fx, fy=cam.fy, cx=cam.cx - x0, cy=cam.cy - y0, R=cam.R, t=cam.t, H=h, W=w)

@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): tile lists and sort order bit-exact; features within 1e-4 absolute;
+alpha bit-exact (T/A decisions are taken in the same fp32 sequence on both sides).
+"""
+import numpy as np
+import pytest
+
+import synthgen as sg
+from tests import _parity as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    import paper_2405_14866_b200 as tb
+    assert torch.cuda.is_available()
+    tb.lib(build_if_stale=True)
+    return tb.Context(0)
+
+
+@pytest.fixture(scope="module")
+def oracle_lib():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def full_parity(ctx, O, scene, tidx=0, tiles=None, **pkw):
+    gp = P.gpu_params(scene, **pkw)
+    op = P.oracle_params(scene, **pkw)
+    g = P.gpu_unproject(ctx, scene, gp)
+    gh = P.gaussians_to_host(g)
+    go = O.unproject(scene, op)
+    P.check_unproject(gh, go)
+    cam = scene.targets[tidx]
+    out = P.gpu_rasterize(ctx, g, cam, gp)
+    K, R, t = sg.cam_arrays(cam)
+    pr = O.project(go, K, R, t, cam.H, cam.W, op)
+    P.check_project(out, pr, go["alpha"])
+    P.check_order(out, pr, go["ids"])
+    ranges, lst = O.tile_lists(pr, go["ids"], cam.H, cam.W)
+    P.check_lists(out, ranges, lst)
+    F, A, nc, _ = O.composite(go, pr, ranges, lst, cam.H, cam.W, op, tiles=tiles)
+    err = P.check_composite(out, F, A, nc, tiles=tiles, tx=(cam.W + 15) // 16)
+    return out, err
+
+
+def test_tiny_config(ctx, oracle_lib):
+    """configs[0] (Tiny) end to end: a1 .. a6."""
+    out, err = full_parity(ctx, oracle_lib, sg.make_config("tiny"))
+    assert out["K"] == 5400 and out["n"] == 4096
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_scenes(ctx, oracle_lib, seed):
+    """Random anisotropic scenes, ragged targets (not multiples of 16), C in {8,16,32,64}, f16/f32."""
+    C = (8, 16, 32, 64)[seed % 4]
+    dt = "f16" if seed % 2 else "f32"
+    s = sg.make_random_scene(seed, H=17 + 13 * seed, W=90 - 5 * seed, C=C, n_src=12 + 3 * seed, feat_dtype=dt)
+    full_parity(ctx, oracle_lib, s)
+
+
+def test_c2_full(ctx, oracle_lib):
+    """configs[1]: 2 x 512^2 sources, 512^2 target -- every stage, every pixel."""
+    full_parity(ctx, oracle_lib, sg.make_config("c2"))
+
+
+def test_c3_reduced_ragged(ctx, oracle_lib):
+    """configs[2] distributions at 256^2 sources, ragged 200 x 136 target."""
+    full_parity(ctx, oracle_lib, sg.make_config("c3", res=256, target_hw=(136, 200)))
+
+
+def test_c3_full_size_sampled_tiles(ctx, oracle_lib):
+    """configs[2] at full size (4 x 1024^2, ~1.67M Gaussians, 1024^2 target) in the launch
+    configuration bench.py times: a1-a5 bit-exact in full; a6 on sampled tiles incl. the longest lists."""
+    s = sg.make_config("c3")
+    cam = s.targets[0]
+    TX = (cam.W + 15) // 16
+    # tiles: the 8 longest lists + 24 seeded random non-empty tiles + the 4 corners
+    import oracle as O
+    op = P.oracle_params(s)
+    go = O.unproject(s, op)
+    K, R, t = sg.cam_arrays(cam)
+    pr = O.project(go, K, R, t, cam.H, cam.W, op)
+    ranges, _ = O.tile_lists(pr, go["ids"], cam.H, cam.W)
+    lens = ranges[:, 1].astype(np.int64) - ranges[:, 0]
+    nonempty = np.nonzero(lens)[0]
+    rng = np.random.default_rng(0)
+    tiles = np.unique(np.concatenate([np.argsort(lens)[-8:], rng.choice(nonempty, 24, replace=False),
+                                      [0, TX - 1, len(lens) - TX, len(lens) - 1]])).astype(np.int32)
+    out, err = full_parity(ctx, oracle_lib, s, tiles=tiles)
+    assert out["n"] == 1666464
+
+
+def test_c4_views_vs_single_view(ctx, oracle_lib):
+    """configs[3]: one Gaussian set, several parallax targets on one context; each equals the oracle
+    on sampled tiles (the 32-view batch at reduced source resolution)."""
+    s = sg.make_config("c4", res=256, target_hw=(256, 256), n_targets=5)
+    gp = P.gpu_params(s)
+    op = P.oracle_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    go = oracle_lib.unproject(s, op)
+    for cam in s.targets:
+        out = P.gpu_rasterize(ctx, g, cam, gp)
+        K, R, t = sg.cam_arrays(cam)
+        pr = oracle_lib.project(go, K, R, t, cam.H, cam.W, op)
+        ranges, lst = oracle_lib.tile_lists(pr, go["ids"], cam.H, cam.W)
+        P.check_lists(out, ranges, lst)
+        F, A, nc, _ = oracle_lib.composite(go, pr, ranges, lst, cam.H, cam.W, op)
+        P.check_composite(out, F, A, nc)
+
+
+def test_c5_stress_sampled_tiles(ctx, oracle_lib):
+    """configs[4] (4 x 2048^2, ~6.7M Gaussians, C = 64, 2048^2 target): a1 + a2 bit-exact in full,
+    a4 depth order, a3/a5 on sampled tiles via per-tile enumeration, a6 on the sampled tiles."""
+    s = sg.make_config("c5", n_targets=1)
+    gp = P.gpu_params(s)
+    op = P.oracle_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    gh = P.gaussians_to_host(g)
+    go = oracle_lib.unproject(s, op)
+    P.check_unproject(gh, go)
+    del gh
+    cam = s.targets[0]
+    out = P.gpu_rasterize(ctx, g, cam, gp)
+    K, R, t = sg.cam_arrays(cam)
+    pr = oracle_lib.project(go, K, R, t, cam.H, cam.W, op)
+    P.check_project(out, pr, go["alpha"])
+    P.check_order(out, pr, go["ids"])
+    TX = (cam.W + 15) // 16
+    vis = np.nonzero(pr["visible"])[0]
+    rect = pr["rect"][vis] >> 4
+    lens = out["ranges"][:, 1].astype(np.int64) - out["ranges"][:, 0]
+    rng = np.random.default_rng(1)
+    tiles = np.unique(np.concatenate([np.argsort(lens)[-3:], rng.choice(np.nonzero(lens)[0], 6, replace=False)]))
+    sub_ranges = np.zeros((len(lens), 2), np.uint32)
+    chunks, pos = [], 0
+    for tt in tiles:
+        ty, tx = divmod(int(tt), TX)
+        cov = vis[(rect[:, 0] <= tx) & (tx <= rect[:, 1]) & (rect[:, 2] <= ty) & (ty <= rect[:, 3])]
+        cov = cov[np.lexsort((go["ids"][cov], pr["dkey"][cov]))]
+        a, b = out["ranges"][tt]
+        assert np.array_equal(out["list"][a:b].astype(np.int64), cov)
+        sub_ranges[tt] = (pos, pos + len(cov))
+        chunks.append(cov)
+        pos += len(cov)
+    F, A, nc, _ = oracle_lib.composite(go, pr, sub_ranges, np.concatenate(chunks), cam.H, cam.W, op, tiles=tiles)
+    P.check_composite(out, F, A, nc, tiles=tiles, tx=TX)
+
+
+# ------------------------------------------------------------------ closed forms / properties on the GPU
+
+def test_identity_camera_reproduces_source(ctx):
+    """north_star closed form on the GPU: identity target, sigma = 0.05 px, alpha = 1 ->
+    F = fl(f * 0.99f), A = fl(1 - fl(1 - 0.99f)) bit-exactly."""
+    rng = np.random.default_rng(3)
+    H, W, f, B = 45, 61, 60.0, 0.1
+    cam = sg.Camera(fx=f, fy=f, cx=(W - 1) / 2, cy=(H - 1) / 2, R=np.eye(3), t=np.zeros(3), H=H, W=W)
+    d = rng.uniform(5, 15, (H, W)).astype(np.float32)
+    z = (np.float32(f) * np.float32(B)) / d
+    sc = (0.05 * z / f).astype(np.float32)
+    feat = rng.standard_normal((H, W, 16)).astype(np.float32)
+    v = sg.SourceView(cam=cam, baseline=B, disparity=d, mask=None, scale=np.repeat(sc[..., None], 3, -1), quat=None,
+                      opacity=np.ones((H, W), np.float32), feat=feat)
+    s = sg.Scene("ident", [v], [cam], 16, "f32")
+    gp = P.gpu_params(s, dilation=0.0)
+    g = P.gpu_unproject(ctx, s, gp)
+    out = P.gpu_rasterize(ctx, g, cam, gp)
+    a = np.float32(0.99)
+    assert np.array_equal(out["F"], feat * a)
+    assert np.all(out["A"] == np.float32(1.0) - (np.float32(1.0) - a))
+
+
+def test_permutation_invariance_and_determinism(ctx):
+    """Permuting the Gaussian arrays (ids travel) gives identical bits; repeated runs are bit-identical."""
+    import torch
+    s = sg.make_config("c2", res=128, target_hw=(112, 144))
+    gp = P.gpu_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    cam = s.targets[0]
+    a = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
+    b = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
+    assert np.array_equal(a["F"], b["F"]) and np.array_equal(a["A"], b["A"])
+    n = g.n
+    perm = torch.randperm(n, generator=torch.Generator().manual_seed(0)).cuda()
+    g.pos_alpha[:n] = g.pos_alpha[:n][perm].clone()
+    g.cov[:n] = g.cov[:n][perm].clone()
+    g.feat[:n] = g.feat[:n][perm].clone()
+    c = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
+    assert np.array_equal(a["F"], c["F"]) and np.array_equal(a["A"], c["A"])
+
+
+def test_empty_and_degenerate_inputs(ctx):
+    """Empty cloud, all culled (target looking away), n = 0: F = 0, A = 0 everywhere."""
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("tiny", res=32)
+    s.views[0].mask = np.zeros((32, 32), np.uint8)
+    gp = P.gpu_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    assert g.n == 0
+    out = P.gpu_rasterize(ctx, g, s.targets[0], gp)
+    assert np.all(out["F"] == 0) and np.all(out["A"] == 0) and out["K"] == 0
+    s = sg.make_config("tiny", res=32)
+    g = P.gpu_unproject(ctx, s, gp)
+    away = sg.Camera(fx=32.0, fy=32.0, cx=15.5, cy=15.5, R=sg.rot_y(180.0), t=np.zeros(3), H=40, W=24)
+    out = P.gpu_rasterize(ctx, g, away, gp)
+    assert np.all(out["F"] == 0) and np.all(out["A"] == 0)
+    out = P.gpu_rasterize(ctx, g, s.targets[0], gp, n=0)
+    assert np.all(out["F"] == 0) and np.all(out["A"] == 0)
+    torch.cuda.synchronize()
+
+
+def test_async_reserve_and_overflow(ctx):
+    """TA_FLAG_ASYNC after ta_reserve gives the same bits as a synchronous call; too small a
+    reservation is reported by ta_check_overflow (no silent truncation)."""
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("c2", res=128, target_hw=(128, 128))
+    gp = P.gpu_params(s, flags=0)
+    g = P.gpu_unproject(ctx, s, gp)
+    cam = s.targets[0]
+    ref = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
+    dbg = ctx.debug_last()
+    ctx2 = tb.Context(0)
+    ctx2.reserve(g.capacity, dbg.K, cam.H, cam.W)
+    ga = P.gpu_params(s, flags=tb.TA_FLAG_ASYNC)
+    out = P.gpu_rasterize(ctx2, g, cam, ga, debug=False)
+    assert not ctx2.check_overflow()
+    assert np.array_equal(out["F"], ref["F"]) and np.array_equal(out["A"], ref["A"])
+    ctx3 = tb.Context(0)
+    ctx3.reserve(g.capacity, dbg.K // 2, cam.H, cam.W)
+    P.gpu_rasterize(ctx3, g, cam, ga, debug=False)
+    assert ctx3.check_overflow()
+
+
+def test_invalid_arguments_are_rejected(ctx):
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("tiny", res=16)
+    gp = P.gpu_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    F = torch.empty((16, 16, 8), device="cuda")
+    A = torch.empty((16, 16), device="cuda")
+    bad_R = np.eye(3, dtype=np.float32).reshape(9) * 2
+    with pytest.raises(tb.TaError) as e:
+        ctx.rasterize(g, -1, tb.intrinsics((16, 16, 7.5, 7.5)), tb.extrinsics(bad_R, np.zeros(3)), 16, 16, gp, F, A)
+    assert e.value.status == 1
+    with pytest.raises(tb.TaError) as e:
+        ctx.rasterize(g, -1, tb.intrinsics((-1, 16, 7.5, 7.5)), tb.extrinsics(np.eye(3).reshape(9), np.zeros(3)),
+                      16, 16, gp, F, A)
+    assert e.value.status == 1
+    small = tb.GaussianBuffers(10, 8, "f32")
+    views, keep = tb.views_to_device(s.views)
+    with pytest.raises(tb.TaError) as e:
+        ctx.unproject(views, gp, small)
+    assert e.value.status == 5
+    odd = tb.GaussianBuffers(256, 12, "f32")
+    with pytest.raises(tb.TaError) as e:
+        ctx.unproject(views, gp, odd)
+    assert e.value.status == 2

@@ -175,7 +175,8 @@ def run_ours(args):
 
     n_views = args.views
     targets = sg.make_targets("c4", n_targets=n_views)
-    mine = list(range(rank * n_views // world, (rank + 1) * n_views // world))
+    from paper_2405_14866_b200 import dist as tdist
+    mine = tdist.shard(n_views, rank, world)
     ctx = tb.Context(local)
     C_, H, W = 32, 1024, 1024
     cap = 4 * 1024 * 1024
@@ -196,13 +197,8 @@ def run_ours(args):
              torch.empty((H, W), dtype=torch.float32, device=dev)) for _ in mine]
 
     def broadcast():
-        if world == 1:
-            return
-        dist.broadcast(g.n_dev, 0)
-        n = int(g.n_dev.item())
-        dist.broadcast(g.pos_alpha[:n], 0)
-        dist.broadcast(g.cov[:n], 0)
-        dist.broadcast(g.feat[:n], 0)
+        if world > 1:
+            tdist.broadcast_gaussians((g.pos_alpha, g.cov, g.feat), g.n_dev, src=0)
 
     def step(p):
         if rank == 0:
@@ -214,30 +210,23 @@ def run_ours(args):
     # sizing pass (synchronous): learn K per view, reserve for async steps
     step(params_sync)
     torch.cuda.synchronize()
-    kmax = 0
+    kmax = kcmax = 0
     for (Ki, Ri), (F, A) in zip(cams, outs):
         ctx.rasterize(g, -1, Ki, Ri, H, W, params_sync, F, A, stream)
-        kmax = max(kmax, ctx.debug_last().K)
+        d = ctx.debug_last()
+        kmax, kcmax = max(kmax, d.K), max(kcmax, d.Kc)
     n_g = g.n
-    ctx.reserve(cap, int(kmax * 1.05) + 4096, H, W)
+    ctx.reserve(cap, int(kcmax * 1.05) + 4096, H, W)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return tdist.reduce_scalar(x, "max", device=dev)
 
     def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return tdist.reduce_scalar(x, "sum", device=dev)
 
     for _ in range(args.warmup):
         step(params)
@@ -325,7 +314,8 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
     nvis = int(np.count_nonzero((rec[:, 6] & 0xffff) <= (rec[:, 6] >> 16)))
     pairs = int(P.d2h(d.n_contrib, H * W, np.int32).astype(np.int64).sum())
     K = int(d.K)
-    T = d.tiles_x * d.tiles_y
+    Kc = int(d.Kc)
+    NB = ((W + 31) // 32) * ((H + 31) // 32)
     peaks, src = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS))
     mhz = float(peaks.get("sm_max_mhz", SM_CLOCK_MAX_MHZ))
@@ -335,10 +325,10 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
     bytes_alg = {
         "project": n_g * (48 + 32 + 8),
         "sort": 16 * n_g * max(1, d.sort_passes),
-        "bin_count": 12 * nvis + 4 * T * d.P,
-        "bin_scan": 8 * T * d.P,
-        "bin_place": 12 * nvis + 4 * K + 4 * T * d.P,
-        "composite": 4 * K + nvis * (32 + fb) + 4 * H * W * (C_ + 1),
+        "bin_count": 12 * nvis + 4 * NB * d.P,
+        "bin_scan": 8 * NB * d.P,
+        "bin_place": 12 * nvis + 4 * Kc + 4 * NB * d.P,
+        "composite": 4 * Kc + nvis * (32 + fb) + 4 * H * W * (C_ + 1),
     }
     flops_comp = pairs * (2 * C_ + 12)
     dom = max((k for k in bytes_alg), key=lambda k: stages.get(k, 0.0))
@@ -358,7 +348,7 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
         r = {"bound": "hbm", "achieved": hb, "peak": hbm, "unit": "GB/s", "frac": hb / hbm, "peak_source": src}
     r.update({"kernel": dom, "traffic": None, "ms_per_launch": stages[dom],
               "algorithmic_bytes_per_launch": bytes_alg[dom], "composited_pairs_per_view": pairs,
-              "visible_gaussians": nvis, "entries_per_view": K})
+              "visible_gaussians": nvis, "entries_per_view": K, "coarse_entries_per_view": Kc})
     # whole-view roofline: all per-view algorithmic bytes vs the summed per-view stage time
     view_ms = sum(v for k, v in stages.items() if k != "unproject")
     b_view = n_g * 48 + nvis * fb + 16 * K + 4 * H * W * (C_ + 1)

@@ -124,8 +124,9 @@ void ta_default_params(ta_raster_params* p);
 ta_status ta_context_create(int32_t device, ta_context** out);
 ta_status ta_context_destroy(ta_context* ctx);
 
-/* Grow scratch for up to `max_gaussians` Gaussians, `max_entries` (tile, Gaussian) pairs and an
-   H x W target (synchronous: allocation).  Needed before TA_FLAG_ASYNC calls / graph capture. */
+/* Grow scratch for up to `max_gaussians` Gaussians, `max_entries` (32x32-pixel bin, Gaussian) pairs
+   (ta_debug_view.Kc of a representative call) and an H x W target (synchronous: allocation).
+   Needed before TA_FLAG_ASYNC calls / graph capture. */
 ta_status ta_reserve(ta_context* ctx, int64_t max_gaussians, int64_t max_entries, int32_t H, int32_t W);
 
 /*
@@ -158,13 +159,15 @@ ta_status ta_rasterize(ta_context* ctx, const ta_gaussians* g, int64_t n, const 
  *   depth_keys  [n] uint32 in depth-rank order: camera-space depth bits (0xffffffff when culled;
  *               culled Gaussians carry no tile entries, their rank positions are unspecified)
  *   order       [n] uint32: array index of the Gaussian of depth rank r
- *   tile_offsets [T*P + 1] uint32: list of tile t is tile_list[tile_offsets[t*P] .. tile_offsets[(t+1)*P])
- *   tile_list   [K] uint32 array indices ordered by (tile, depth, id)
+ *   tile_offsets [T + 1] uint32: list of tile t is tile_list[tile_offsets[t] .. tile_offsets[t+1])
+ *   tile_list   [K] uint32 array indices ordered by (tile, depth, id) -- the sequence the compositor
+ *               walks for each tile (its coarse 32x32 bin list filtered by the tile box), materialised
+ *               by this call (the hot path never writes per-tile lists)
  *   n_contrib   [H][W] int32 composited pairs per pixel (only with TA_FLAG_DEBUG_COUNTS)
  * The host fields (n, K, P, tiles_x, tiles_y, sort_passes) are filled by a synchronising read.
  */
 typedef struct {
-    int64_t n, K;
+    int64_t n, K, Kc;            /* Gaussians, (tile, Gaussian) entries, (32x32 bin, Gaussian) entries */
     int32_t P, tiles_x, tiles_y, sort_passes;
     const uint32_t* records;
     const uint32_t* depth_keys;

@@ -23,7 +23,7 @@ struct DevBuf {
 
 // Scans per rasterize call: depth-sort passes 0..3 use status regions / counters 0..3, the
 // tile-offset scan uses 4.
-constexpr int kScanSlots = 5;
+constexpr int kScanSlots = 6;   // + slot 5: debug tile-list scan
 
 }  // namespace
 
@@ -41,6 +41,8 @@ struct ta_context {
     int last_TX = 0, last_TY = 0, last_H = 0, last_W = 0;
     uint32_t last_P = 0;
     bool last_counts = false;
+    CompositeGeom last_cg{};
+    DevBuf dbg_offs, dbg_list;
     // stage profiling
     bool profiling = false;
     struct EvPair { cudaEvent_t a, b; int stage; };
@@ -227,7 +229,7 @@ ta_status ta_context_destroy(ta_context* c) {
     if (!c) return TA_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
-                      &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus};
+                      &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -241,20 +243,35 @@ ta_status ta_context_destroy(ta_context* c) {
 
 namespace {
 
-// Binning geometry for an H x W target: tiles, difference-grid pitch, warps per block, P.
+// Coarse-binning geometry for an H x W target: 32 x 32-pixel bins, difference-grid pitch,
+// warps per block (per-warp shared state must fit), P = partitions (warps).
 ta_status bin_geometry(ta_context* c, int H, int W, BinGeom* bg, int* nwb) {
-    bg->TX = (W + kTile - 1) / kTile;
-    bg->TY = (H + kTile - 1) / kTile;
+    bg->shift = kCoarseShift;
+    const int bs = 1 << kCoarseShift;
+    bg->TX = (W + bs - 1) / bs;
+    bg->TY = (H + bs - 1) / bs;
     bg->GW = (bg->TX + 1) | 1;
     bg->GS = (bg->TY + 1) * bg->GW;
-    const size_t per_warp = (size_t)bg->GS * 4;   // >= T*4 (k_bin_place's per-warp offsets)
+    const size_t per_warp = (size_t)std::max(bg->GS, bg->TX * bg->TY) * 4;
     const size_t budget = c->smem_optin > 4096 ? c->smem_optin - 1024 : 0;
-    int w = (int)std::min<size_t>(8, budget / per_warp);
-    if (w < 1) return fail(c, TA_ERR_UNSUPPORTED, "target of %d x %d tiles exceeds the binning shared-memory budget",
+    int w = (int)std::min<size_t>(16, budget / per_warp);
+    if (w < 1) return fail(c, TA_ERR_UNSUPPORTED, "target of %d x %d coarse bins exceeds the binning shared-memory budget",
                            bg->TX, bg->TY);
     *nwb = w;
     bg->P = (uint32_t)(c->num_sms * w);
     return TA_OK;
+}
+
+CompositeGeom composite_geometry(const BinGeom& bg, int H, int W) {
+    CompositeGeom cg;
+    cg.TX = (W + kTile - 1) / kTile;
+    cg.TY = (H + kTile - 1) / kTile;
+    cg.W = W;
+    cg.H = H;
+    cg.shift = bg.shift;
+    cg.BX = bg.TX;
+    cg.P = bg.P;
+    return cg;
 }
 
 ta_status reserve_gaussians(ta_context* c, int64_t cap) {
@@ -265,18 +282,20 @@ ta_status reserve_gaussians(ta_context* c, int64_t cap) {
     if ((st = grow(c, c->keys1, n * 4)) != TA_OK) return st;
     if ((st = grow(c, c->vals0, n * 4)) != TA_OK) return st;
     if ((st = grow(c, c->vals1, n * 4)) != TA_OK) return st;
-    const size_t parts = (n + kSortItemsPerWarp - 1) / kSortItemsPerWarp;
+    const size_t parts = (n + kSortKeysPerBlock - 1) / kSortKeysPerBlock;
     if ((st = grow(c, c->sort_hist, 256 * parts * 4 + 64)) != TA_OK) return st;
     return TA_OK;
 }
 
-ta_status reserve_target(ta_context* c, const BinGeom& bg, int64_t cap) {
+ta_status reserve_target(ta_context* c, const BinGeom& bg, int64_t cap, int H, int W) {
     ta_status st;
     const size_t T = (size_t)bg.TX * bg.TY;
     const size_t bin_len = T * bg.P + 1;
     if ((st = grow(c, c->bin_offs, bin_len * 4 + 64)) != TA_OK) return st;
-    const size_t parts = ((size_t)std::max<int64_t>(cap, 1) + kSortItemsPerWarp - 1) / kSortItemsPerWarp;
-    const uint32_t region = std::max(scan_tiles((uint32_t)(256 * parts)), scan_tiles((uint32_t)bin_len));
+    const size_t parts = ((size_t)std::max<int64_t>(cap, 1) + kSortKeysPerBlock - 1) / kSortKeysPerBlock;
+    const CompositeGeom cg = composite_geometry(bg, H, W);
+    const uint32_t region = std::max(std::max(scan_tiles((uint32_t)(256 * parts)), scan_tiles((uint32_t)bin_len)),
+                                     scan_tiles((uint32_t)(cg.TX * cg.TY) + 1));
     if (region > c->status_region || !c->status.p) {
         if ((st = grow(c, c->status, (size_t)region * kScanSlots * 8)) != TA_OK) return st;
         c->status_region = region;
@@ -299,7 +318,7 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     BinGeom bg;
     int nwb;
     if ((st = bin_geometry(c, H, W, &bg, &nwb)) != TA_OK) return st;
-    if ((st = reserve_target(c, bg, max_gaussians)) != TA_OK) return st;
+    if ((st = reserve_target(c, bg, max_gaussians, H, W)) != TA_OK) return st;
     if ((st = grow(c, c->list, (size_t)std::max<int64_t>(max_entries, 1) * 4)) != TA_OK) return st;
     return TA_OK;
 }
@@ -400,14 +419,16 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     int nwb;
     if ((st = bin_geometry(c, H, W, &bg, &nwb)) != TA_OK) return st;
     const int64_t cap = n >= 0 ? n : g->capacity;
-    const int T = bg.TX * bg.TY;
-    const uint32_t bin_len = (uint32_t)T * bg.P + 1;
+    const int NB = bg.TX * bg.TY;                      // coarse bins
+    const uint32_t bin_len = (uint32_t)NB * bg.P + 1;
+    const CompositeGeom cg = composite_geometry(bg, H, W);
+    const int T = cg.TX * cg.TY;                       // 16 x 16 tiles
     if (async) {
         if (c->rec.bytes < (size_t)cap * 32 || c->bin_offs.bytes < (size_t)bin_len * 4 || !c->list.p)
             return fail(c, TA_ERR_CAPACITY, "TA_FLAG_ASYNC needs ta_reserve() for this size first");
     }
     if ((st = reserve_gaussians(c, cap)) != TA_OK) return st;
-    if ((st = reserve_target(c, bg, cap)) != TA_OK) return st;
+    if ((st = reserve_target(c, bg, cap, H, W)) != TA_OK) return st;
     if (counts && (st = grow(c, c->ncontrib, (size_t)H * W * 4)) != TA_OK) return st;
     if (!c->list.p && (st = grow(c, c->list, (size_t)std::max<int64_t>(cap, 1) * 16)) != TA_OK) return st;
 
@@ -445,8 +466,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     }
     tm.end();
     tm.begin(TA_STAGE_SORT);
-    const uint32_t parts_max = (uint32_t)((cap + kSortItemsPerWarp - 1) / kSortItemsPerWarp);
-    const uint32_t sort_blocks = (parts_max + kSortWarps - 1) / kSortWarps;
+    const uint32_t parts_max = (uint32_t)((cap + kSortKeysPerBlock - 1) / kSortKeysPerBlock);
+    const uint32_t sort_blocks = parts_max;
     if (sort_blocks > 0) {
         for (int pass = 0; pass < 4; pass++) {
             k_sort_hist<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, pass, cs, hist);
@@ -460,7 +481,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     }
     tm.end();
     const size_t smem_count = (size_t)nwb * bg.GS * 4;
-    const size_t smem_place = (size_t)nwb * T * 4;
+    const size_t smem_place = (size_t)nwb * NB * 4;
     tm.begin(TA_STAGE_BIN_COUNT);
     k_bin_count<<<c->num_sms, nwb * 32, smem_count, s>>>(rec, v0, v1, cs, bg, offs);
     TA_LAUNCHED(c);
@@ -482,14 +503,15 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);
-    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, 0, rec, g->feat, (const uint32_t*)c->list.p,
-                                     offs, bg.P, bg.TX, W, H, rc, feat_out, alpha_out,
+    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, rec, g->feat, (const uint32_t*)c->list.p,
+                                     offs, cg, rc, cs, (uint64_t)(c->list.bytes / 4), feat_out, alpha_out,
                                      counts ? (int32_t*)c->ncontrib.p : nullptr, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "composite launch");
     c->launches++;
     tm.end();
     c->have_last = true;
-    c->last_TX = bg.TX; c->last_TY = bg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;
+    c->last_TX = cg.TX; c->last_TY = cg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;
+    c->last_cg = cg;
     c->last_counts = counts;
     return TA_OK;
 }
@@ -499,8 +521,27 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     if (!c->have_last) return fail(c, TA_ERR_INVALID_ARG, "no rasterize call yet");
     cudaSetDevice(c->device);
     cudaStream_t s = (cudaStream_t)stream;
+    CallState* cs = (CallState*)c->cs.p;
+    const CompositeGeom& cg = c->last_cg;
+    const int T = cg.TX * cg.TY;
+    ta_status st;
+    if ((st = grow(c, c->dbg_offs, ((size_t)T + 1) * 4 + 64)) != TA_OK) return st;
+    unsigned long long* status = (unsigned long long*)c->status.p + (size_t)5 * c->status_region;
+    if (scan_tiles((uint32_t)T + 1) > c->status_region) return fail(c, TA_ERR_CAPACITY, "debug scan status too small");
+    TA_CUDA(c, cudaMemsetAsync(status, 0, (size_t)c->status_region * 8, s));
+    TA_CUDA(c, cudaMemsetAsync(&cs->scan_counter[5], 0, 4, s));
+    launch_debug_tile_lists((const uint4*)c->rec.p, (const uint32_t*)c->list.p, (const uint32_t*)c->bin_offs.p, cg, cs,
+                            (uint32_t*)c->dbg_offs.p, status, &cs->scan_counter[5], &cs->sort_total, nullptr, 0, 0, s);
+    TA_CUDA(c, cudaGetLastError());
     CallState h;
     TA_CUDA(c, cudaMemcpyAsync(&h, c->cs.p, sizeof(CallState), cudaMemcpyDeviceToHost, s));
+    TA_CUDA(c, cudaStreamSynchronize(s));
+    const uint64_t K = h.sort_total;
+    if ((st = grow(c, c->dbg_list, (size_t)std::max<uint64_t>(K, 1) * 4)) != TA_OK) return st;
+    launch_debug_tile_lists((const uint4*)c->rec.p, (const uint32_t*)c->list.p, (const uint32_t*)c->bin_offs.p, cg, cs,
+                            (uint32_t*)c->dbg_offs.p, status, &cs->scan_counter[5], &cs->sort_total,
+                            (uint32_t*)c->dbg_list.p, K, 1, s);
+    TA_CUDA(c, cudaGetLastError());
     TA_CUDA(c, cudaStreamSynchronize(s));
     int passes = 0;
     const uint32_t m = h.key_or ^ h.key_and;
@@ -511,16 +552,17 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
         passes = (hi - lo) / 8 + 1;
     }
     out->n = h.n;
-    out->K = (int64_t)h.K;
+    out->K = (int64_t)K;
+    out->Kc = (int64_t)h.K;
     out->P = (int32_t)c->last_P;
-    out->tiles_x = c->last_TX;
-    out->tiles_y = c->last_TY;
+    out->tiles_x = cg.TX;
+    out->tiles_y = cg.TY;
     out->sort_passes = passes;
     out->records = (const uint32_t*)c->rec.p;
     out->depth_keys = (const uint32_t*)((passes & 1) ? c->keys1.p : c->keys0.p);
     out->order = (const uint32_t*)((passes & 1) ? c->vals1.p : c->vals0.p);
-    out->tile_offsets = (const uint32_t*)c->bin_offs.p;
-    out->tile_list = (const uint32_t*)c->list.p;
+    out->tile_offsets = (const uint32_t*)c->dbg_offs.p;
+    out->tile_list = (const uint32_t*)c->dbg_list.p;
     out->n_contrib = c->last_counts ? (const int32_t*)c->ncontrib.p : nullptr;
     return TA_OK;
 }

@@ -12,6 +12,7 @@
 namespace ta {
 
 constexpr int kTile = 16;
+constexpr int kCoarseShift = 5;        // coarse bins are 32 x 32 pixels (2 x 2 tiles)
 constexpr uint32_t kCulledKey = 0xffffffffu;
 constexpr uint32_t kEmptyRect = 1u;     // x0 = 1, x1 = 0  -> empty box
 
@@ -74,15 +75,16 @@ struct CallState {
     uint32_t n;                    // Gaussians of this call
     uint32_t n_visible;
     uint32_t key_or, key_and;      // OR / AND of visible depth keys -> varying bit range
-    uint32_t sort_parts;           // depth-sort partitions (warps): ceil(n / kSortItemsPerWarp)
+    uint32_t sort_parts;           // depth-sort partitions (blocks): ceil(n / kSortKeysPerBlock)
     uint32_t sort_len;             // 256 * sort_parts
     uint32_t bin_len;              // T * P (+1 for the total)
     uint32_t overflow;             // sticky: entries exceeded the list capacity (not reset by k_init)
     uint32_t scan_counter[8];      // tile counters of the look-back scans (one per scan)
 };
 
-constexpr int kSortItemsPerWarp = 1024;   // depth sort: keys per warp partition
-constexpr int kSortWarps = 8;             // warps per block in the sort kernels
+constexpr int kSortWarps = 8;                                  // warps per block in the sort kernels
+constexpr int kSortKeysPerWarp = 256;                          // depth sort: keys per warp
+constexpr int kSortKeysPerBlock = kSortWarps * kSortKeysPerWarp;   // keys per block (= partition)
 
 // Number of LSD passes of 8 bits covering the varying bits of the visible depth keys.
 __device__ __forceinline__ int sort_passes(const CallState* cs) {

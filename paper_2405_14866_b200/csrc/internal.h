@@ -18,7 +18,8 @@ struct RasterConsts {
 };
 
 struct BinGeom {
-    int TX, TY;           // tiles per row / column
+    int shift;            // bin = (1 << shift) x (1 << shift) pixels (coarse bins: 32 x 32)
+    int TX, TY;           // bins per row / column
     int GW, GS;           // difference-grid row pitch ((TX+1)|1) and size ((TY+1)*GW)
     uint32_t P;           // binning partitions (warps)
 };
@@ -72,9 +73,20 @@ void launch_scan(uint32_t* data, const uint32_t* len_ptr, uint32_t len_max, unsi
 constexpr uint32_t scan_tiles(uint32_t len_max) { return len_max / 4096u + 1u; }
 
 // composite.cu
-cudaError_t launch_composite(int C, int fbytes, int tiles, int threads_smem_dummy, const uint4* rec,
-                             const void* feat, const uint32_t* list, const uint32_t* offs, uint32_t P, int TX,
-                             int W, int H, RasterConsts rc, float* F, float* A, int32_t* ncontrib,
+struct CompositeGeom {
+    int TX, TY;           // 16 x 16 tiles per row / column
+    int W, H;
+    int shift, BX;        // coarse bins: (1 << shift) pixels square, BX per row
+    uint32_t P;           // coarse-binning partitions (columns of the bin-major offset matrix)
+};
+cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
+                             const uint32_t* list, const uint32_t* offs, CompositeGeom cg, RasterConsts rc,
+                             const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
+                             cudaStream_t st);
+// debug: materialise the per-tile (tile, depth, id) lists the compositor walks (a3/a5 check)
+void launch_debug_tile_lists(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
+                             const CallState* cs, uint32_t* tile_offs, unsigned long long* status, uint32_t* counter,
+                             unsigned long long* total, uint32_t* out_list, uint64_t out_cap, int pass,
                              cudaStream_t st);
 
 // unproject.cu

@@ -33,7 +33,7 @@ __global__ void k_init(CallState* __restrict__ cs, unsigned long long* __restric
         cs->n_visible = 0;
         cs->key_or = 0u;
         cs->key_and = 0xffffffffu;
-        cs->sort_parts = (uint32_t)((n + kSortItemsPerWarp - 1) / kSortItemsPerWarp);
+        cs->sort_parts = (uint32_t)((n + kSortKeysPerBlock - 1) / kSortKeysPerBlock);
         cs->sort_len = 256u * cs->sort_parts;
         cs->bin_len = bin_len;
         for (int k = 0; k < 8; k++) cs->scan_counter[k] = 0u;
@@ -135,7 +135,9 @@ __global__ void __launch_bounds__(256) k_project(const float4* __restrict__ pos_
 
 // ----------------------------------------------------------------------------- depth sort
 // Pass `pass` sorts by 8 bits starting at sort_shift(); keys/vals ping-pong a -> b -> a ...
-// Inactive passes (beyond the varying bits) return immediately.
+// Inactive passes (beyond the varying bits) return immediately.  A block owns kSortKeysPerBlock
+// consecutive keys, each warp kSortKeysPerWarp of them in order; warps rank their keys stably
+// (match.any per 32-key chunk, per-warp digit counters), the block combines warps in order.
 __global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* __restrict__ keys_a,
                                                                const uint32_t* __restrict__ keys_b, int pass,
                                                                const CallState* __restrict__ cs,
@@ -143,78 +145,91 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* _
     __shared__ uint32_t s_cnt[kSortWarps][256];
     if (pass >= sort_passes(cs)) return;
     const uint32_t parts = cs->sort_parts;
-    if (blockIdx.x * kSortWarps >= parts) return;
+    if (blockIdx.x >= parts) return;
     const uint32_t* src = (pass & 1) ? keys_b : keys_a;
     const int shift = sort_shift(cs, pass);
     const uint32_t n = cs->n;
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t part = blockIdx.x * kSortWarps + warp;
+    for (int k = threadIdx.x; k < kSortWarps * 256; k += blockDim.x) (&s_cnt[0][0])[k] = 0u;
+    __syncthreads();
     uint32_t* cnt = s_cnt[warp];
-    for (int d = lane; d < 256; d += 32) cnt[d] = 0u;
-    __syncwarp();
-    if (part < parts) {
-        const uint32_t b = part * kSortItemsPerWarp;
-        const uint32_t e = min(n, b + kSortItemsPerWarp);
-        for (uint32_t c = b; c < e; c += 32) {
-            const uint32_t idx = c + lane;
-            const bool ok = idx < e;
-            const uint32_t d = ok ? (src[idx] >> shift) & 255u : 256u + lane;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (ok && lane == (uint32_t)(__ffs(peers) - 1)) cnt[d] += __popc(peers);
-            __syncwarp();
-        }
+    const uint32_t b = blockIdx.x * kSortKeysPerBlock + warp * kSortKeysPerWarp;
+    const uint32_t e = min(n, b + kSortKeysPerWarp);
+    for (uint32_t c = b; c < e; c += 32) {
+        const uint32_t idx = c + lane;
+        const bool ok = idx < e;
+        const uint32_t d = ok ? (src[idx] >> shift) & 255u : 256u + lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (ok && lane == (uint32_t)(__ffs(peers) - 1)) cnt[d] += __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 256 * kSortWarps; k += blockDim.x) {
-        const int d = k / kSortWarps, w = k % kSortWarps;
-        const uint32_t p = blockIdx.x * kSortWarps + w;
-        if (p < parts) hist[(size_t)d * parts + p] = s_cnt[w][d];
-    }
+    const uint32_t d = threadIdx.x;
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; w++) sum += s_cnt[w][d];
+    hist[(size_t)d * parts + blockIdx.x] = sum;
 }
 
 __global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __restrict__ keys_a, uint32_t* __restrict__ keys_b,
                                                                   uint32_t* __restrict__ vals_a, uint32_t* __restrict__ vals_b,
                                                                   int pass, const CallState* __restrict__ cs,
                                                                   const uint32_t* __restrict__ offs) {
+    constexpr int kChunks = kSortKeysPerWarp / 32;
     __shared__ uint32_t s_off[kSortWarps][256];
     if (pass >= sort_passes(cs)) return;
     const uint32_t parts = cs->sort_parts;
-    if (blockIdx.x * kSortWarps >= parts) return;
+    if (blockIdx.x >= parts) return;
     const uint32_t* sk = (pass & 1) ? keys_b : keys_a;
     const uint32_t* sv = (pass & 1) ? vals_b : vals_a;
     uint32_t* dk = (pass & 1) ? keys_a : keys_b;
     uint32_t* dv = (pass & 1) ? vals_a : vals_b;
     const int shift = sort_shift(cs, pass);
     const uint32_t n = cs->n;
-    for (int k = threadIdx.x; k < 256 * kSortWarps; k += blockDim.x) {
-        const int d = k / kSortWarps, w = k % kSortWarps;
-        const uint32_t p = blockIdx.x * kSortWarps + w;
-        s_off[w][d] = p < parts ? offs[(size_t)d * parts + p] : 0u;
+    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+    for (int k = threadIdx.x; k < kSortWarps * 256; k += blockDim.x) (&s_off[0][0])[k] = 0u;
+    __syncthreads();
+    uint32_t* cnt = s_off[warp];
+    const uint32_t lt = lanemask_lt();
+    const uint32_t b = blockIdx.x * kSortKeysPerBlock + warp * kSortKeysPerWarp;
+    uint32_t key[kChunks], val[kChunks], rank[kChunks];
+#pragma unroll
+    for (int k = 0; k < kChunks; k++) {
+        const uint32_t idx = b + k * 32 + lane;
+        const bool ok = idx < n;
+        key[k] = ok ? sk[idx] : 0u;
+        val[k] = ok ? sv[idx] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kChunks; k++) {
+        const bool ok = b + k * 32 + lane < n;
+        const uint32_t d = ok ? (key[k] >> shift) & 255u : 256u + lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t base = ok ? cnt[d] : 0u;
+        __syncwarp();
+        rank[k] = base + __popc(peers & lt);
+        if (ok && lane == (uint32_t)(__ffs(peers) - 1)) cnt[d] = base + __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
-    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t part = blockIdx.x * kSortWarps + warp;
-    if (part >= parts) return;
-    uint32_t* off = s_off[warp];
-    const uint32_t lt = lanemask_lt();
-    const uint32_t b = part * kSortItemsPerWarp;
-    const uint32_t e = min(n, b + kSortItemsPerWarp);
-    for (uint32_t c = b; c < e; c += 32) {
-        const uint32_t idx = c + lane;
-        const bool ok = idx < e;
-        const uint32_t key = ok ? sk[idx] : 0u;
-        const uint32_t val = ok ? sv[idx] : 0u;
-        const uint32_t d = ok ? (key >> shift) & 255u : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t base = ok ? off[d] : 0u;
-        __syncwarp();
-        if (ok) {
-            const uint32_t pos = base + __popc(peers & lt);
-            dk[pos] = key;
-            dv[pos] = val;
-            if (lane == (uint32_t)(__ffs(peers) - 1)) off[d] = base + __popc(peers);
+    {   // per digit: warps in order after the block's global offset
+        const uint32_t d = threadIdx.x;
+        uint32_t run = offs[(size_t)d * parts + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < kSortWarps; w++) {
+            const uint32_t c = s_off[w][d];
+            s_off[w][d] = run;
+            run += c;
         }
-        __syncwarp();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kChunks; k++) {
+        if (b + k * 32 + lane < n) {
+            const uint32_t pos = cnt[(key[k] >> shift) & 255u] + rank[k];
+            dk[pos] = key[k];
+            dv[pos] = val[k];
+        }
     }
 }
 
@@ -232,7 +247,7 @@ __device__ __forceinline__ const uint32_t* sorted_vals(const CallState* cs, cons
 // Per-warp tile counts over depth ranks [rb, re): 2-D difference array on a (TY+1) x GW grid
 // (GW = (TX+1)|1, odd to spread banks), prefix-summed in place, then written tile-major
 // into counts[t * P + p].  The last element counts[T*P] is zeroed (it becomes K after the scan).
-__global__ void __launch_bounds__(256) k_bin_count(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
+__global__ void __launch_bounds__(512) k_bin_count(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
                                                    const uint32_t* __restrict__ vals_b,
                                                    const CallState* __restrict__ cs, BinGeom bg,
                                                    uint32_t* __restrict__ counts) {
@@ -258,7 +273,8 @@ __global__ void __launch_bounds__(256) k_bin_count(const uint4* __restrict__ rec
         }
         const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
         ok = ok && x0 <= x1 && y0 <= y1;
-        const int tx0 = x0 >> 4, tx1 = (x1 >> 4) + 1, ty0 = y0 >> 4, ty1 = (y1 >> 4) + 1;
+        const int sh = bg.shift;
+        const int tx0 = x0 >> sh, tx1 = (x1 >> sh) + 1, ty0 = y0 >> sh, ty1 = (y1 >> sh) + 1;
 #pragma unroll
         for (int corner = 0; corner < 4; corner++) {
             const int cy = (corner & 2) ? ty1 : ty0;
@@ -295,7 +311,7 @@ __global__ void __launch_bounds__(256) k_bin_count(const uint4* __restrict__ rec
 // Each warp appends its depth-rank range to the tile lists, in rank order.  32 consecutive
 // (Gaussian, tile) entries per step; same-tile entries inside a step are ordered by lane with
 // match.any, so each list stays ordered by (depth, id).
-__global__ void __launch_bounds__(256) k_bin_place(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
+__global__ void __launch_bounds__(512) k_bin_place(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
                                                    const uint32_t* __restrict__ vals_b,
                                                    CallState* __restrict__ cs, BinGeom bg,
                                                    const uint32_t* __restrict__ offs, uint32_t* __restrict__ list,
@@ -327,9 +343,10 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint4* __restrict__ rec
         }
         const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
         const bool ok = x0 <= x1 && y0 <= y1;
-        const int tx0 = x0 >> 4, ty0 = y0 >> 4;
-        const int tw = ok ? (x1 >> 4) - tx0 + 1 : 1;
-        const uint32_t cnt = ok ? (uint32_t)(tw * ((y1 >> 4) - ty0 + 1)) : 0u;
+        const int sh = bg.shift;
+        const int tx0 = x0 >> sh, ty0 = y0 >> sh;
+        const int tw = ok ? (x1 >> sh) - tx0 + 1 : 1;
+        const uint32_t cnt = ok ? (uint32_t)(tw * ((y1 >> sh) - ty0 + 1)) : 0u;
         uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

@@ -45,28 +45,40 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
     return warp_excl + x - v;
 }
 
-// Look-back: thread 0 of the block publishes its aggregate and returns the exclusive prefix of
-// all earlier tiles (the whole block must call it; the result is broadcast through smem).
+// Look-back (warp 0, 32 predecessors per step): publishes this tile's aggregate, sums the
+// aggregates of earlier tiles until one with an inclusive prefix is found, publishes the
+// inclusive prefix and returns the exclusive prefix to the whole block (broadcast via smem).
 __device__ __forceinline__ unsigned long long lookback_prefix(unsigned long long* status, uint32_t tile,
                                                               unsigned long long block_total,
                                                               unsigned long long* s_bcast) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
         unsigned long long prefix = 0;
         if (tile == 0) {
-            st_release_u64(&status[0], kFlagInc | block_total);
+            if (lane == 0) st_release_u64(&status[0], kFlagInc | block_total);
         } else {
-            st_relaxed_u64(&status[tile], kFlagAgg | block_total);
-            int p = (int)tile - 1;
+            if (lane == 0) st_relaxed_u64(&status[tile], kFlagAgg | block_total);
+            int p = (int)tile - 1 - (int)lane;
             while (true) {
-                unsigned long long s;
-                do { s = ld_acquire_u64(&status[p]); } while ((s >> 62) == 0);
-                prefix += s & kValMask;
-                if ((s & kFlagInc) != 0) break;
-                --p;
+                unsigned long long s = kFlagInc;       // before tile 0: inclusive prefix 0
+                if (p >= 0) {
+                    do { s = ld_acquire_u64(&status[p]); } while ((s >> 62) == 0);
+                }
+                const uint32_t inc = __ballot_sync(0xffffffffu, (s & kFlagInc) != 0);
+                unsigned long long v = s & kValMask;
+                if (inc) {
+                    const int f = __ffs(inc) - 1;      // nearest predecessor with an inclusive prefix
+                    if ((int)lane > f) v = 0;
+                }
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (inc) break;
+                p -= 32;
             }
-            st_release_u64(&status[tile], kFlagInc | (prefix + block_total));
+            if (lane == 0) st_release_u64(&status[tile], kFlagInc | (prefix + block_total));
         }
-        *s_bcast = prefix;
+        if (lane == 0) *s_bcast = prefix;
     }
     __syncthreads();
     return *s_bcast;

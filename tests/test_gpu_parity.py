@@ -225,13 +225,13 @@ def test_async_reserve_and_overflow(ctx):
     ref = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
     dbg = ctx.debug_last()
     ctx2 = tb.Context(0)
-    ctx2.reserve(g.capacity, dbg.K, cam.H, cam.W)
+    ctx2.reserve(g.capacity, dbg.Kc, cam.H, cam.W)
     ga = P.gpu_params(s, flags=tb.TA_FLAG_ASYNC)
     out = P.gpu_rasterize(ctx2, g, cam, ga, debug=False)
     assert not ctx2.check_overflow()
     assert np.array_equal(out["F"], ref["F"]) and np.array_equal(out["A"], ref["A"])
     ctx3 = tb.Context(0)
-    ctx3.reserve(g.capacity, dbg.K // 2, cam.H, cam.W)
+    ctx3.reserve(g.capacity, dbg.Kc // 2, cam.H, cam.W)
     P.gpu_rasterize(ctx3, g, cam, ga, debug=False)
     assert ctx3.check_overflow()
 

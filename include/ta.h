@@ -103,7 +103,7 @@ typedef struct {
     float alpha_max;             /* 0.99 clamp of alpha' (R9) */
     float alpha_min;             /* 1/255: alpha' below it is skipped (R9) */
     float t_eps;                 /* 1e-4: stop before T would drop below it (R10) */
-    float cull_sigma;            /* 3: q <= cull_sigma^2 and the cull_sigma-sigma box (R8) */
+    float cull_sigma;            /* 3: q <= cull_sigma^2 and the cull_sigma-sigma box (R8); (0, 12] */
     float z_near;                /* 0.01 m (R14) */
     float d_min;                 /* 0: lift iff d > d_min */
     float default_scale;         /* used when a view has no scale map */

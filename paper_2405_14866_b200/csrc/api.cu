@@ -408,6 +408,11 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     if ((n != 0) && (!g->pos_alpha || !g->cov || !g->feat)) return fail(c, TA_ERR_INVALID_ARG, "NULL Gaussian array");
     if ((((uintptr_t)g->pos_alpha) | ((uintptr_t)g->cov) | ((uintptr_t)g->feat) | ((uintptr_t)feat_out)) & 15)
         return fail(c, TA_ERR_INVALID_ARG, "Gaussian arrays / feat_out must be 16-byte aligned");
+    if (!(p->cull_sigma > 0.0f && p->cull_sigma <= 12.0f) || !(p->alpha_max > 0.0f && p->alpha_max < 1.0f) ||
+        !(p->t_eps > 0.0f && p->t_eps < 1.0f) || !(p->alpha_min >= 0.0f) || !(p->dilation >= 0.0f) ||
+        !std::isfinite(p->z_near))
+        return fail(c, TA_ERR_INVALID_ARG, "raster params out of range (0 < cull_sigma <= 12, 0 < alpha_max < 1, "
+                                           "0 < t_eps < 1, alpha_min >= 0, dilation >= 0)");
     ta_status st;
     if (!finite_cam(*K, *RT, c, &st)) return st;
     cudaSetDevice(c->device);

@@ -67,6 +67,18 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// Lanes of the warp whose 8-bit digit equals this lane's (warp multisplit with 8 ballots; no
+// match.any, which throttles the MIO pipe).  Lanes outside `valid` never count as peers.
+__device__ __forceinline__ uint32_t peers8(uint32_t d, uint32_t valid) {
+    uint32_t m = valid;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    return m;
+}
+
 // ------------------------------------------------------------------ per-call device state
 // One small struct of device scalars, reset by k_init at the start of every rasterize call.
 struct CallState {

@@ -87,234 +87,241 @@ __device__ __forceinline__ bool ellipse_may_touch(float mx, float my, float ca, 
     return best <= qlim;
 }
 
-// ------------------------------------------------------------------ mbarrier helpers (sm_90+)
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+// Packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): each component is one IEEE fp32
+// operation rounded to nearest -- the same result as the scalar __f*_rn sequence, two pixels per
+// instruction.
+typedef unsigned long long u64x;
+__device__ __forceinline__ u64x pk2(float2 a) { return *reinterpret_cast<const u64x*>(&a); }
+__device__ __forceinline__ float2 up2(u64x a) { return *reinterpret_cast<const float2*>(&a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    u64x r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return up2(r);
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(b))
-                 : "memory");
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    u64x r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return up2(r);
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(b)),
-        "r"(parity)
-        : "memory");
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    u64x r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return up2(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    u64x r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+    return up2(r);
+}
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
+
+// exp_det (R13) of two arguments at once; identical per component to exp_det() for
+// x >= -80 (the only arguments whose results are used: x = -q/2 with q <= q_max).
+__device__ __forceinline__ float2 exp_det2(float2 x) {
+    const float2 kf = mul2(x, bc2(1.44269502162933349609375f));
+    const float2 k = make_float2(rintf(kf.x), rintf(kf.y));
+    const float2 nk = make_float2(-k.x, -k.y);
+    float2 r = fma2(nk, bc2(0.693145751953125f), x);
+    r = fma2(nk, bc2(1.428606765330187045037746429443359375e-06f), r);
+    float2 p = bc2(1.98412698412698412698e-4f);
+    p = fma2(p, r, bc2(1.38888888888888888889e-3f));
+    p = fma2(p, r, bc2(8.33333333333333333333e-3f));
+    p = fma2(p, r, bc2(4.16666666666666666667e-2f));
+    p = fma2(p, r, bc2(1.66666666666666666667e-1f));
+    p = fma2(p, r, bc2(0.5f));
+    p = fma2(p, r, bc2(1.0f));
+    p = fma2(p, r, bc2(1.0f));
+    const float2 s = make_float2(__int_as_float(((int)k.x + 127) << 23), __int_as_float(((int)k.y + 127) << 23));
+    return mul2(p, s);
 }
 
-constexpr int kSlots = 6;          // ring depth
-constexpr int kSlotCoarse = 64;    // coarse-list entries scanned per slot (2 chunks of 32)
-constexpr int kSlotEntries = 64;   // capacity: Gaussians staged per slot
-constexpr int kConsumers = 8;      // consumer warps = 8x4-pixel blocks of the 16x16 tile
-constexpr int kProducers = 2;      // producer warps (slot k is filled by warp k % kProducers)
-constexpr int kCompositeThreads = 32 * (kConsumers + kProducers);
+constexpr int kWarps = 4;                        // warps per CTA = 8x8-pixel blocks of the 16x16 tile
+constexpr int kThreads = 32 * kWarps;
+constexpr int kBuf = 32;                         // entries staged per warp at a time
 
 template <int C>
-struct CompositeSmem {
+struct WarpBuf {
     static constexpr int CP = C + 4;   // padded fp32 feature row
-    float4 g[kSlots][kSlotEntries];    // mx, my, ca, cb2
-    float2 g2[kSlots][kSlotEntries];   // cc, alpha
-    uint2 rect[kSlots][kSlotEntries];  // x0|x1<<16, y0|y1<<16
-    float f[kSlots][kSlotEntries][CP];
-    uint64_t full[kSlots], empty[kSlots];
-    int cnt[kSlots];                   // entries staged in the slot
-    int ndone;                         // consumer warps whose 32 pixels all stopped
+    float4 g[kBuf];                    // mx, my, ca, cb2
+    float2 g2[kBuf];                   // cc, alpha
+    uint2 rect[kBuf];                  // x0|x1<<16, y0|y1<<16
+    float f[kBuf][CP];
 };
 
-// Warp-specialised compositing.  Producer warps walk the tile's coarse (32x32-bin) list in
-// depth order, 64 entries per slot, keep the Gaussians whose tile box covers this tile (the
-// tile's (tile, depth, id) list) and whose ellipse can reach the tile (conservative), and stage
-// their splat records + fp32 feature rows.  Consumer warps (8x4 pixels each) consume slots in
-// order without waiting on each other.  Every slot is produced and consumed (empty once all
-// pixels stopped), so no party can wait on a slot that never comes.
+// One CTA per 16x16 tile; warp w owns the 8x8 block (8*(w&1), 8*(w>>1)); lane l owns the two pixels
+// (l&7, l>>3) and (l&7, (l>>3)+4) of its block (same column: dx is shared, the rest is computed
+// for both pixels with packed fp32x2 instructions).  Warps are fully independent (no barrier):
+// each walks the tile's coarse (32x32-bin) list in depth order, keeps the entries whose tile box
+// covers this tile (= the tile's (tile, depth, id) list) and whose ellipse can reach its block
+// (conservative), stages up to 32 of them in a warp-private shared buffer (splat record + fp32
+// feature row) and composites them; the 4 warps of a tile share the list reads through L1.
 template <int C, typename FT>
-__global__ void __launch_bounds__(kCompositeThreads, (C >= 64 ? 1 : 2))
+__global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const uint32_t* __restrict__ clist,
             const uint32_t* __restrict__ coffs, CompositeGeom cg, RasterConsts rc, const CallState* __restrict__ cs,
             uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout, int32_t* __restrict__ ncontrib) {
-    using Smem = CompositeSmem<C>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+    WarpBuf<C>& bf = reinterpret_cast<WarpBuf<C>*>(smem_raw)[warp];
 
     const int tile = blockIdx.x;
     const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
-    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    // coarse bin of this tile and its (depth, id)-ordered Gaussian list
     const int sb = cg.shift - 4;
     const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
     const uint32_t cstart = coffs[(size_t)bin * cg.P];
     uint32_t cend = coffs[(size_t)(bin + 1) * cg.P];
     if (cend > list_cap) cend = (uint32_t)list_cap;   // overflowed async call: never read past the list
-    if (cend < cstart) cend = cstart;
-    const int nslots = (int)((cend - cstart + kSlotCoarse - 1) / kSlotCoarse);
     const uint32_t n = cs->n;
     const int W = cg.W, H = cg.H;
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kSlots; s++) {
-            mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.empty[s], kConsumers);
-        }
-        sm.ndone = 0;
-    }
-    __syncthreads();
-
-    if (warp >= kConsumers) {
-        // ------------------------------------------------------------ producers
-        const uint32_t pw = warp - kConsumers;
-        const uint32_t lt = lanemask_lt();
-        const float TX0 = (float)(txi * kTile), TX1 = TX0 + 15.0f, TY0 = (float)(tyi * kTile), TY1 = TY0 + 15.0f;
-        const float qlim = rc.q_max * 1.015625f + 0.01f;
-        for (int k = (int)pw; k < nslots; k += kProducers) {
-            const int s = k % kSlots;
-            if (k >= kSlots) mbar_wait(&sm.empty[s], ((k / kSlots) - 1) & 1);
-            int cnt = 0;
-            if (*(volatile int*)&sm.ndone < kConsumers) {
-                const uint32_t pos = cstart + (uint32_t)k * kSlotCoarse;
-                uint32_t idx[2];
-                uint4 r0[2], r1[2];
-                bool pass[2];
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const uint32_t e = pos + 32 * h + lane;
-                    idx[h] = e < cend ? clist[e] : 0xffffffffu;
-                }
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    pass[h] = idx[h] < n;                     // (>= n only after an overflow / past the end)
-                    const uint32_t i = pass[h] ? idx[h] : 0u;
-                    r0[h] = rec[2 * i];
-                    r1[h] = rec[2 * i + 1];
-                }
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const int x0 = (int)(r1[h].z & 0xffff), x1 = (int)(r1[h].z >> 16);
-                    const int y0 = (int)(r1[h].w & 0xffff), y1 = (int)(r1[h].w >> 16);
-                    pass[h] = pass[h] && x0 <= x1 && (x0 >> 4) <= txi && txi <= (x1 >> 4) && (y0 >> 4) <= tyi &&
-                              tyi <= (y1 >> 4) &&
-                              ellipse_may_touch(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y),
-                                                __uint_as_float(r0[h].z), __uint_as_float(r0[h].w),
-                                                __uint_as_float(r1[h].x), TX0, TX1, TY0, TY1, qlim);
-                }
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const uint32_t bal = __ballot_sync(0xffffffffu, pass[h]);
-                    if (pass[h]) {
-                        const int d = cnt + (int)__popc(bal & lt);
-                        sm.g[s][d] = make_float4(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y),
-                                                 __uint_as_float(r0[h].z), __uint_as_float(r0[h].w));
-                        sm.g2[s][d] = make_float2(__uint_as_float(r1[h].x), __uint_as_float(r1[h].y));
-                        sm.rect[s][d] = make_uint2(r1[h].z, r1[h].w);
-                        FeatLoad<FT>::template row<C>(feat + (size_t)idx[h] * C, &sm.f[s][d][0]);
-                    }
-                    cnt += __popc(bal);
-                }
-            }
-            if (lane == 0) sm.cnt[s] = cnt;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.full[s]);
-        }
-        return;
-    }
-
-    // ---------------------------------------------------------------- consumers
-    // warp w owns the 8x4 pixel block (8*(w&1), 4*(w>>1)) of the tile
-    const int bx0 = txi * kTile + 8 * (int)(warp & 1), by0 = tyi * kTile + 4 * (int)(warp >> 1);
-    const int px = bx0 + (int)(lane & 7), py = by0 + (int)(lane >> 3);
-    const float pxf = (float)px, pyf = (float)py;
+    const int bx0 = txi * kTile + 8 * (int)(warp & 1), by0 = tyi * kTile + 8 * (int)(warp >> 1);
+    const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
+    const float pxf = (float)px;
+    const float2 py2 = make_float2((float)pyA, (float)pyB);
     const float qlim = rc.q_max * 1.015625f + 0.01f;
-    const float X0 = (float)bx0, X1 = (float)(bx0 + 7), Y0 = (float)by0, Y1 = (float)(by0 + 3);
+    const float X0 = (float)bx0, X1 = (float)(bx0 + 7), Y0 = (float)by0, Y1 = (float)(by0 + 7);
+    const uint32_t lt = lanemask_lt();
 
-    float2 F[C / 2];
+    float2 FA[C / 2], FB[C / 2];
 #pragma unroll
-    for (int c = 0; c < C / 2; c++) F[c] = make_float2(0.0f, 0.0f);
-    float T = 1.0f;
-    int nc = 0;
-    bool done = (px >= W) || (py >= H);
-    bool warp_done = __all_sync(0xffffffffu, done);
-    if (warp_done && lane == 0) atomicAdd(&sm.ndone, 1);
+    for (int c = 0; c < C / 2; c++) { FA[c] = make_float2(0.0f, 0.0f); FB[c] = make_float2(0.0f, 0.0f); }
+    float2 T = make_float2(1.0f, 1.0f);
+    int ncA = 0, ncB = 0;
+    bool doneA = (px >= W) || (pyA >= H);
+    bool doneB = (px >= W) || (pyB >= H);
 
-    for (int k = 0; k < nslots; k++) {
-        const int s = k % kSlots;
-        mbar_wait(&sm.full[s], (k / kSlots) & 1);
-        const int ne = sm.cnt[s];
-        for (int g0 = 0; g0 < ne && !warp_done; g0 += 32) {
-            // lanes over entries: cull against this warp's block
+    uint32_t pos = cstart;
+    while (pos < cend && !__all_sync(0xffffffffu, doneA && doneB)) {
+        // ---- fill: up to kBuf entries of this warp, in list order
+        int cnt = 0;
+        uint32_t inbits = 0;
+        while (cnt < kBuf && pos < cend) {
+            const uint32_t e = pos + lane;
+            uint32_t idx = 0;
+            uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = make_uint4(0u, 0u, 0u, 0u);
             bool keep = false, inbox = false;
-            const int jl = g0 + (int)lane;
-            if (jl < ne) {
-                const float4 G = sm.g[s][jl];
-                const float cc = sm.g2[s][jl].x;
-                const uint2 rr = sm.rect[s][jl];
-                const int gx0 = (int)(rr.x & 0xffff), gx1 = (int)(rr.x >> 16);
-                const int gy0 = (int)(rr.y & 0xffff), gy1 = (int)(rr.y >> 16);
-                keep = gx0 <= bx0 + 7 && gx1 >= bx0 && gy0 <= by0 + 3 && gy1 >= by0 &&
-                       ellipse_may_touch(G.x, G.y, G.z, G.w, cc, X0, X1, Y0, Y1, qlim);
-                inbox = gx0 <= bx0 && gx1 >= bx0 + 7 && gy0 <= by0 && gy1 >= by0 + 3;
-            }
-            uint32_t bits = __ballot_sync(0xffffffffu, keep);
-            const uint32_t inbits = __ballot_sync(0xffffffffu, inbox);
-            while (bits) {
-                const int b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int j = g0 + b;
-                const float4 G = sm.g[s][j];
-                const float2 G2 = sm.g2[s][j];
-                if (!done) {
-                    bool inside = true;
-                    if (!((inbits >> b) & 1u)) {
-                        const uint2 rr = sm.rect[s][j];
-                        inside = px >= (int)(rr.x & 0xffff) && px <= (int)(rr.x >> 16) &&
-                                 py >= (int)(rr.y & 0xffff) && py <= (int)(rr.y >> 16);
-                    }
-                    if (inside) {
-                        const float dx = fsub(pxf, G.x), dy = fsub(pyf, G.y);
-                        const float q = ffma(ffma(G.z, dx, fmul(G.w, dy)), dx, fmul(fmul(G2.x, dy), dy));
-                        if (q <= rc.q_max) {
-                            const float e = exp_det(fmul(-0.5f, q));
-                            const float a = fminf(rc.alpha_max, fmul(G2.y, e));
-                            if (a >= rc.alpha_min) {
-                                const float Tn = fmul(T, fsub(1.0f, a));
-                                if (Tn < rc.t_eps) {
-                                    done = true;
-                                } else {
-                                    const float w = fmul(a, T);
-                                    const float4* fr = reinterpret_cast<const float4*>(&sm.f[s][j][0]);
-#pragma unroll
-                                    for (int c = 0; c < C / 4; c++) {
-                                        const float4 f4 = fr[c];
-                                        F[2 * c] = ffma2(make_float2(f4.x, f4.y), w, F[2 * c]);
-                                        F[2 * c + 1] = ffma2(make_float2(f4.z, f4.w), w, F[2 * c + 1]);
-                                    }
-                                    T = Tn;
-                                    nc++;
-                                }
-                            }
-                        }
+            if (e < cend) {
+                idx = clist[e];
+                if (idx < n) {
+                    r1 = rec[2 * idx + 1];
+                    const int gx0 = (int)(r1.z & 0xffff), gx1 = (int)(r1.z >> 16);
+                    const int gy0 = (int)(r1.w & 0xffff), gy1 = (int)(r1.w >> 16);
+                    keep = gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
+                           tyi <= (gy1 >> 4) && gx0 <= bx0 + 7 && gx1 >= bx0 && gy0 <= by0 + 7 && gy1 >= by0;
+                    if (keep) {
+                        r0 = rec[2 * idx];
+                        keep = ellipse_may_touch(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
+                                                 __uint_as_float(r0.w), __uint_as_float(r1.x), X0, X1, Y0, Y1, qlim);
+                        inbox = gx0 <= bx0 && gx1 >= bx0 + 7 && gy0 <= by0 && gy1 >= by0 + 7;
                     }
                 }
-                if (__all_sync(0xffffffffu, done)) {
-                    warp_done = true;
-                    if (lane == 0) atomicAdd(&sm.ndone, 1);
-                    break;
-                }
             }
+            uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            const int room = kBuf - cnt;
+            const uint32_t rank = __popc(bal & lt);
+            uint32_t adv = min(32u, cend - pos);
+            if (__popc(bal) > room) {                     // buffer full: resume at the first entry not taken
+                const uint32_t cut = __ballot_sync(0xffffffffu, keep && rank == (uint32_t)room);
+                const int cl = __ffs(cut) - 1;
+                bal &= (1u << cl) - 1u;
+                adv = (uint32_t)cl;
+                keep = keep && (int)lane < cl;
+            }
+            if (keep) {
+                const int d = cnt + (int)rank;
+                bf.g[d] = make_float4(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
+                                      __uint_as_float(r0.w));
+                bf.g2[d] = make_float2(__uint_as_float(r1.x), __uint_as_float(r1.y));
+                bf.rect[d] = make_uint2(r1.z, r1.w);
+                FeatLoad<FT>::template row<C>(feat + (size_t)idx * C, &bf.f[d][0]);
+            }
+            inbits |= __reduce_or_sync(0xffffffffu, (keep && inbox) ? (1u << (cnt + (int)rank)) : 0u);
+            cnt += __popc(bal);
+            pos += adv;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        // ---- composite the staged entries in order, two pixels per lane
+        for (int j = 0; j < cnt; j++) {
+            const float4 G = bf.g[j];
+            const float2 G2 = bf.g2[j];
+            bool inA = !doneA, inB = !doneB;
+            if (!((inbits >> j) & 1u)) {
+                const uint2 rr = bf.rect[j];
+                const bool inx = px >= (int)(rr.x & 0xffff) && px <= (int)(rr.x >> 16);
+                const int y0 = (int)(rr.y & 0xffff), y1 = (int)(rr.y >> 16);
+                inA = inA && inx && pyA >= y0 && pyA <= y1;
+                inB = inB && inx && pyB >= y0 && pyB <= y1;
+            }
+            // q = fma(fma(ca, dx, cb2*dy), dx, (cc*dy)*dy), both pixels
+            const float dx = fsub(pxf, G.x);
+            const float2 dy = sub2(py2, bc2(G.y));
+            const float2 t1 = mul2(bc2(G.w), dy);
+            const float2 t2 = fma2(bc2(G.z), bc2(dx), t1);
+            const float2 t4 = mul2(mul2(bc2(G2.x), dy), dy);
+            const float2 q = fma2(t2, bc2(dx), t4);
+            inA = inA && q.x <= rc.q_max;
+            inB = inB && q.y <= rc.q_max;
+            if (!__any_sync(0xffffffffu, inA || inB)) continue;
+            const float2 e = exp_det2(mul2(bc2(-0.5f), q));
+            const float2 ae = mul2(bc2(G2.y), e);
+            const float2 a = make_float2(fminf(rc.alpha_max, ae.x), fminf(rc.alpha_max, ae.y));
+            inA = inA && a.x >= rc.alpha_min;
+            inB = inB && a.y >= rc.alpha_min;
+            const float2 Tn = mul2(T, sub2(bc2(1.0f), a));
+            const bool stopA = inA && Tn.x < rc.t_eps, stopB = inB && Tn.y < rc.t_eps;
+            doneA = doneA || stopA;
+            doneB = doneB || stopB;
+            inA = inA && !stopA;
+            inB = inB && !stopB;
+            const float2 w = mul2(a, T);
+            const float wA = inA ? w.x : 0.0f, wB = inB ? w.y : 0.0f;   // weight 0: exact no-op FMA
+            const bool anyA = __any_sync(0xffffffffu, inA), anyB = __any_sync(0xffffffffu, inB);
+            const float4* fr = reinterpret_cast<const float4*>(&bf.f[j][0]);
+            if (anyA && anyB) {
+#pragma unroll
+                for (int c = 0; c < C / 4; c++) {
+                    const float4 f4 = fr[c];
+                    const float2 lo = make_float2(f4.x, f4.y), hi = make_float2(f4.z, f4.w);
+                    FA[2 * c] = ffma2(lo, wA, FA[2 * c]);
+                    FA[2 * c + 1] = ffma2(hi, wA, FA[2 * c + 1]);
+                    FB[2 * c] = ffma2(lo, wB, FB[2 * c]);
+                    FB[2 * c + 1] = ffma2(hi, wB, FB[2 * c + 1]);
+                }
+            } else if (anyA) {
+#pragma unroll
+                for (int c = 0; c < C / 4; c++) {
+                    const float4 f4 = fr[c];
+                    FA[2 * c] = ffma2(make_float2(f4.x, f4.y), wA, FA[2 * c]);
+                    FA[2 * c + 1] = ffma2(make_float2(f4.z, f4.w), wA, FA[2 * c + 1]);
+                }
+            } else if (anyB) {
+#pragma unroll
+                for (int c = 0; c < C / 4; c++) {
+                    const float4 f4 = fr[c];
+                    FB[2 * c] = ffma2(make_float2(f4.x, f4.y), wB, FB[2 * c]);
+                    FB[2 * c + 1] = ffma2(make_float2(f4.z, f4.w), wB, FB[2 * c + 1]);
+                }
+            }
+            T = make_float2(inA ? Tn.x : T.x, inB ? Tn.y : T.y);
+            ncA += inA ? 1 : 0;
+            ncB += inB ? 1 : 0;
+            if (__all_sync(0xffffffffu, doneA && doneB)) break;
+        }
+        __syncwarp();
     }
 
-    if (px < W && py < H) {
-        const size_t pix = (size_t)py * W + px;
-        float4* out = reinterpret_cast<float4*>(Fout + pix * C);
 #pragma unroll
-        for (int c = 0; c < C / 4; c++) out[c] = make_float4(F[2 * c].x, F[2 * c].y, F[2 * c + 1].x, F[2 * c + 1].y);
-        Aout[pix] = fsub(1.0f, T);
-        if (ncontrib) ncontrib[pix] = nc;
+    for (int h = 0; h < 2; h++) {
+        const int py = h ? pyB : pyA;
+        if (px < W && py < H) {
+            const size_t pix = (size_t)py * W + px;
+            float4* out = reinterpret_cast<float4*>(Fout + pix * C);
+            const float2* Fp = h ? FB : FA;
+#pragma unroll
+            for (int c = 0; c < C / 4; c++) out[c] = make_float4(Fp[2 * c].x, Fp[2 * c].y, Fp[2 * c + 1].x, Fp[2 * c + 1].y);
+            Aout[pix] = fsub(1.0f, h ? T.y : T.x);
+            if (ncontrib) ncontrib[pix] = h ? ncB : ncA;
+        }
     }
 }
 
@@ -322,7 +329,7 @@ template <int C, typename FT>
 static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, const uint32_t* list,
                               const uint32_t* offs, CompositeGeom cg, RasterConsts rc, const CallState* cs,
                               uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
-    const size_t smem = sizeof(CompositeSmem<C>);
+    const size_t smem = sizeof(WarpBuf<C>) * kWarps;
     static bool attr_set = false;   // per template instance; set once per process
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_composite<C, FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -331,7 +338,7 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
         attr_set = true;
     }
     if (tiles == 0) return cudaSuccess;
-    k_composite<C, FT><<<tiles, kCompositeThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg,
+    k_composite<C, FT><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg,
                                                                    rc, cs, list_cap, F, A, ncontrib);
     return cudaGetLastError();
 }

@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* _
     for (uint32_t c = b; c < e; c += 32) {
         const uint32_t idx = c + lane;
         const bool ok = idx < e;
-        const uint32_t d = ok ? (src[idx] >> shift) & 255u : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = ok ? (src[idx] >> shift) & 255u : 0u;
+        const uint32_t peers = peers8(d, __ballot_sync(0xffffffffu, ok));
         if (ok && lane == (uint32_t)(__ffs(peers) - 1)) cnt[d] += __popc(peers);
         __syncwarp();
     }
@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __re
 #pragma unroll
     for (int k = 0; k < kChunks; k++) {
         const bool ok = b + k * 32 + lane < n;
-        const uint32_t d = ok ? (key[k] >> shift) & 255u : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = ok ? (key[k] >> shift) & 255u : 0u;
+        const uint32_t peers = peers8(d, __ballot_sync(0xffffffffu, ok));
         const uint32_t base = ok ? cnt[d] : 0u;
         __syncwarp();
         rank[k] = base + __popc(peers & lt);

@@ -48,5 +48,6 @@ def summary(path):
             print("   top stall reasons (pc sampling):", ", ".join(f"{k.split('stalled_')[-1]}={f / tot:.2f}" for f, k in vv[:7]))
 
 
-for p in sys.argv[1:]:
-    summary(p)
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        summary(p)

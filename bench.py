@@ -346,7 +346,17 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
     else:
         hb = bytes_alg[dom] / t / 1e9
         r = {"bound": "hbm", "achieved": hb, "peak": hbm, "unit": "GB/s", "frac": hb / hbm, "peak_source": src}
-    r.update({"kernel": dom, "traffic": None, "ms_per_launch": stages[dom],
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        kname = {"project": "k_project", "bin_count": "k_bin_count", "bin_place": "k_bin_place",
+                 "composite": "k_composite", "sort": "k_sort_scatter"}.get(dom)
+        if kname in tj:
+            traffic = tj[kname]["dram_bytes"]
+            r["traffic_source"] = "profiles/traffic.json <- " + tj[kname]["source"] + " (ncu --set full, one launch)"
+    except Exception:
+        pass
+    r.update({"kernel": dom, "traffic": traffic, "ms_per_launch": stages[dom],
               "algorithmic_bytes_per_launch": bytes_alg[dom], "composited_pairs_per_view": pairs,
               "visible_gaussians": nvis, "entries_per_view": K, "coarse_entries_per_view": Kc})
     # whole-view roofline: all per-view algorithmic bytes vs the summed per-view stage time

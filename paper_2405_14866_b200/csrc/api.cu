@@ -33,7 +33,7 @@ struct ta_context {
     size_t smem_optin = 0;
     std::string err;
     uint64_t launches = 0;
-    DevBuf cs, status, rec, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
+    DevBuf cs, status, rec, boxes, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
     // last rasterize call
@@ -228,7 +228,7 @@ ta_status ta_context_create(int32_t device, ta_context** out) {
 ta_status ta_context_destroy(ta_context* c) {
     if (!c) return TA_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
+    DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->boxes, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
                       &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
@@ -278,6 +278,7 @@ ta_status reserve_gaussians(ta_context* c, int64_t cap) {
     ta_status st;
     const size_t n = (size_t)std::max<int64_t>(cap, 1);
     if ((st = grow(c, c->rec, n * 32)) != TA_OK) return st;
+    if ((st = grow(c, c->boxes, n * 8)) != TA_OK) return st;
     if ((st = grow(c, c->keys0, n * 4)) != TA_OK) return st;
     if ((st = grow(c, c->keys1, n * 4)) != TA_OK) return st;
     if ((st = grow(c, c->vals0, n * 4)) != TA_OK) return st;
@@ -488,7 +489,11 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const size_t smem_count = (size_t)nwb * bg.GS * 4;
     const size_t smem_place = (size_t)nwb * NB * 4;
     tm.begin(TA_STAGE_BIN_COUNT);
-    k_bin_count<<<c->num_sms, nwb * 32, smem_count, s>>>(rec, v0, v1, cs, bg, offs);
+    if (cap_blocks > 0) {
+        k_gather_boxes<<<(unsigned)cap_blocks, 256, 0, s>>>(rec, v0, v1, cs, (uint2*)c->boxes.p);
+        TA_LAUNCHED(c);
+    }
+    k_bin_count<<<c->num_sms, nwb * 32, smem_count, s>>>((const uint2*)c->boxes.p, cs, bg, offs);
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_BIN_SCAN);
@@ -503,7 +508,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     }
     tm.end();
     tm.begin(TA_STAGE_BIN_PLACE);
-    k_bin_place<<<c->num_sms, nwb * 32, smem_place, s>>>(rec, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
+    k_bin_place<<<c->num_sms, nwb * 32, smem_place, s>>>((const uint2*)c->boxes.p, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
                                                         (uint64_t)(c->list.bytes / 4));
     TA_LAUNCHED(c);
     tm.end();

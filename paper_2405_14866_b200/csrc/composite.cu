@@ -118,8 +118,12 @@ __device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
 // exp_det (R13) of two arguments at once; identical per component to exp_det() for
 // x >= -80 (the only arguments whose results are used: x = -q/2 with q <= q_max).
 __device__ __forceinline__ float2 exp_det2(float2 x) {
-    const float2 kf = mul2(x, bc2(1.44269502162933349609375f));
-    const float2 k = make_float2(rintf(kf.x), rintf(kf.y));
+    // k = rint(x*log2e) without FRND/F2I: adding 1.5*2^23 rounds y = x*log2e to the nearest integer
+    // (ties to even, |y| < 2^22) exactly like rintf, the difference recovers it as a float and the
+    // low mantissa bits hold it as an integer.
+    constexpr float kMagic = 12582912.0f;                  // 1.5 * 2^23
+    const float2 t = add2(mul2(x, bc2(1.44269502162933349609375f)), bc2(kMagic));
+    const float2 k = sub2(t, bc2(kMagic));
     const float2 nk = make_float2(-k.x, -k.y);
     float2 r = fma2(nk, bc2(0.693145751953125f), x);
     r = fma2(nk, bc2(1.428606765330187045037746429443359375e-06f), r);
@@ -131,7 +135,8 @@ __device__ __forceinline__ float2 exp_det2(float2 x) {
     p = fma2(p, r, bc2(0.5f));
     p = fma2(p, r, bc2(1.0f));
     p = fma2(p, r, bc2(1.0f));
-    const float2 s = make_float2(__int_as_float(((int)k.x + 127) << 23), __int_as_float(((int)k.y + 127) << 23));
+    const int kx = __float_as_int(t.x) - 0x4b400000, ky = __float_as_int(t.y) - 0x4b400000;
+    const float2 s = make_float2(__int_as_float((kx + 127) << 23), __int_as_float((ky + 127) << 23));
     return mul2(p, s);
 }
 
@@ -144,9 +149,21 @@ struct WarpBuf {
     static constexpr int CP = C + 4;   // padded fp32 feature row
     float4 g[kBuf];                    // mx, my, ca, cb2
     float2 g2[kBuf];                   // cc, alpha
-    uint2 rect[kBuf];                  // x0|x1<<16, y0|y1<<16
+    uint2 bm[kBuf];                    // lanes whose pixel A / pixel B lies inside the pixel box
     float f[kBuf][CP];
 };
+
+// Lanes of an 8x8 block (lane l: column l&7, row l>>3 (+4 for pixel B)) whose pixel lies inside the
+// box [gx0,gx1]x[gy0,gy1]; computed once per staged entry instead of once per pixel.
+__device__ __forceinline__ uint32_t box_lane_mask(int gx0, int gx1, int gy0, int gy1, int bx0, int ry) {
+    const int cx0 = max(gx0 - bx0, 0), cx1 = min(gx1 - bx0, 7);
+    const int ry0 = max(gy0 - ry, 0), ry1 = min(gy1 - ry, 3);
+    if (cx0 > cx1 || ry0 > ry1) return 0u;
+    const uint32_t col = (0xffu >> (7 - cx1)) & (0xffu << cx0);
+    const int span = 8 * (ry1 - ry0 + 1);
+    const uint32_t rows = (span >= 32 ? 0xffffffffu : ((1u << span) - 1u)) << (8 * ry0);
+    return rows & (col * 0x01010101u);
+}
 
 // One CTA per 16x16 tile; warp w owns the 8x8 block (8*(w&1), 8*(w>>1)); lane l owns the two pixels
 // (l&7, l>>3) and (l&7, (l>>3)+4) of its block (same column: dx is shared, the rest is computed
@@ -155,7 +172,7 @@ struct WarpBuf {
 // covers this tile (= the tile's (tile, depth, id) list) and whose ellipse can reach its block
 // (conservative), stages up to 32 of them in a warp-private shared buffer (splat record + fp32
 // feature row) and composites them; the 4 warps of a tile share the list reads through L1.
-template <int C, typename FT>
+template <int C, typename FT, bool kCounts>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const uint32_t* __restrict__ clist,
             const uint32_t* __restrict__ coffs, CompositeGeom cg, RasterConsts rc, const CallState* __restrict__ cs,
@@ -192,51 +209,66 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
 
     uint32_t pos = cstart;
     while (pos < cend && !__all_sync(0xffffffffu, doneA && doneB)) {
-        // ---- fill: up to kBuf entries of this warp, in list order
+        // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries (two independent
+        //      32-entry chunks) per round trip
         int cnt = 0;
-        uint32_t inbits = 0;
         while (cnt < kBuf && pos < cend) {
-            const uint32_t e = pos + lane;
-            uint32_t idx = 0;
-            uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = make_uint4(0u, 0u, 0u, 0u);
-            bool keep = false, inbox = false;
-            if (e < cend) {
-                idx = clist[e];
-                if (idx < n) {
-                    r1 = rec[2 * idx + 1];
-                    const int gx0 = (int)(r1.z & 0xffff), gx1 = (int)(r1.z >> 16);
-                    const int gy0 = (int)(r1.w & 0xffff), gy1 = (int)(r1.w >> 16);
-                    keep = gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
-                           tyi <= (gy1 >> 4) && gx0 <= bx0 + 7 && gx1 >= bx0 && gy0 <= by0 + 7 && gy1 >= by0;
-                    if (keep) {
-                        r0 = rec[2 * idx];
-                        keep = ellipse_may_touch(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
-                                                 __uint_as_float(r0.w), __uint_as_float(r1.x), X0, X1, Y0, Y1, qlim);
-                        inbox = gx0 <= bx0 && gx1 >= bx0 + 7 && gy0 <= by0 && gy1 >= by0 + 7;
-                    }
+            uint32_t idx[2];
+            uint4 r0[2], r1[2];
+            bool keep[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t e = pos + 32 * h + lane;
+                idx[h] = e < cend ? clist[e] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t i = idx[h] < n ? idx[h] : 0u;
+                r0[h] = rec[2 * i];
+                r1[h] = rec[2 * i + 1];
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int gx0 = (int)(r1[h].z & 0xffff), gx1 = (int)(r1[h].z >> 16);
+                const int gy0 = (int)(r1[h].w & 0xffff), gy1 = (int)(r1[h].w >> 16);
+                keep[h] = idx[h] < n && gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
+                          tyi <= (gy1 >> 4) && gx0 <= bx0 + 7 && gx1 >= bx0 && gy0 <= by0 + 7 && gy1 >= by0 &&
+                          ellipse_may_touch(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y), __uint_as_float(r0[h].z),
+                                            __uint_as_float(r0[h].w), __uint_as_float(r1[h].x), X0, X1, Y0, Y1, qlim);
+            }
+            uint32_t adv = 0;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if (cnt >= kBuf) break;                   // warp-uniform
+                const uint32_t base = pos + 32 * h;
+                if (base >= cend) break;
+                bool kp = keep[h];
+                uint32_t bal = __ballot_sync(0xffffffffu, kp);
+                const int room = kBuf - cnt;
+                const uint32_t rank = __popc(bal & lt);
+                uint32_t step = min(32u, cend - base);
+                if (__popc(bal) > room) {                 // buffer full: resume at the first entry not taken
+                    const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
+                    const int cl = __ffs(cut) - 1;
+                    bal &= (1u << cl) - 1u;
+                    step = (uint32_t)cl;
+                    kp = kp && (int)lane < cl;
                 }
+                if (kp) {
+                    const int d = cnt + (int)rank;
+                    bf.g[d] = make_float4(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y), __uint_as_float(r0[h].z),
+                                          __uint_as_float(r0[h].w));
+                    bf.g2[d] = make_float2(__uint_as_float(r1[h].x), __uint_as_float(r1[h].y));
+                    const int gx0 = (int)(r1[h].z & 0xffff), gx1 = (int)(r1[h].z >> 16);
+                    const int gy0 = (int)(r1[h].w & 0xffff), gy1 = (int)(r1[h].w >> 16);
+                    bf.bm[d] = make_uint2(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0),
+                                          box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4));
+                    FeatLoad<FT>::template row<C>(feat + (size_t)idx[h] * C, &bf.f[d][0]);
+                }
+                cnt += __popc(bal);
+                adv += step;
+                if (step < 32u) break;                     // partial chunk: the next round resumes here
             }
-            uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            const int room = kBuf - cnt;
-            const uint32_t rank = __popc(bal & lt);
-            uint32_t adv = min(32u, cend - pos);
-            if (__popc(bal) > room) {                     // buffer full: resume at the first entry not taken
-                const uint32_t cut = __ballot_sync(0xffffffffu, keep && rank == (uint32_t)room);
-                const int cl = __ffs(cut) - 1;
-                bal &= (1u << cl) - 1u;
-                adv = (uint32_t)cl;
-                keep = keep && (int)lane < cl;
-            }
-            if (keep) {
-                const int d = cnt + (int)rank;
-                bf.g[d] = make_float4(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
-                                      __uint_as_float(r0.w));
-                bf.g2[d] = make_float2(__uint_as_float(r1.x), __uint_as_float(r1.y));
-                bf.rect[d] = make_uint2(r1.z, r1.w);
-                FeatLoad<FT>::template row<C>(feat + (size_t)idx * C, &bf.f[d][0]);
-            }
-            inbits |= __reduce_or_sync(0xffffffffu, (keep && inbox) ? (1u << (cnt + (int)rank)) : 0u);
-            cnt += __popc(bal);
             pos += adv;
         }
         __syncwarp();
@@ -244,14 +276,8 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
         for (int j = 0; j < cnt; j++) {
             const float4 G = bf.g[j];
             const float2 G2 = bf.g2[j];
-            bool inA = !doneA, inB = !doneB;
-            if (!((inbits >> j) & 1u)) {
-                const uint2 rr = bf.rect[j];
-                const bool inx = px >= (int)(rr.x & 0xffff) && px <= (int)(rr.x >> 16);
-                const int y0 = (int)(rr.y & 0xffff), y1 = (int)(rr.y >> 16);
-                inA = inA && inx && pyA >= y0 && pyA <= y1;
-                inB = inB && inx && pyB >= y0 && pyB <= y1;
-            }
+            const uint2 bm = bf.bm[j];
+            bool inA = !doneA && ((bm.x >> lane) & 1u), inB = !doneB && ((bm.y >> lane) & 1u);
             // q = fma(fma(ca, dx, cb2*dy), dx, (cc*dy)*dy), both pixels
             const float dx = fsub(pxf, G.x);
             const float2 dy = sub2(py2, bc2(G.y));
@@ -303,8 +329,10 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
                 }
             }
             T = make_float2(inA ? Tn.x : T.x, inB ? Tn.y : T.y);
-            ncA += inA ? 1 : 0;
-            ncB += inB ? 1 : 0;
+            if (kCounts) {
+                ncA += inA ? 1 : 0;
+                ncB += inB ? 1 : 0;
+            }
             if (__all_sync(0xffffffffu, doneA && doneB)) break;
         }
         __syncwarp();
@@ -320,7 +348,7 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
 #pragma unroll
             for (int c = 0; c < C / 4; c++) out[c] = make_float4(Fp[2 * c].x, Fp[2 * c].y, Fp[2 * c + 1].x, Fp[2 * c + 1].y);
             Aout[pix] = fsub(1.0f, h ? T.y : T.x);
-            if (ncontrib) ncontrib[pix] = h ? ncB : ncA;
+            if (kCounts) ncontrib[pix] = h ? ncB : ncA;
         }
     }
 }
@@ -332,14 +360,20 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
     const size_t smem = sizeof(WarpBuf<C>) * kWarps;
     static bool attr_set = false;   // per template instance; set once per process
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_composite<C, FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_composite<C, FT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_composite<C, FT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     if (tiles == 0) return cudaSuccess;
-    k_composite<C, FT><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg,
-                                                                   rc, cs, list_cap, F, A, ncontrib);
+    if (ncontrib)
+        k_composite<C, FT, true><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg, rc, cs,
+                                                               list_cap, F, A, ncontrib);
+    else
+        k_composite<C, FT, false><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg, rc,
+                                                                cs, list_cap, F, A, ncontrib);
     return cudaGetLastError();
 }
 

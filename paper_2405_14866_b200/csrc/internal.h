@@ -61,9 +61,10 @@ __global__ void k_sort_hist(const uint32_t* keys_a, const uint32_t* keys_b, int 
                             uint32_t* hist);
 __global__ void k_sort_scatter(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int pass,
                                const CallState* cs, const uint32_t* offs);
-__global__ void k_bin_count(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, const CallState* cs,
-                            BinGeom bg, uint32_t* counts);
-__global__ void k_bin_place(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, CallState* cs,
+__global__ void k_gather_boxes(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, const CallState* cs,
+                               uint2* boxes);
+__global__ void k_bin_count(const uint2* boxes, const CallState* cs, BinGeom bg, uint32_t* counts);
+__global__ void k_bin_place(const uint2* boxes, const uint32_t* vals_a, const uint32_t* vals_b, CallState* cs,
                             BinGeom bg, const uint32_t* offs, uint32_t* list, uint64_t list_cap);
 
 // In-place exclusive scan of data[0 .. len) with len = *len_ptr (device) or len_max (len_ptr NULL);

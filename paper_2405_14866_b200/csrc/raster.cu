@@ -244,13 +244,22 @@ __device__ __forceinline__ const uint32_t* sorted_vals(const CallState* cs, cons
     return (sort_passes(cs) & 1) ? vals_b : vals_a;
 }
 
+// Pixel boxes in depth-rank order (coalesced input for both binning kernels).
+__global__ void __launch_bounds__(256) k_gather_boxes(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
+                                                      const uint32_t* __restrict__ vals_b,
+                                                      const CallState* __restrict__ cs, uint2* __restrict__ boxes) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= cs->n) return;
+    const uint32_t* sorted = sorted_vals(cs, vals_a, vals_b);
+    const uint4 q = rec[2 * sorted[r] + 1];
+    boxes[r] = make_uint2(q.z, q.w);
+}
+
 // Per-warp tile counts over depth ranks [rb, re): 2-D difference array on a (TY+1) x GW grid
 // (GW = (TX+1)|1, odd to spread banks), prefix-summed in place, then written tile-major
 // into counts[t * P + p].  The last element counts[T*P] is zeroed (it becomes K after the scan).
-__global__ void __launch_bounds__(512) k_bin_count(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
-                                                   const uint32_t* __restrict__ vals_b,
-                                                   const CallState* __restrict__ cs, BinGeom bg,
-                                                   uint32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(512) k_bin_count(const uint2* __restrict__ boxes, const CallState* __restrict__ cs,
+                                                   BinGeom bg, uint32_t* __restrict__ counts) {
     extern __shared__ int32_t s_grid[];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     const int nw = blockDim.x >> 5;
@@ -258,19 +267,15 @@ __global__ void __launch_bounds__(512) k_bin_count(const uint4* __restrict__ rec
     int32_t* grid = s_grid + (size_t)warp * GS;
     for (int k = lane; k < GS; k += 32) grid[k] = 0;
     __syncwarp();
-    const uint32_t* sorted = sorted_vals(cs, vals_a, vals_b);
     const uint32_t p = blockIdx.x * nw + warp;
     uint32_t rb, re;
     rank_range(cs->n, bg.P, p, &rb, &re);
+    uint2 nxt = rb + lane < re ? boxes[rb + lane] : make_uint2(kEmptyRect, kEmptyRect);
     for (uint32_t r0 = rb; r0 < re; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        bool ok = r < re;
-        uint32_t rx = kEmptyRect, ry = kEmptyRect;
-        if (ok) {
-            const uint4 q = rec[2 * sorted[r] + 1];
-            rx = q.z;
-            ry = q.w;
-        }
+        const uint2 bx = nxt;
+        nxt = r0 + 32 + lane < re ? boxes[r0 + 32 + lane] : make_uint2(kEmptyRect, kEmptyRect);
+        bool ok = r0 + lane < re;
+        const uint32_t rx = bx.x, ry = bx.y;
         const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
         ok = ok && x0 <= x1 && y0 <= y1;
         const int sh = bg.shift;
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(512) k_bin_count(const uint4* __restrict__ rec
 // Each warp appends its depth-rank range to the tile lists, in rank order.  32 consecutive
 // (Gaussian, tile) entries per step; same-tile entries inside a step are ordered by lane with
 // match.any, so each list stays ordered by (depth, id).
-__global__ void __launch_bounds__(512) k_bin_place(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
+__global__ void __launch_bounds__(512) k_bin_place(const uint2* __restrict__ boxes, const uint32_t* __restrict__ vals_a,
                                                    const uint32_t* __restrict__ vals_b,
                                                    CallState* __restrict__ cs, BinGeom bg,
                                                    const uint32_t* __restrict__ offs, uint32_t* __restrict__ list,
@@ -332,15 +337,14 @@ __global__ void __launch_bounds__(512) k_bin_place(const uint4* __restrict__ rec
     uint32_t rb, re;
     rank_range(cs->n, bg.P, p, &rb, &re);
     bool overflow = false;
+    uint32_t nidx = rb + lane < re ? sorted[rb + lane] : 0u;
+    uint2 nbx = rb + lane < re ? boxes[rb + lane] : make_uint2(kEmptyRect, kEmptyRect);
     for (uint32_t r0 = rb; r0 < re; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        uint32_t idx = 0, rx = kEmptyRect, ry = kEmptyRect;
-        if (r < re) {
-            idx = sorted[r];
-            const uint4 q = rec[2 * idx + 1];
-            rx = q.z;
-            ry = q.w;
-        }
+        const uint32_t idx = nidx;
+        const uint32_t rx = nbx.x, ry = nbx.y;
+        const uint32_t rn = r0 + 32 + lane;
+        nidx = rn < re ? sorted[rn] : 0u;
+        nbx = rn < re ? boxes[rn] : make_uint2(kEmptyRect, kEmptyRect);
         const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
         const bool ok = x0 <= x1 && y0 <= y1;
         const int sh = bg.shift;

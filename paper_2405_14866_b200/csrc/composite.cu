@@ -273,6 +273,7 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
         }
         __syncwarp();
         // ---- composite the staged entries in order, two pixels per lane
+#pragma unroll 2
         for (int j = 0; j < cnt; j++) {
             const float4 G = bf.g[j];
             const float2 G2 = bf.g2[j];

@@ -33,7 +33,7 @@ struct ta_context {
     size_t smem_optin = 0;
     std::string err;
     uint64_t launches = 0;
-    DevBuf cs, status, rec, boxes, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
+    DevBuf cs, status, rec, boxes, tile_order, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
     // last rasterize call
@@ -228,7 +228,7 @@ ta_status ta_context_create(int32_t device, ta_context** out) {
 ta_status ta_context_destroy(ta_context* c) {
     if (!c) return TA_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->boxes, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
+    DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->boxes, &c->tile_order, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
                       &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
@@ -293,6 +293,10 @@ ta_status reserve_target(ta_context* c, const BinGeom& bg, int64_t cap, int H, i
     const size_t T = (size_t)bg.TX * bg.TY;
     const size_t bin_len = T * bg.P + 1;
     if ((st = grow(c, c->bin_offs, bin_len * 4 + 64)) != TA_OK) return st;
+    {
+        const CompositeGeom cg0 = composite_geometry(bg, H, W);
+        if ((st = grow(c, c->tile_order, (size_t)cg0.TX * cg0.TY * 4 + 64)) != TA_OK) return st;
+    }
     const size_t parts = ((size_t)std::max<int64_t>(cap, 1) + kSortKeysPerBlock - 1) / kSortKeysPerBlock;
     const CompositeGeom cg = composite_geometry(bg, H, W);
     const uint32_t region = std::max(std::max(scan_tiles((uint32_t)(256 * parts)), scan_tiles((uint32_t)bin_len)),
@@ -514,10 +518,10 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);
     cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, rec, g->feat, (const uint32_t*)c->list.p,
-                                     offs, cg, rc, cs, (uint64_t)(c->list.bytes / 4), feat_out, alpha_out,
+                                     offs, (uint32_t*)c->tile_order.p, cg, rc, cs, (uint64_t)(c->list.bytes / 4), feat_out, alpha_out,
                                      counts ? (int32_t*)c->ncontrib.p : nullptr, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "composite launch");
-    c->launches++;
+    c->launches += 2;   // k_tile_order + k_composite
     tm.end();
     c->have_last = true;
     c->last_TX = cg.TX; c->last_TY = cg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;

@@ -175,13 +175,14 @@ __device__ __forceinline__ uint32_t box_lane_mask(int gx0, int gx1, int gy0, int
 template <int C, typename FT, bool kCounts>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const uint32_t* __restrict__ clist,
-            const uint32_t* __restrict__ coffs, CompositeGeom cg, RasterConsts rc, const CallState* __restrict__ cs,
-            uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout, int32_t* __restrict__ ncontrib) {
+            const uint32_t* __restrict__ coffs, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
+            const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
+            int32_t* __restrict__ ncontrib) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     WarpBuf<C>& bf = reinterpret_cast<WarpBuf<C>*>(smem_raw)[warp];
 
-    const int tile = blockIdx.x;
+    const int tile = (int)order[blockIdx.x];           // heaviest tiles first (k_tile_order)
     const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
     const int sb = cg.shift - 4;
     const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
@@ -196,7 +197,6 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
     const float pxf = (float)px;
     const float2 py2 = make_float2((float)pyA, (float)pyB);
     const float qlim = rc.q_max * 1.015625f + 0.01f;
-    const float X0 = (float)bx0, X1 = (float)(bx0 + 7), Y0 = (float)by0, Y1 = (float)(by0 + 7);
     const uint32_t lt = lanemask_lt();
 
     float2 FA[C / 2], FB[C / 2];
@@ -209,6 +209,14 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
 
     uint32_t pos = cstart;
     while (pos < cend && !__all_sync(0xffffffffu, doneA && doneB)) {
+        // culling rectangle = bounding box of the pixels still compositing (shrinks as pixels stop;
+        // entries that can only reach stopped pixels are never staged)
+        const bool actA = !doneA, actB = !doneB;
+        const int ax0 = __reduce_min_sync(0xffffffffu, (actA || actB) ? px : 0x7fffffff);
+        const int ax1 = __reduce_max_sync(0xffffffffu, (actA || actB) ? px : -1);
+        const int ay0 = __reduce_min_sync(0xffffffffu, actA ? pyA : (actB ? pyB : 0x7fffffff));
+        const int ay1 = __reduce_max_sync(0xffffffffu, actB ? pyB : (actA ? pyA : -1));
+        const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
         // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries (two independent
         //      32-entry chunks) per round trip
         int cnt = 0;
@@ -232,7 +240,7 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
                 const int gx0 = (int)(r1[h].z & 0xffff), gx1 = (int)(r1[h].z >> 16);
                 const int gy0 = (int)(r1[h].w & 0xffff), gy1 = (int)(r1[h].w >> 16);
                 keep[h] = idx[h] < n && gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
-                          tyi <= (gy1 >> 4) && gx0 <= bx0 + 7 && gx1 >= bx0 && gy0 <= by0 + 7 && gy1 >= by0 &&
+                          tyi <= (gy1 >> 4) && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
                           ellipse_may_touch(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y), __uint_as_float(r0[h].z),
                                             __uint_as_float(r0[h].w), __uint_as_float(r1[h].x), X0, X1, Y0, Y1, qlim);
             }
@@ -354,10 +362,37 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
     }
 }
 
+// Launch order of the tile CTAs: by decreasing log2 of the tile's coarse-list length (longest
+// lists first, so the last wave is made of short tiles).  One block; order within a bucket is
+// arbitrary (it only affects scheduling, never results).
+__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict__ coffs, CompositeGeom cg,
+                                                     uint32_t* __restrict__ order) {
+    __shared__ uint32_t s_cnt[33], s_off[33];
+    const int T = cg.TX * cg.TY;
+    if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const int sb = cg.shift - 4;
+    auto bucket = [&](int t) {
+        const int tyi = t / cg.TX, txi = t - tyi * cg.TX;
+        const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
+        const uint32_t len = coffs[(size_t)(bin + 1) * cg.P] - coffs[(size_t)bin * cg.P];
+        return 32 - (32 - __clz(len));                 // 32 - bit length: longer lists -> smaller bucket
+    };
+    for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_cnt[bucket(t)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < 33; b++) { s_off[b] = run; run += s_cnt[b]; }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += blockDim.x) order[atomicAdd(&s_off[bucket(t)], 1u)] = (uint32_t)t;
+}
+
 template <int C, typename FT>
 static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, const uint32_t* list,
-                              const uint32_t* offs, CompositeGeom cg, RasterConsts rc, const CallState* cs,
-                              uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
+                              const uint32_t* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc,
+                              const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
+                              cudaStream_t st) {
     const size_t smem = sizeof(WarpBuf<C>) * kWarps;
     static bool attr_set = false;   // per template instance; set once per process
     if (!attr_set) {
@@ -369,23 +404,24 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
         attr_set = true;
     }
     if (tiles == 0) return cudaSuccess;
+    k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     if (ncontrib)
-        k_composite<C, FT, true><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg, rc, cs,
-                                                               list_cap, F, A, ncontrib);
+        k_composite<C, FT, true><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, order, cg,
+                                                               rc, cs, list_cap, F, A, ncontrib);
     else
-        k_composite<C, FT, false><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, cg, rc,
-                                                                cs, list_cap, F, A, ncontrib);
+        k_composite<C, FT, false><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, order,
+                                                                cg, rc, cs, list_cap, F, A, ncontrib);
     return cudaGetLastError();
 }
 
 cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
-                             const uint32_t* list, const uint32_t* offs, CompositeGeom cg, RasterConsts rc,
-                             const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
-                             cudaStream_t st) {
+                             const uint32_t* list, const uint32_t* offs, uint32_t* order, CompositeGeom cg,
+                             RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
+                             int32_t* ncontrib, cudaStream_t st) {
 #define TA_CASE(CC)                                                                                           \
     case CC:                                                                                                  \
-        return fbytes == 2 ? launch_one<CC, __half>(tiles, rec, feat, list, offs, cg, rc, cs, list_cap, F, A, ncontrib, st) \
-                           : launch_one<CC, float>(tiles, rec, feat, list, offs, cg, rc, cs, list_cap, F, A, ncontrib, st);
+        return fbytes == 2 ? launch_one<CC, __half>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st) \
+                           : launch_one<CC, float>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st);
     switch (C) {
         TA_CASE(8)
         TA_CASE(16)

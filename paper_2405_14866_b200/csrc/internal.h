@@ -81,9 +81,9 @@ struct CompositeGeom {
     uint32_t P;           // coarse-binning partitions (columns of the bin-major offset matrix)
 };
 cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
-                             const uint32_t* list, const uint32_t* offs, CompositeGeom cg, RasterConsts rc,
-                             const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
-                             cudaStream_t st);
+                             const uint32_t* list, const uint32_t* offs, uint32_t* order, CompositeGeom cg,
+                             RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
+                             int32_t* ncontrib, cudaStream_t st);
 // debug: materialise the per-tile (tile, depth, id) lists the compositor walks (a3/a5 check)
 void launch_debug_tile_lists(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
                              const CallState* cs, uint32_t* tile_offs, unsigned long long* status, uint32_t* counter,

@@ -142,7 +142,7 @@ __device__ __forceinline__ float2 exp_det2(float2 x) {
 
 constexpr int kWarps = 4;                        // warps per CTA = 8x8-pixel blocks of the 16x16 tile
 constexpr int kThreads = 32 * kWarps;
-constexpr int kBuf = 32;                         // entries staged per warp at a time
+constexpr int kBuf = 64;                         // entries staged per warp at a time
 
 template <int C>
 struct WarpBuf {

@@ -153,12 +153,18 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* _
     for (int k = threadIdx.x; k < kSortWarps * 256; k += blockDim.x) (&s_cnt[0][0])[k] = 0u;
     __syncthreads();
     uint32_t* cnt = s_cnt[warp];
+    constexpr int kChunks = kSortKeysPerWarp / 32;
     const uint32_t b = blockIdx.x * kSortKeysPerBlock + warp * kSortKeysPerWarp;
-    const uint32_t e = min(n, b + kSortKeysPerWarp);
-    for (uint32_t c = b; c < e; c += 32) {
-        const uint32_t idx = c + lane;
-        const bool ok = idx < e;
-        const uint32_t d = ok ? (src[idx] >> shift) & 255u : 0u;
+    uint32_t key[kChunks];
+#pragma unroll
+    for (int k = 0; k < kChunks; k++) {          // all loads in flight before any ranking
+        const uint32_t idx = b + k * 32 + lane;
+        key[k] = idx < n ? src[idx] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kChunks; k++) {
+        const bool ok = b + k * 32 + lane < n;
+        const uint32_t d = ok ? (key[k] >> shift) & 255u : 0u;
         const uint32_t peers = peers8(d, __ballot_sync(0xffffffffu, ok));
         if (ok && lane == (uint32_t)(__ffs(peers) - 1)) cnt[d] += __popc(peers);
         __syncwarp();

@@ -89,13 +89,14 @@ static float dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
 
 /*
  * exp_det -- DESIGN.md reading R13.  exp(x) for x <= 0 by a fixed fp32 sequence:
- * k = rint(x*log2 e); Cody-Waite reduction r = x - k*ln2 (hi/lo split); degree-7
+ * k = the integer nearest (ties to even) to the exact product x*log2 e, obtained with one
+ * rounding as fma(x, log2 e, 1.5*2^23) - 1.5*2^23; Cody-Waite reduction r = x - k*ln2 (hi/lo split); degree-7
  * Taylor polynomial in Horner form with fmaf; scale by 2^k (exact).  Pinned in
  * tests/test_oracle_pins.py against float64 exp over [-4.5, 0] (<= 2 ulp).
  */
 float tao_exp_det(float x) {
     if (x < -80.0f) x = -80.0f;
-    float k = rintf(x * 1.44269502162933349609375f);          /* float(log2 e) */
+    float k = fmaf(x, 1.44269502162933349609375f, 12582912.0f) - 12582912.0f;   /* float(log2 e) */
     float r = fmaf(-k, 0.693145751953125f, x);                  /* ln2 hi */
     r = fmaf(-k, 1.428606765330187045037746429443359375e-06f, r); /* ln2 lo */
     float p = 1.98412698412698412698e-4f;                       /* 1/5040 */

@@ -32,7 +32,7 @@ __device__ __forceinline__ float dot3(float a0, float a1, float a2, float b0, fl
 // DESIGN.md R13 exp_det: exp(x), x <= 0, by a fixed fp32 sequence (Cody-Waite + degree-7 Taylor).
 __device__ __forceinline__ float exp_det(float x) {
     x = fmaxf(x, -80.0f);
-    const float k = rintf(fmul(x, 1.44269502162933349609375f));
+    const float k = fsub(ffma(x, 1.44269502162933349609375f, 12582912.0f), 12582912.0f);   // nearest-even of x*log2e
     float r = ffma(-k, 0.693145751953125f, x);
     r = ffma(-k, 1.428606765330187045037746429443359375e-06f, r);
     float p = 1.98412698412698412698e-4f;
@@ -92,6 +92,7 @@ struct CallState {
     uint32_t bin_len;              // T * P (+1 for the total)
     uint32_t overflow;             // sticky: entries exceeded the list capacity (not reset by k_init)
     uint32_t scan_counter[8];      // tile counters of the look-back scans (one per scan)
+    unsigned long long work[8];    // compositor work counters (TA_FLAG_DEBUG_COUNTS only, reset by k_init)
 };
 
 constexpr int kSortWarps = 8;                                  // warps per block in the sort kernels

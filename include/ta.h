@@ -175,6 +175,10 @@ typedef struct {
     const uint32_t* tile_offsets;
     const uint32_t* tile_list;
     const int32_t* n_contrib;
+    /* compositor work counters (only with TA_FLAG_DEBUG_COUNTS): [0] coarse-list entries read,
+       [1] entries staged, [2] staged entries evaluated, [3] evaluated with some q <= q_max,
+       [4] accumulated, [5] composited (pixel, Gaussian) pairs, [6] warps, [7] fill rounds */
+    int64_t work[8];
 } ta_debug_view;
 ta_status ta_debug_last(ta_context* ctx, ta_debug_view* out, void* stream);
 

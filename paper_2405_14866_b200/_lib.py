@@ -53,7 +53,8 @@ class DebugView(C.Structure):
     _fields_ = [("n", C.c_int64), ("K", C.c_int64), ("Kc", C.c_int64), ("P", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("sort_passes", C.c_int32), ("records", C.c_void_p),
                 ("depth_keys", C.c_void_p), ("order", C.c_void_p), ("tile_offsets", C.c_void_p),
-                ("tile_list", C.c_void_p), ("n_contrib", C.c_void_p)]
+                ("tile_list", C.c_void_p), ("n_contrib", C.c_void_p),
+                ("work", C.c_int64 * 8)]
 
 
 STAGES = ("unproject", "project", "sort", "bin_count", "bin_scan", "bin_place", "composite")

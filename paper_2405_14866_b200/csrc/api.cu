@@ -578,6 +578,7 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     out->tile_offsets = (const uint32_t*)c->dbg_offs.p;
     out->tile_list = (const uint32_t*)c->dbg_list.p;
     out->n_contrib = c->last_counts ? (const int32_t*)c->ncontrib.p : nullptr;
+    for (int k = 0; k < 8; k++) out->work[k] = c->last_counts ? (int64_t)h.work[k] : 0;
     return TA_OK;
 }
 

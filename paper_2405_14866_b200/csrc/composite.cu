@@ -118,11 +118,12 @@ __device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
 // exp_det (R13) of two arguments at once; identical per component to exp_det() for
 // x >= -80 (the only arguments whose results are used: x = -q/2 with q <= q_max).
 __device__ __forceinline__ float2 exp_det2(float2 x) {
-    // k = rint(x*log2e) without FRND/F2I: adding 1.5*2^23 rounds y = x*log2e to the nearest integer
-    // (ties to even, |y| < 2^22) exactly like rintf, the difference recovers it as a float and the
-    // low mantissa bits hold it as an integer.
+    // k = the integer nearest (ties to even) to the exact product x*log2e, with one rounding:
+    // fma(x, log2e, 1.5*2^23) lands on that integer (|x*log2e| < 2^22), the difference recovers it as
+    // a float and the low mantissa bits hold it as an integer.  (Written as one fma on purpose: ptxas
+    // contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2, so a separate product is not expressible.)
     constexpr float kMagic = 12582912.0f;                  // 1.5 * 2^23
-    const float2 t = add2(mul2(x, bc2(1.44269502162933349609375f)), bc2(kMagic));
+    const float2 t = fma2(x, bc2(1.44269502162933349609375f), bc2(kMagic));
     const float2 k = sub2(t, bc2(kMagic));
     const float2 nk = make_float2(-k.x, -k.y);
     float2 r = fma2(nk, bc2(0.693145751953125f), x);
@@ -207,6 +208,7 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
     bool doneA = (px >= W) || (pyA >= H);
     bool doneB = (px >= W) || (pyB >= H);
 
+    unsigned long long wk[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // kCounts: work counters (lane 0)
     uint32_t pos = cstart;
     while (pos < cend && !__all_sync(0xffffffffu, doneA && doneB)) {
         // culling rectangle = bounding box of the pixels still compositing (shrinks as pixels stop;
@@ -278,7 +280,9 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
                 if (step < 32u) break;                     // partial chunk: the next round resumes here
             }
             pos += adv;
+            if (kCounts) { wk[0] += adv; wk[7] += 1; }
         }
+        if (kCounts) wk[1] += cnt;
         __syncwarp();
         // ---- composite the staged entries in order, two pixels per lane
 #pragma unroll 2
@@ -296,7 +300,9 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
             const float2 q = fma2(t2, bc2(dx), t4);
             inA = inA && q.x <= rc.q_max;
             inB = inB && q.y <= rc.q_max;
+            if (kCounts) wk[2] += 1;
             if (!__any_sync(0xffffffffu, inA || inB)) continue;
+            if (kCounts) wk[3] += 1;
             const float2 e = exp_det2(mul2(bc2(-0.5f), q));
             const float2 ae = mul2(bc2(G2.y), e);
             const float2 a = make_float2(fminf(rc.alpha_max, ae.x), fminf(rc.alpha_max, ae.y));
@@ -339,6 +345,8 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
             }
             T = make_float2(inA ? Tn.x : T.x, inB ? Tn.y : T.y);
             if (kCounts) {
+                wk[4] += (anyA || anyB) ? 1 : 0;
+                wk[5] += __popc(__ballot_sync(0xffffffffu, inA)) + __popc(__ballot_sync(0xffffffffu, inB));
                 ncA += inA ? 1 : 0;
                 ncB += inB ? 1 : 0;
             }
@@ -347,6 +355,12 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
         __syncwarp();
     }
 
+    if (kCounts && lane == 0) {
+        unsigned long long* work = const_cast<CallState*>(cs)->work;
+        wk[6] = 1;
+#pragma unroll
+        for (int k = 0; k < 8; k++) atomicAdd(&work[k], wk[k]);
+    }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int py = h ? pyB : pyA;
@@ -388,6 +402,382 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict_
     for (int t = threadIdx.x; t < T; t += blockDim.x) order[atomicAdd(&s_off[bucket(t)], 1u)] = (uint32_t)t;
 }
 
+// ============================================================================ tensor-core variant
+// k_composite_tc<C>: fp16-stored features.  The per-pixel recurrence (q, exp_det, alpha', T, the
+// stop rule) is the same packed fp32 sequence as k_composite, so T and A stay bit-exact; only the
+// C-channel accumulation F[pixel][c] += w[pixel][j] * f[j][c] moves to the tensor cores.  Per 16
+// staged entries it is a dense contraction F[64 px x C] += W[64 px x 16] . f[16 x C], done with
+// mma.sync m16n8k16 (fp16 x fp16 -> fp32).  The fp16 features are exact operands; the fp32 weight
+// w is split into w_hi = fp16(2^11 w) and w_lo = fp16(2^11 w - w_hi), both multiplied by the same
+// f (two MMAs), so each weight keeps ~22 significant bits; the 2^11 scale keeps w_lo clear of the
+// fp16 subnormals and is removed exactly at the end.  Products are exact and the MMA accumulates
+// in fp32, so F matches the oracle's sequential fp32 sum to ~1e-6 (tolerance 1e-4, R22).
+
+template <int C>
+struct TcBuf {
+    // fp16 feature row pitch (halves): an odd number of 16-B chunks, so the 8 rows one ldmatrix
+    // phase reads fall into 8 different 16-B bank groups
+    static constexpr int PH = (((C + 8) / 8) & 1) ? C + 8 : C + 16;
+    static constexpr int WP = 36;      // weight row pitch (32-bit words): 144 B, odd number of 16-B chunks
+    float4 g[kBuf];                    // mx, my, ca, cb2
+    float4 h[kBuf];                    // cc, alpha, box lane mask (pixel A), box lane mask (pixel B)
+    __half f[kBuf][PH];                // staged fp16 feature rows
+    uint32_t w[2][16][WP];             // [hi|lo][k][lane]: half2 (w(pixel A), w(pixel B)) of staged entry j0+k
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void hmma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Conservative "may the ellipse q <= qlim reach the pixel rectangle [X0,X1] x [Y0,Y1]" test.  For a
+// centre outside the rectangle the minimum of the convex q over it lies on an edge facing the centre
+// (at a minimiser on x = X0 the gradient 2 C d has no y part, so d_x = (g_x / 2) Sigma_xx >= 0, i.e.
+// mx <= X0; likewise for the other edges), so only those (at most one vertical and one horizontal)
+// are evaluated, each at the clamped minimiser along it.  The approximate reciprocal only moves the
+// evaluation point by ~1e-7 relative (q error second order); qlim carries a 1.6 % + 0.01 margin.
+// Nearly degenerate conics (condition > 4096) are never culled (the per-pixel test decides).
+__device__ __forceinline__ bool ellipse_may_touch2(float mx, float my, float ca, float cb2, float cc, float X0,
+                                                   float X1, float Y0, float Y1, float qlim) {
+    const float lx = X0 - mx, hx = X1 - mx, ly = Y0 - my, hy = Y1 - my;
+    const bool vx = lx > 0.0f || hx < 0.0f, vy = ly > 0.0f || hy < 0.0f;
+    if (!vx && !vy) return true;                       // centre inside
+    const float cb = 0.5f * cb2;
+    if (!(fmaf(-cb, cb, ca * cc) * 4096.0f > ca * cc)) return true;
+    float best = 3.0e38f;
+    if (vx) {
+        const float dx = lx > 0.0f ? lx : hx;
+        const float dy = fminf(fmaxf(-cb * dx * rcp_approx(cc), ly), hy);
+        best = dx * (ca * dx + cb2 * dy) + cc * dy * dy;
+    }
+    if (vy) {
+        const float ey = ly > 0.0f ? ly : hy;
+        const float ex = fminf(fmaxf(-cb * ey * rcp_approx(ca), lx), hx);
+        best = fminf(best, ex * (ca * ex + cb2 * ey) + cc * ey * ey);
+    }
+    return best <= qlim;
+}
+
+constexpr float kInf = __builtin_huge_valf();
+
+// q = fma(fma(ca, dx, cb2*dy), dx, (cc*dy)*dy) for the lane's two pixels (normative a6 sequence)
+__device__ __forceinline__ float2 quad_q(const float4 G, float cc, float pxf, float2 py2) {
+    const float dx = fsub(pxf, G.x);
+    const float2 dy = sub2(py2, bc2(G.y));
+    const float2 t1 = mul2(bc2(G.w), dy);
+    const float2 t2 = fma2(bc2(G.z), bc2(dx), t1);
+    const float2 t4 = mul2(mul2(bc2(cc), dy), dy);
+    return fma2(t2, bc2(dx), t4);
+}
+
+// One compositing step of the normative a6 recurrence for the lane's two pixels.  qm = q (or +inf if
+// the pixel is outside the box / already stopped), a = alpha'.  Returns the weight 2^11 alpha' T of
+// each pixel (0 if it does not composite this entry) and advances T / the active bits.
+template <bool kCounts>
+__device__ __forceinline__ float2 tstep(float2 qm, float2 a, float qmax, float amin, float teps, float2& T,
+                                        uint32_t& actA, uint32_t& actB, int& ncA, int& ncB, unsigned long long* wk) {
+    const float2 Tn = mul2(T, sub2(bc2(1.0f), a));
+    const bool okA = qm.x <= qmax && a.x >= amin, okB = qm.y <= qmax && a.y >= amin;
+    const bool inA = okA && Tn.x >= teps, inB = okB && Tn.y >= teps;
+    if (okA && !inA) actA = 0u;           // T would drop below t_eps: stop before this Gaussian (R10)
+    if (okB && !inB) actB = 0u;
+    const float2 ws = mul2(mul2(a, bc2(2048.0f)), T);
+    const float2 w = make_float2(inA ? ws.x : 0.0f, inB ? ws.y : 0.0f);
+    T = make_float2(inA ? Tn.x : T.x, inB ? Tn.y : T.y);
+    if (kCounts) {
+        wk[4] += __any_sync(0xffffffffu, inA || inB) ? 1 : 0;
+        wk[5] += __popc(__ballot_sync(0xffffffffu, inA)) + __popc(__ballot_sync(0xffffffffu, inB));
+        ncA += inA ? 1 : 0;
+        ncB += inB ? 1 : 0;
+    }
+    return w;
+}
+
+template <int C, bool kCounts>
+__global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
+k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
+               const uint32_t* __restrict__ coffs, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
+               const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
+               int32_t* __restrict__ ncontrib) {
+    constexpr int NT = C / 8;                 // n-tiles of 8 channels
+    constexpr int PH = TcBuf<C>::PH;
+    constexpr int WP = TcBuf<C>::WP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+    TcBuf<C>& bf = reinterpret_cast<TcBuf<C>*>(smem_raw)[warp];
+
+    const int tile = (int)order[blockIdx.x];
+    const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
+    const int sb = cg.shift - 4;
+    const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
+    const uint32_t cstart = coffs[(size_t)bin * cg.P];
+    uint32_t cend = coffs[(size_t)(bin + 1) * cg.P];
+    if (cend > list_cap) cend = (uint32_t)list_cap;
+    const uint32_t n = cs->n;
+    const int W = cg.W, H = cg.H;
+
+    const int bx0 = txi * kTile + 8 * (int)(warp & 1), by0 = tyi * kTile + 8 * (int)(warp >> 1);
+    const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
+    const float pxf = (float)px;
+    const float2 py2 = make_float2((float)pyA, (float)pyB);
+    const float qmax = rc.q_max, amax = rc.alpha_max, amin = rc.alpha_min, teps = rc.t_eps;
+    const float qlim = qmax * 1.015625f + 0.01f;
+    const uint32_t lt = lanemask_lt();
+
+    // ldmatrix row addresses.  A (weights, stored [k][pixel p' = 2 lane + (0: A, 1: B)]): lane i
+    // addresses row k = (i & 7) + 8 (i >> 4) of matrix i >> 3, pixel chunk 2 mt + ((i >> 3) & 1).
+    const int li = (int)lane;
+    const uint32_t a_base = smem_u32(&bf.w[0][(li & 7) + 8 * (li >> 4)][0]) + (uint32_t)(((li >> 3) & 1) * 16);
+    constexpr uint32_t kLoOff = 16 * WP * 4;
+    // B (features, stored [k][channel]): lane i addresses row (i & 7) + 8 ((i >> 3) & 1), channel chunk 2 np + (i >> 4)
+    const int bk = (li & 7) + 8 * ((li >> 3) & 1);
+    const uint32_t b_base = smem_u32(&bf.f[0][0]) + (uint32_t)((li >> 4) * 16);
+    uint32_t* const wst = &bf.w[0][0][li];    // this lane's word in weight row 0 (hi)
+
+    float acc[4][NT][4];
+#pragma unroll
+    for (int mt = 0; mt < 4; mt++)
+#pragma unroll
+        for (int nt = 0; nt < NT; nt++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) acc[mt][nt][e] = 0.0f;
+    float2 T = make_float2(1.0f, 1.0f);
+    int ncA = 0, ncB = 0;
+    // active-pixel lane bits: the lane's bit while its pixel still composites, else 0
+    uint32_t actA = (px < W && pyA < H) ? (1u << lane) : 0u;
+    uint32_t actB = (px < W && pyB < H) ? (1u << lane) : 0u;
+
+    unsigned long long wk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t pos = cstart;
+    while (pos < cend && __any_sync(0xffffffffu, (actA | actB) != 0u)) {
+        // culling rectangle = bounding box of the pixels still compositing
+        const int ax0 = __reduce_min_sync(0xffffffffu, (actA | actB) ? px : 0x7fffffff);
+        const int ax1 = __reduce_max_sync(0xffffffffu, (actA | actB) ? px : -1);
+        const int ay0 = __reduce_min_sync(0xffffffffu, actA ? pyA : (actB ? pyB : 0x7fffffff));
+        const int ay1 = __reduce_max_sync(0xffffffffu, actB ? pyB : (actA ? pyA : -1));
+        const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
+        // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip
+        int cnt = 0;
+        while (cnt < kBuf && pos < cend) {
+            uint32_t idx[2];
+            uint4 r0[2], r1[2];
+            bool keep[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const uint32_t e = pos + 32 * hh + lane;
+                idx[hh] = e < cend ? clist[e] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
+                r1[hh] = rec[2 * i + 1];
+                r0[hh] = rec[2 * i];
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
+                const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
+                keep[hh] = idx[hh] < n && gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
+                           tyi <= (gy1 >> 4) && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
+                           ellipse_may_touch2(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
+                                              __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
+                                              __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
+            }
+            uint32_t adv = 0;
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                if (cnt >= kBuf) break;
+                const uint32_t base = pos + 32 * hh;
+                if (base >= cend) break;
+                bool kp = keep[hh];
+                uint32_t bal = __ballot_sync(0xffffffffu, kp);
+                const int room = kBuf - cnt;
+                const uint32_t rank = __popc(bal & lt);
+                uint32_t step = min(32u, cend - base);
+                if (__popc(bal) > room) {
+                    const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
+                    const int cl = __ffs(cut) - 1;
+                    bal &= (1u << cl) - 1u;
+                    step = (uint32_t)cl;
+                    kp = kp && (int)lane < cl;
+                }
+                if (kp) {
+                    const int d = cnt + (int)rank;
+                    const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
+                    const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
+                    bf.g[d] = make_float4(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
+                                          __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w));
+                    bf.h[d] = make_float4(__uint_as_float(r1[hh].x), __uint_as_float(r1[hh].y),
+                                          __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
+                                          __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
+                    const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
+                    const uint32_t dst = smem_u32(&bf.f[d][0]);
+#pragma unroll
+                    for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                }
+                cnt += __popc(bal);
+                adv += step;
+                if (step < 32u) break;
+            }
+            pos += adv;
+            if (kCounts) { wk[0] += adv; wk[7] += 1; }
+        }
+        if (kCounts) wk[1] += cnt;
+        cp_async_wait_all();
+        __syncwarp();
+        // ---- composite the staged entries, 16 at a time: SIMT weights -> smem -> tensor cores
+        for (int j0 = 0; j0 < cnt; j0 += 16) {
+            const int nk = min(16, cnt - j0);
+#pragma unroll
+            for (int jj = 0; jj < 16; jj += 2) {
+                float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
+                if (jj < nk) {                                   // warp-uniform
+                    const int j1 = j0 + jj + (jj + 1 < nk ? 1 : 0);
+                    const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
+                    const float4 G1 = bf.g[j1], H1 = bf.h[j1];
+                    // q of both entries for both pixels; qm = q where the pixel is in the entry's box and
+                    // still compositing, else +inf (so "qm <= q_max" is the whole per-pixel geometric test)
+                    const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
+                    const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : kInf,
+                                                   (__float_as_uint(H0.w) & actB) ? q0.y : kInf);
+                    float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : kInf,
+                                             (__float_as_uint(H1.w) & actB) ? q1.y : kInf);
+                    if (jj + 1 >= nk) qm1 = make_float2(kInf, kInf);
+                    if (kCounts) wk[2] += (jj + 1 < nk) ? 2 : 1;
+                    if (__any_sync(0xffffffffu, fminf(fminf(qm0.x, qm0.y), fminf(qm1.x, qm1.y)) <= qmax)) {
+                        // exp / alpha' of both entries are independent of T: computed side by side
+                        const float2 x0 = exp_det2(mul2(bc2(-0.5f), q0));
+                        const float2 x1 = exp_det2(mul2(bc2(-0.5f), q1));
+                        const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);
+                        const float2 a0 = make_float2(fminf(amax, ae0.x), fminf(amax, ae0.y));
+                        const float2 a1 = make_float2(fminf(amax, ae1.x), fminf(amax, ae1.y));
+                        if (kCounts) {
+                            wk[3] += __any_sync(0xffffffffu, fminf(qm0.x, qm0.y) <= qmax) ? 1 : 0;
+                            wk[3] += __any_sync(0xffffffffu, fminf(qm1.x, qm1.y) <= qmax) ? 1 : 0;
+                        }
+                        w0 = tstep<kCounts>(qm0, a0, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                        // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
+                        qm1 = make_float2(actA ? qm1.x : kInf, actB ? qm1.y : kInf);
+                        w1 = tstep<kCounts>(qm1, a1, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                    }
+                }
+                // split into fp16 hi / lo and store rows jj, jj+1
+                const __half2 h0 = __floats2half2_rn(w0.x, w0.y), h1 = __floats2half2_rn(w1.x, w1.y);
+                const float2 r0 = sub2(w0, __half22float2(h0)), r1 = sub2(w1, __half22float2(h1));
+                const __half2 l0 = __floats2half2_rn(r0.x, r0.y), l1 = __floats2half2_rn(r1.x, r1.y);
+                wst[jj * WP] = *reinterpret_cast<const uint32_t*>(&h0);
+                wst[(jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&h1);
+                wst[16 * WP + jj * WP] = *reinterpret_cast<const uint32_t*>(&l0);
+                wst[16 * WP + (jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&l1);
+            }
+            __syncwarp();
+            // B fragments: feature rows j0 .. j0+15 (rows past cnt carry weight 0: clamp to a staged row)
+            uint32_t bfr[NT][2];
+            {
+                const int row = min(j0 + bk, cnt - 1);
+                const uint32_t rb = b_base + (uint32_t)(row * PH * 2);
+                if constexpr (NT == 1) {
+                    ldsm_x2_t(rb, bfr[0][0], bfr[0][1]);
+                } else {
+#pragma unroll
+                    for (int np = 0; np < NT / 2; np++)
+                        ldsm_x4_t(rb + np * 32, bfr[2 * np][0], bfr[2 * np][1], bfr[2 * np + 1][0], bfr[2 * np + 1][1]);
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; mt++) {
+                uint32_t ah[4], al[4];
+                ldsm_x4_t(a_base + mt * 32, ah[0], ah[1], ah[2], ah[3]);
+                ldsm_x4_t(a_base + mt * 32 + kLoOff, al[0], al[1], al[2], al[3]);
+#pragma unroll
+                for (int nt = 0; nt < NT; nt++) {
+                    hmma16816(acc[mt][nt], ah, bfr[nt][0], bfr[nt][1]);
+                    hmma16816(acc[mt][nt], al, bfr[nt][0], bfr[nt][1]);
+                }
+            }
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, (actA | actB) != 0u)) break;
+        }
+        __syncwarp();
+    }
+
+    if (kCounts && lane == 0) {
+        unsigned long long* work = const_cast<CallState*>(cs)->work;
+        wk[6] = 1;
+#pragma unroll
+        for (int k = 0; k < 8; k++) atomicAdd(&work[k], wk[k]);
+    }
+    // accumulator (mt, row r in 0..15) <-> pixel p' = 16 mt + r = 2 l' + h: lane l' = 8 mt + (r >> 1), pixel A/B = r & 1
+    const int g = li >> 2, t = li & 3;
+#pragma unroll
+    for (int mt = 0; mt < 4; mt++) {
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+            const int r = g + 8 * half;
+            const int l2 = 8 * mt + (r >> 1);
+            const int ox = bx0 + (l2 & 7), oy = by0 + (l2 >> 3) + 4 * (r & 1);
+            if (ox < W && oy < H) {
+                float* out = Fout + ((size_t)oy * W + ox) * C + 2 * t;
+#pragma unroll
+                for (int nt = 0; nt < NT; nt++)
+                    *reinterpret_cast<float2*>(out + 8 * nt) =
+                        make_float2(acc[mt][nt][2 * half] * (1.0f / 2048.0f), acc[mt][nt][2 * half + 1] * (1.0f / 2048.0f));
+            }
+        }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+        const int py = hh ? pyB : pyA;
+        if (px < W && py < H) {
+            const size_t pix = (size_t)py * W + px;
+            Aout[pix] = fsub(1.0f, hh ? T.y : T.x);
+            if (kCounts) ncontrib[pix] = hh ? ncB : ncA;
+        }
+    }
+}
+
+template <int C>
+static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, const uint32_t* list, const uint32_t* offs,
+                             uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs, uint64_t list_cap,
+                             float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
+    const size_t smem = sizeof(TcBuf<C>) * kWarps;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_composite_tc<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_composite_tc<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    if (tiles == 0) return cudaSuccess;
+    k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
+    const __half* fh = static_cast<const __half*>(feat);
+    if (ncontrib)
+        k_composite_tc<C, true><<<tiles, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
+    else
+        k_composite_tc<C, false><<<tiles, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
+    return cudaGetLastError();
+}
+
 template <int C, typename FT>
 static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, const uint32_t* list,
                               const uint32_t* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc,
@@ -420,7 +810,7 @@ cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, con
                              int32_t* ncontrib, cudaStream_t st) {
 #define TA_CASE(CC)                                                                                           \
     case CC:                                                                                                  \
-        return fbytes == 2 ? launch_one<CC, __half>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st) \
+        return fbytes == 2 ? launch_tc<CC>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st) \
                            : launch_one<CC, float>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st);
     switch (C) {
         TA_CASE(8)

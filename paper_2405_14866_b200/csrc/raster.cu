@@ -37,6 +37,7 @@ __global__ void k_init(CallState* __restrict__ cs, unsigned long long* __restric
         cs->sort_len = 256u * cs->sort_parts;
         cs->bin_len = bin_len;
         for (int k = 0; k < 8; k++) cs->scan_counter[k] = 0u;
+        for (int k = 0; k < 8; k++) cs->work[k] = 0ull;
     }
 }
 

@@ -568,6 +568,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 
     unsigned long long wk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t pos = cstart;
+    uint32_t pf_pos = 0xffffffffu, pf[2] = {0u, 0u};     // prefetched list indices of entries pf_pos + [0, 64)
     while (pos < cend && __any_sync(0xffffffffu, (actA | actB) != 0u)) {
         // culling rectangle = bounding box of the pixels still compositing
         const int ax0 = __reduce_min_sync(0xffffffffu, (actA | actB) ? px : 0x7fffffff);
@@ -575,29 +576,42 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         const int ay0 = __reduce_min_sync(0xffffffffu, actA ? pyA : (actB ? pyB : 0x7fffffff));
         const int ay1 = __reduce_max_sync(0xffffffffu, actB ? pyB : (actA ? pyA : -1));
         const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
-        // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip
+        // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip.
+        //      The list indices of the next 64 entries are loaded one round ahead (pf_pos / pf).
         int cnt = 0;
         while (cnt < kBuf && pos < cend) {
             uint32_t idx[2];
+            if (pf_pos == pos) {
+                idx[0] = pf[0];
+                idx[1] = pf[1];
+            } else {
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const uint32_t e = pos + 32 * hh + lane;
+                    idx[hh] = e < cend ? clist[e] : 0xffffffffu;
+                }
+            }
             uint4 r0[2], r1[2];
             bool keep[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                const uint32_t e = pos + 32 * hh + lane;
-                idx[hh] = e < cend ? clist[e] : 0xffffffffu;
-            }
 #pragma unroll
             for (int hh = 0; hh < 2; hh++) {
                 const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
                 r1[hh] = rec[2 * i + 1];
                 r0[hh] = rec[2 * i];
             }
+            pf_pos = pos + 64;
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const uint32_t e = pf_pos + 32 * hh + lane;
+                pf[hh] = e < cend ? clist[e] : 0xffffffffu;
+            }
+            // The warp's block lies inside the tile, so "box overlaps the active rectangle" implies
+            // "box covers the tile": the per-tile list filter is implied (lists hold visible Gaussians only).
 #pragma unroll
             for (int hh = 0; hh < 2; hh++) {
                 const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
                 const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                keep[hh] = idx[hh] < n && gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
-                           tyi <= (gy1 >> 4) && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
+                keep[hh] = idx[hh] < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
                            ellipse_may_touch2(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
                                               __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
                                               __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);

@@ -243,22 +243,23 @@ ta_status ta_context_destroy(ta_context* c) {
 
 namespace {
 
-// Coarse-binning geometry for an H x W target: 32 x 32-pixel bins, difference-grid pitch,
-// warps per block (per-warp shared state must fit), P = partitions (warps).
-ta_status bin_geometry(ta_context* c, int H, int W, BinGeom* bg, int* nwb) {
+// Coarse-binning geometry for an H x W target and up to cap Gaussians: 32 x 32-pixel bins, warps per
+// binning block (per-warp [NB] cursors + lane masks must fit in shared memory), P = rank tiles of
+// nw * 256 ranks.
+ta_status bin_geometry(ta_context* c, int H, int W, int64_t cap, BinGeom* bg) {
     bg->shift = kCoarseShift;
     const int bs = 1 << kCoarseShift;
     bg->TX = (W + bs - 1) / bs;
     bg->TY = (H + bs - 1) / bs;
-    bg->GW = (bg->TX + 1) | 1;
-    bg->GS = (bg->TY + 1) * bg->GW;
-    const size_t per_warp = (size_t)std::max(bg->GS, bg->TX * bg->TY) * 4;
+    const int NB = bg->TX * bg->TY;
+    const size_t per_warp = (size_t)NB * 8;      // write cursors + lane masks
     const size_t budget = c->smem_optin > 4096 ? c->smem_optin - 1024 : 0;
-    int w = (int)std::min<size_t>(16, budget / per_warp);
+    int w = (int)std::min<size_t>(8, budget / per_warp);
     if (w < 1) return fail(c, TA_ERR_UNSUPPORTED, "target of %d x %d coarse bins exceeds the binning shared-memory budget",
                            bg->TX, bg->TY);
-    *nwb = w;
-    bg->P = (uint32_t)(c->num_sms * w);
+    bg->nw = w;
+    const uint64_t R = kBinTileRanks(w);
+    bg->P = (uint32_t)(((uint64_t)std::max<int64_t>(cap, 1) + R - 1) / R);
     return TA_OK;
 }
 
@@ -321,8 +322,7 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     ta_status st;
     if ((st = reserve_gaussians(c, max_gaussians)) != TA_OK) return st;
     BinGeom bg;
-    int nwb;
-    if ((st = bin_geometry(c, H, W, &bg, &nwb)) != TA_OK) return st;
+    if ((st = bin_geometry(c, H, W, max_gaussians, &bg)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, max_gaussians, H, W)) != TA_OK) return st;
     if ((st = grow(c, c->list, (size_t)std::max<int64_t>(max_entries, 1) * 4)) != TA_OK) return st;
     return TA_OK;
@@ -425,10 +425,9 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const bool async = (p->flags & TA_FLAG_ASYNC) != 0;
     const bool counts = (p->flags & TA_FLAG_DEBUG_COUNTS) != 0;
 
-    BinGeom bg;
-    int nwb;
-    if ((st = bin_geometry(c, H, W, &bg, &nwb)) != TA_OK) return st;
     const int64_t cap = n >= 0 ? n : g->capacity;
+    BinGeom bg;
+    if ((st = bin_geometry(c, H, W, cap, &bg)) != TA_OK) return st;
     const int NB = bg.TX * bg.TY;                      // coarse bins
     const uint32_t bin_len = (uint32_t)NB * bg.P + 1;
     const CompositeGeom cg = composite_geometry(bg, H, W);
@@ -485,19 +484,20 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
             launch_scan(hist, &cs->sort_len, 256 * parts_max, status + (size_t)pass * region, &cs->scan_counter[pass],
                         &cs->sort_total, s);
             TA_LAUNCHED(c);
-            k_sort_scatter<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs, hist);
+            k_sort_scatter<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs, hist, rec,
+                                                                   (uint2*)c->boxes.p);
             TA_LAUNCHED(c);
         }
     }
     tm.end();
-    const size_t smem_count = (size_t)nwb * bg.GS * 4;
-    const size_t smem_place = (size_t)nwb * NB * 4;
+    const size_t smem_count = (size_t)NB * 4;
+    const size_t smem_place = (size_t)bg.nw * NB * 8;
     tm.begin(TA_STAGE_BIN_COUNT);
     if (cap_blocks > 0) {
         k_gather_boxes<<<(unsigned)cap_blocks, 256, 0, s>>>(rec, v0, v1, cs, (uint2*)c->boxes.p);
         TA_LAUNCHED(c);
     }
-    k_bin_count<<<c->num_sms, nwb * 32, smem_count, s>>>((const uint2*)c->boxes.p, cs, bg, offs);
+    k_bin_count<<<bg.P, bg.nw * 32, smem_count, s>>>((const uint2*)c->boxes.p, cs, bg, offs);
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_BIN_SCAN);
@@ -512,8 +512,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     }
     tm.end();
     tm.begin(TA_STAGE_BIN_PLACE);
-    k_bin_place<<<c->num_sms, nwb * 32, smem_place, s>>>((const uint2*)c->boxes.p, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
-                                                        (uint64_t)(c->list.bytes / 4));
+    k_bin_place<<<bg.P, bg.nw * 32, smem_place, s>>>((const uint2*)c->boxes.p, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
+                                                     (uint64_t)(c->list.bytes / 4));
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);

@@ -20,8 +20,8 @@ struct RasterConsts {
 struct BinGeom {
     int shift;            // bin = (1 << shift) x (1 << shift) pixels (coarse bins: 32 x 32)
     int TX, TY;           // bins per row / column
-    int GW, GS;           // difference-grid row pitch ((TX+1)|1) and size ((TY+1)*GW)
-    uint32_t P;           // binning partitions (warps)
+    int nw;               // warps per k_bin_place block (per-warp [NB] cursors in shared memory)
+    uint32_t P;           // rank tiles = columns of the bin-major [NB x P] run-start matrix
 };
 
 struct ViewDesc {
@@ -60,12 +60,13 @@ __global__ void k_project(const float4* pos_alpha, const float4* cov, TargetCam 
 __global__ void k_sort_hist(const uint32_t* keys_a, const uint32_t* keys_b, int pass, const CallState* cs,
                             uint32_t* hist);
 __global__ void k_sort_scatter(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int pass,
-                               const CallState* cs, const uint32_t* offs);
+                               const CallState* cs, const uint32_t* offs, const uint4* rec, uint2* boxes);
 __global__ void k_gather_boxes(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, const CallState* cs,
                                uint2* boxes);
 __global__ void k_bin_count(const uint2* boxes, const CallState* cs, BinGeom bg, uint32_t* counts);
 __global__ void k_bin_place(const uint2* boxes, const uint32_t* vals_a, const uint32_t* vals_b, CallState* cs,
                             BinGeom bg, const uint32_t* offs, uint32_t* list, uint64_t list_cap);
+constexpr uint32_t kBinTileRanks(int nw) { return (uint32_t)nw * 256u; }
 
 // In-place exclusive scan of data[0 .. len) with len = *len_ptr (device) or len_max (len_ptr NULL);
 // status (>= len_max/4096 + 1 words) and *counter must be zero.

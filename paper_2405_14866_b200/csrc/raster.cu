@@ -6,14 +6,11 @@
 //                   depth key scattered BY ID so the depth sort sees id order (tie-break by id)
 //   k_sort_hist / k_scan / k_sort_scatter   x passes: stable LSD radix sort of the depth keys over
 //                   only the bits that vary among visible Gaussians (8-bit digits, per-warp
-//                   partitions, warp-synchronous stable ranking with match.any)
-//   k_bin_count     per-warp tile histograms of a contiguous depth-rank range, via 2-D
-//                   difference arrays (4 updates per Gaussian instead of one per tile)
-//   k_scan          over the tile-major [T x P] count matrix -> every (tile, warp) list offset,
-//                   tile ranges and the entry total K in one flat exclusive scan
-//   k_bin_place     each warp walks its depth-rank range in order and appends the Gaussian's
-//                   array index to every covered tile's list: lists come out ordered by
-//                   (tile, depth, id) without a global sort over the K entries
+//                   partitions, warp-synchronous stable ranking with ballot multisplit)
+//   k_bin_count     per-tile (consecutive depth ranks) counts of the coarse (32 x 32-pixel) bins
+//   k_scan          flat exclusive scan of the bin-major [bins x tiles] counts -> run starts, K
+//   k_bin_place     per tile: per-warp cursors, then every (Gaussian, bin) entry appended in rank
+//                   order: lists come out ordered by (bin, depth, id) without a sort over K entries
 #include "common.cuh"
 #include "scan.cuh"
 #include "internal.h"
@@ -138,7 +135,7 @@ __global__ void __launch_bounds__(256) k_project(const float4* __restrict__ pos_
 // Pass `pass` sorts by 8 bits starting at sort_shift(); keys/vals ping-pong a -> b -> a ...
 // Inactive passes (beyond the varying bits) return immediately.  A block owns kSortKeysPerBlock
 // consecutive keys, each warp kSortKeysPerWarp of them in order; warps rank their keys stably
-// (match.any per 32-key chunk, per-warp digit counters), the block combines warps in order.
+// (ballot multisplit per 32-key chunk, per-warp digit counters), the block combines warps in order.
 __global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* __restrict__ keys_a,
                                                                const uint32_t* __restrict__ keys_b, int pass,
                                                                const CallState* __restrict__ cs,
@@ -178,13 +175,17 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* _
     hist[(size_t)d * parts + blockIdx.x] = sum;
 }
 
+// The last pass also writes the pixel box of every rank (boxes[rank]) for the binning kernels.
 __global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __restrict__ keys_a, uint32_t* __restrict__ keys_b,
                                                                   uint32_t* __restrict__ vals_a, uint32_t* __restrict__ vals_b,
                                                                   int pass, const CallState* __restrict__ cs,
-                                                                  const uint32_t* __restrict__ offs) {
+                                                                  const uint32_t* __restrict__ offs,
+                                                                  const uint4* __restrict__ rec, uint2* __restrict__ boxes) {
     constexpr int kChunks = kSortKeysPerWarp / 32;
     __shared__ uint32_t s_off[kSortWarps][256];
-    if (pass >= sort_passes(cs)) return;
+    const int npass = sort_passes(cs);
+    if (pass >= npass) return;
+    const bool last = pass == npass - 1;
     const uint32_t parts = cs->sort_parts;
     if (blockIdx.x >= parts) return;
     const uint32_t* sk = (pass & 1) ? keys_b : keys_a;
@@ -236,174 +237,163 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __re
             const uint32_t pos = cnt[(key[k] >> shift) & 255u] + rank[k];
             dk[pos] = key[k];
             dv[pos] = val[k];
+            if (last) {
+                const uint4 q = rec[2 * val[k] + 1];
+                boxes[pos] = make_uint2(q.z, q.w);
+            }
         }
     }
 }
 
 // ----------------------------------------------------------------------------- binning
-__device__ __forceinline__ void rank_range(uint32_t n, uint32_t P, uint32_t p, uint32_t* rb, uint32_t* re) {
-    *rb = (uint32_t)(((uint64_t)n * p) / P);
-    *re = (uint32_t)(((uint64_t)n * (p + 1)) / P);
-}
+// Coarse bins are (1 << shift)-pixel squares.  The per-bin lists hold the array index of every
+// visible Gaussian whose pixel box overlaps the bin, in depth-rank order: a stable counting sort
+// of the (Gaussian, bin) entries by bin, the entries being generated on the fly from the
+// rank-ordered boxes.  The ranks are cut into P tiles of R = nw * 256 consecutive ranks:
+//   k_bin_count  per-tile bin counts -> counts[bin * P + tile] (bin-major)
+//   (scan)       one flat exclusive scan: the start of every (bin, tile) run, K = entries
+//   k_bin_place  per tile: per-warp bin counts, exclusive scan over the warps (cursors), then each
+//                warp re-walks its ranks and appends every entry at its cursor: lists come out in
+//                (bin, depth, id) order.  List of bin b = [offs[b * P], offs[(b + 1) * P]).
+constexpr int kBinRanksPerWarp = 256;
 
-__device__ __forceinline__ const uint32_t* sorted_vals(const CallState* cs, const uint32_t* vals_a,
-                                                       const uint32_t* vals_b) {
-    return (sort_passes(cs) & 1) ? vals_b : vals_a;
-}
-
-// Pixel boxes in depth-rank order (coalesced input for both binning kernels).
+// Pixel boxes in depth-rank order; only used when the depth sort ran no pass (otherwise the last
+// scatter pass writes them).
 __global__ void __launch_bounds__(256) k_gather_boxes(const uint4* __restrict__ rec, const uint32_t* __restrict__ vals_a,
                                                       const uint32_t* __restrict__ vals_b,
                                                       const CallState* __restrict__ cs, uint2* __restrict__ boxes) {
+    if (sort_passes(cs) > 0) return;
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= cs->n) return;
-    const uint32_t* sorted = sorted_vals(cs, vals_a, vals_b);
-    const uint4 q = rec[2 * sorted[r] + 1];
+    const uint4 q = rec[2 * vals_a[r] + 1];
     boxes[r] = make_uint2(q.z, q.w);
 }
 
-// Per-warp tile counts over depth ranks [rb, re): 2-D difference array on a (TY+1) x GW grid
-// (GW = (TX+1)|1, odd to spread banks), prefix-summed in place, then written tile-major
-// into counts[t * P + p].  The last element counts[T*P] is zeroed (it becomes K after the scan).
-__global__ void __launch_bounds__(512) k_bin_count(const uint2* __restrict__ boxes, const CallState* __restrict__ cs,
-                                                   BinGeom bg, uint32_t* __restrict__ counts) {
-    extern __shared__ int32_t s_grid[];
-    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    const int nw = blockDim.x >> 5;
-    const int GW = bg.GW, GH = bg.TY + 1, GS = bg.GS;
-    int32_t* grid = s_grid + (size_t)warp * GS;
-    for (int k = lane; k < GS; k += 32) grid[k] = 0;
-    __syncwarp();
-    const uint32_t p = blockIdx.x * nw + warp;
-    uint32_t rb, re;
-    rank_range(cs->n, bg.P, p, &rb, &re);
-    uint2 nxt = rb + lane < re ? boxes[rb + lane] : make_uint2(kEmptyRect, kEmptyRect);
-    for (uint32_t r0 = rb; r0 < re; r0 += 32) {
-        const uint2 bx = nxt;
-        nxt = r0 + 32 + lane < re ? boxes[r0 + 32 + lane] : make_uint2(kEmptyRect, kEmptyRect);
-        bool ok = r0 + lane < re;
-        const uint32_t rx = bx.x, ry = bx.y;
-        const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-        ok = ok && x0 <= x1 && y0 <= y1;
-        const int sh = bg.shift;
-        const int tx0 = x0 >> sh, tx1 = (x1 >> sh) + 1, ty0 = y0 >> sh, ty1 = (y1 >> sh) + 1;
-#pragma unroll
-        for (int corner = 0; corner < 4; corner++) {
-            const int cy = (corner & 2) ? ty1 : ty0;
-            const int cx = (corner & 1) ? tx1 : tx0;
-            const int sign = (corner == 0 || corner == 3) ? 1 : -1;
-            const uint32_t cell = ok ? (uint32_t)(cy * GW + cx) : (0x80000000u | lane);
-            const uint32_t peers = __match_any_sync(0xffffffffu, cell);
-            if (ok && lane == (uint32_t)(__ffs(peers) - 1)) grid[cell] += sign * __popc(peers);
-            __syncwarp();
-        }
-    }
-    // 2-D inclusive prefix: rows, then columns
-    for (int row = lane; row < GH; row += 32) {
-        int32_t acc = 0;
-        int32_t* g = grid + row * GW;
-        for (int x = 0; x < GW; x++) { acc += g[x]; g[x] = acc; }
-    }
-    __syncwarp();
-    for (int col = lane; col < GW; col += 32) {
-        int32_t acc = 0;
-        for (int y = 0; y < GH; y++) { acc += grid[y * GW + col]; grid[y * GW + col] = acc; }
-    }
-    __syncthreads();
-    const int T = bg.TX * bg.TY;
-    for (int k = threadIdx.x; k < T * nw; k += blockDim.x) {
-        const int t = k / nw, w = k % nw;
-        const uint32_t pp = blockIdx.x * nw + w;
-        const int ty = t / bg.TX, tx = t - ty * bg.TX;
-        counts[(size_t)t * bg.P + pp] = (uint32_t)s_grid[(size_t)w * GS + ty * GW + tx];
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) counts[(size_t)T * bg.P] = 0u;
+__device__ __forceinline__ bool box_bins(uint2 bx, int sh, int* bx0, int* bx1, int* by0, int* by1) {
+    const int x0 = bx.x & 0xffff, x1 = bx.x >> 16, y0 = bx.y & 0xffff, y1 = bx.y >> 16;
+    *bx0 = x0 >> sh;
+    *bx1 = x1 >> sh;
+    *by0 = y0 >> sh;
+    *by1 = y1 >> sh;
+    return x0 <= x1 && y0 <= y1;
 }
 
-// Each warp appends its depth-rank range to the tile lists, in rank order.  32 consecutive
-// (Gaussian, tile) entries per step; same-tile entries inside a step are ordered by lane with
-// match.any, so each list stays ordered by (depth, id).
-__global__ void __launch_bounds__(512) k_bin_place(const uint2* __restrict__ boxes, const uint32_t* __restrict__ vals_a,
-                                                   const uint32_t* __restrict__ vals_b,
-                                                   CallState* __restrict__ cs, BinGeom bg,
-                                                   const uint32_t* __restrict__ offs, uint32_t* __restrict__ list,
-                                                   uint64_t list_cap) {
-    extern __shared__ uint32_t s_run[];
+// Adds 1 to cnt[bin] for every bin of the box (row-major walk of the bin rectangle).
+__device__ __forceinline__ void count_box(uint32_t* cnt, uint2 box, const BinGeom& bg) {
+    int x0, x1, y0, y1;
+    if (!box_bins(box, bg.shift, &x0, &x1, &y0, &y1)) return;
+    for (int y = y0; y <= y1; y++)
+        for (int x = x0; x <= x1; x++) atomicAdd(&cnt[y * bg.TX + x], 1u);
+}
+
+__global__ void __launch_bounds__(256) k_bin_count(const uint2* __restrict__ boxes, const CallState* __restrict__ cs,
+                                                   BinGeom bg, uint32_t* __restrict__ counts) {
+    extern __shared__ uint32_t s_h[];
+    const int NB = bg.TX * bg.TY;
+    const uint32_t tile = blockIdx.x, P = gridDim.x;
+    for (int k = threadIdx.x; k < NB; k += blockDim.x) s_h[k] = 0u;
+    if (tile == 0 && threadIdx.x == 0) counts[(size_t)NB * P] = 0u;
+    __syncthreads();
+    const uint32_t n = cs->n;
+    const uint32_t R = (uint32_t)bg.nw * kBinRanksPerWarp;
+    const uint32_t r1 = min(n, (tile + 1) * R);
+    for (uint32_t r = tile * R + threadIdx.x; r < r1; r += blockDim.x) count_box(s_h, boxes[r], bg);
+    __syncthreads();
+    for (int k = threadIdx.x; k < NB; k += blockDim.x) counts[(size_t)k * P + tile] = s_h[k];
+}
+
+__global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ boxes, const uint32_t* __restrict__ vals_a,
+                                                   const uint32_t* __restrict__ vals_b, CallState* __restrict__ cs,
+                                                   BinGeom bg, const uint32_t* __restrict__ offs,
+                                                   uint32_t* __restrict__ list, uint64_t list_cap) {
+    extern __shared__ uint32_t s_cnt[];          // [nw][NB] counts, then write cursors; [nw][NB] lane masks
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     const int nw = blockDim.x >> 5;
-    const int T = bg.TX * bg.TY;
-    for (int k = threadIdx.x; k < T * nw; k += blockDim.x) {
-        const int t = k / nw, w = k % nw;
-        s_run[(size_t)w * T + t] = offs[(size_t)t * bg.P + blockIdx.x * nw + w];
+    const int NB = bg.TX * bg.TY;
+    const uint32_t n = cs->n;
+    const uint32_t tile = blockIdx.x, P = gridDim.x;
+    for (int k = threadIdx.x; k < (nw * NB) / 2; k += blockDim.x)       // 2 nw NB words (NB even or not)
+        reinterpret_cast<uint4*>(s_cnt)[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (threadIdx.x == 0 && (nw * NB) % 2) { s_cnt[2 * nw * NB - 2] = 0u; s_cnt[2 * nw * NB - 1] = 0u; }
+    __syncthreads();
+    const uint32_t R = (uint32_t)nw * kBinRanksPerWarp;
+    if ((uint64_t)tile * R >= n) return;
+    const uint32_t* sorted = (sort_passes(cs) & 1) ? vals_b : vals_a;
+    const uint32_t wr0 = tile * R + warp * kBinRanksPerWarp;
+    const uint32_t wr1 = min(n, wr0 + kBinRanksPerWarp);
+    uint32_t* run = s_cnt + (size_t)warp * NB;
+    // ---- per-warp bin counts of the warp's ranks
+    for (uint32_t r = wr0 + lane; r < wr1; r += 32) count_box(run, boxes[r], bg);
+    __syncthreads();
+    // ---- per bin: cursors = start of the (bin, tile) run + entries of the earlier warps
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+        uint32_t cur = offs[(size_t)b * P + tile];
+        for (int w = 0; w < nw; w++) {
+            const uint32_t c = s_cnt[w * NB + b];
+            s_cnt[w * NB + b] = cur;
+            cur += c;
+        }
     }
     __syncthreads();
-    uint32_t* run = s_run + (size_t)warp * T;
-    const uint32_t* sorted = sorted_vals(cs, vals_a, vals_b);
-    const uint32_t p = blockIdx.x * nw + warp;
-    const uint32_t lt = lanemask_lt();
-    uint32_t rb, re;
-    rank_range(cs->n, bg.P, p, &rb, &re);
-    bool overflow = false;
-    uint32_t nidx = rb + lane < re ? sorted[rb + lane] : 0u;
-    uint2 nbx = rb + lane < re ? boxes[rb + lane] : make_uint2(kEmptyRect, kEmptyRect);
-    for (uint32_t r0 = rb; r0 < re; r0 += 32) {
-        const uint32_t idx = nidx;
-        const uint32_t rx = nbx.x, ry = nbx.y;
-        const uint32_t rn = r0 + 32 + lane;
-        nidx = rn < re ? sorted[rn] : 0u;
-        nbx = rn < re ? boxes[rn] : make_uint2(kEmptyRect, kEmptyRect);
-        const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-        const bool ok = x0 <= x1 && y0 <= y1;
-        const int sh = bg.shift;
-        const int tx0 = x0 >> sh, ty0 = y0 >> sh;
-        const int tw = ok ? (x1 >> sh) - tx0 + 1 : 1;
-        const uint32_t cnt = ok ? (uint32_t)(tw * ((y1 >> sh) - ty0 + 1)) : 0u;
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
+    // ---- phase B: each warp re-walks its ranks in order, one Gaussian per lane, looping over the
+    //      bins of its box.  Same-bin entries of one 32-Gaussian step are ranked by lane through a
+    //      per-warp lane bitmask per bin (set, read, then cleared by the lowest lane of the mask).
+    const uint32_t mbase = (uint32_t)(nw + warp) * NB, rbase = warp * (uint32_t)NB;
+    const uint32_t lt = lanemask_lt(), bit = 1u << lane;
+    const uint32_t cap32 = (uint32_t)min(list_cap, (uint64_t)0xffffffffu);
+    uint32_t overflow = 0u;
+    for (uint32_t r0 = wr0; r0 < wr1; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t idx = 0u;
+        int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
+        bool ok = false;
+        if (r < wr1) {
+            ok = box_bins(boxes[r], bg.shift, &x0, &x1, &y0, &y1);
+            idx = sorted[r];
         }
-        const uint32_t excl = incl - cnt;
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t org = (uint32_t)tx0 | ((uint32_t)ty0 << 16);
-        for (uint32_t e0 = 0; e0 < total; e0 += 32) {
-            const uint32_t j = e0 + lane;
-            const bool valid = j < total;
-            // largest window lane k with excl_k <= j (always a lane with cnt_k > 0)
-            int k = 0;
-#pragma unroll
-            for (int s = 16; s >= 1; s >>= 1) {
-                const uint32_t ex = __shfl_sync(0xffffffffu, excl, k + s);
-                if (ex <= j) k += s;
+        const int tw = x1 - x0 + 1;
+        const int cnt = ok ? tw * (y1 - y0 + 1) : 0;
+        const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+        const uint32_t t0 = (uint32_t)(y0 * bg.TX + x0), stride = (uint32_t)(bg.TX - tw);
+#pragma unroll 1
+        for (int i = 0, xi = 0, t = t0; i < maxc; i++) {
+            if (i < cnt) {
+                atomicOr(&s_cnt[mbase + t], bit);
+                t++;
+                if (++xi == tw) { xi = 0; t += stride; }
             }
-            const uint32_t ex_k = __shfl_sync(0xffffffffu, excl, k);
-            const uint32_t idx_k = __shfl_sync(0xffffffffu, idx, k);
-            const uint32_t org_k = __shfl_sync(0xffffffffu, org, k);
-            const int tw_k = __shfl_sync(0xffffffffu, tw, k);
-            const int m = (int)(j - ex_k);
-            int row = (int)__fmul_rz((float)m + 0.5f, __frcp_rn((float)tw_k));
-            if (row * tw_k > m) row--;
-            if ((row + 1) * tw_k <= m) row++;
-            const int col = m - row * tw_k;
-            const uint32_t t = (uint32_t)(((int)(org_k >> 16) + row) * bg.TX + (int)(org_k & 0xffff) + col);
-            const uint32_t key = valid ? t : (0x80000000u | lane);
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            const uint32_t base = valid ? run[t] : 0u;
-            __syncwarp();
-            if (valid) {
-                const uint32_t pos = base + __popc(peers & lt);
-                if (pos < list_cap) list[pos] = idx_k;
-                else overflow = true;
-                if (lane == (uint32_t)(__ffs(peers) - 1)) run[t] = base + __popc(peers);
-            }
-            __syncwarp();
         }
+        __syncwarp();
+#pragma unroll 1
+        for (int i = 0, xi = 0, t = t0; i < maxc; i++) {
+            if (i < cnt) {
+                const uint32_t pos = s_cnt[rbase + t] + __popc(s_cnt[mbase + t] & lt);
+                if (pos < cap32) list[pos] = idx;
+                else overflow = 1u;
+                t++;
+                if (++xi == tw) { xi = 0; t += stride; }
+            }
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int i = 0, xi = 0, t = t0; i < maxc; i++) {
+            if (i < cnt) {
+                const uint32_t m = s_cnt[mbase + t];
+                if ((m & bit) && !(m & lt)) {          // lowest lane of the mask: advance the cursor, clear
+                    s_cnt[rbase + t] += __popc(m);
+                    s_cnt[mbase + t] = 0u;
+                }
+                t++;
+                if (++xi == tw) { xi = 0; t += stride; }
+            }
+        }
+        __syncwarp();
     }
     if (overflow) atomicOr(&cs->overflow, 1u);
 }
 
 }  // namespace ta
+
 
 namespace ta {
 void launch_scan(uint32_t* data, const uint32_t* len_ptr, uint32_t len_max, unsigned long long* status,

@@ -566,15 +566,36 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     uint32_t actA = (px < W && pyA < H) ? (1u << lane) : 0u;
     uint32_t actB = (px < W && pyB < H) ? (1u << lane) : 0u;
 
+    // Compacted mode (entered once, when at most 32 of the 64 pixels still composite): each such pixel
+    // moves to its own lane (original lane ol, half hs -> weight column p' = 2 ol + hs) and the packed
+    // fp32x2 arithmetic runs over pairs of entries instead of pairs of pixels, so the warp walks the
+    // rest of the list at twice the rate.  T and the decisions keep the same fp32 sequence.
+    bool modeB = false, movedA = false, movedB = false, chas = false;
+    int ol = 0, hs = 0, cpx = 0, cpy = 0, nc1 = 0;
+    float T1 = 1.0f;
+    uint32_t act1 = 0u;
+
     unsigned long long wk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t pos = cstart;
     uint32_t pf_pos = 0xffffffffu, pf[2] = {0u, 0u};     // prefetched list indices of entries pf_pos + [0, 64)
-    while (pos < cend && __any_sync(0xffffffffu, (actA | actB) != 0u)) {
+    while (pos < cend && __any_sync(0xffffffffu, (actA | actB | act1) != 0u)) {
         // culling rectangle = bounding box of the pixels still compositing
-        const int ax0 = __reduce_min_sync(0xffffffffu, (actA | actB) ? px : 0x7fffffff);
-        const int ax1 = __reduce_max_sync(0xffffffffu, (actA | actB) ? px : -1);
-        const int ay0 = __reduce_min_sync(0xffffffffu, actA ? pyA : (actB ? pyB : 0x7fffffff));
-        const int ay1 = __reduce_max_sync(0xffffffffu, actB ? pyB : (actA ? pyA : -1));
+        int lx0, lx1, ly0, ly1;
+        if (!modeB) {
+            lx0 = (actA | actB) ? px : 0x7fffffff;
+            lx1 = (actA | actB) ? px : -1;
+            ly0 = actA ? pyA : (actB ? pyB : 0x7fffffff);
+            ly1 = actB ? pyB : (actA ? pyA : -1);
+        } else {
+            lx0 = act1 ? cpx : 0x7fffffff;
+            lx1 = act1 ? cpx : -1;
+            ly0 = act1 ? cpy : 0x7fffffff;
+            ly1 = act1 ? cpy : -1;
+        }
+        const int ax0 = __reduce_min_sync(0xffffffffu, lx0);
+        const int ax1 = __reduce_max_sync(0xffffffffu, lx1);
+        const int ay0 = __reduce_min_sync(0xffffffffu, ly0);
+        const int ay1 = __reduce_max_sync(0xffffffffu, ly1);
         const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
         // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip.
         //      The list indices of the next 64 entries are loaded one round ahead (pf_pos / pf).
@@ -661,6 +682,95 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         // ---- composite the staged entries, 16 at a time: SIMT weights -> smem -> tensor cores
         for (int j0 = 0; j0 < cnt; j0 += 16) {
             const int nk = min(16, cnt - j0);
+            if (!modeB) {
+                const uint32_t mA = __ballot_sync(0xffffffffu, actA != 0u), mB = __ballot_sync(0xffffffffu, actB != 0u);
+                const int nA = __popc(mA), na = nA + __popc(mB);
+                if (na <= 32) {                           // enter the compacted mode (warp-uniform)
+                    modeB = true;
+                    movedA = actA != 0u;
+                    movedB = actB != 0u;
+                    const bool has = li < na;
+                    int src = 0;
+                    hs = 0;
+                    if (has) {
+                        if (li < nA) src = (int)__fns(mA, 0, li + 1);
+                        else { src = (int)__fns(mB, 0, li - nA + 1); hs = 1; }
+                    }
+                    const float tA = __shfl_sync(0xffffffffu, T.x, src), tB = __shfl_sync(0xffffffffu, T.y, src);
+                    const int cA = __shfl_sync(0xffffffffu, ncA, src), cB = __shfl_sync(0xffffffffu, ncB, src);
+                    ol = src;
+                    T1 = hs ? tB : tA;
+                    nc1 = hs ? cB : cA;
+                    act1 = has ? 1u : 0u;
+                    chas = has;
+                    cpx = bx0 + (ol & 7);
+                    cpy = by0 + (ol >> 3) + 4 * hs;
+                    actA = actB = 0u;
+                    // weight columns of pixels that stopped earlier are never written again: zero them all
+                    uint4* wz = reinterpret_cast<uint4*>(&bf.w[0][0][0]);
+                    for (int k = li; k < 2 * 16 * WP / 4; k += 32) wz[k] = make_uint4(0u, 0u, 0u, 0u);
+                    __syncwarp();
+                }
+            }
+            if (modeB) {
+                const float cpxf = (float)cpx, cpyf = (float)cpy;
+                __half* const wh = reinterpret_cast<__half*>(&bf.w[0][0][0]) + 2 * ol + hs;   // column p', row 0 (hi)
+#pragma unroll 2
+                for (int jj = 0; jj < 16; jj += 2) {
+                    float w0 = 0.0f, w1 = 0.0f;
+                    if (jj < nk) {
+                        const bool has1 = jj + 1 < nk;
+                        const int j1 = j0 + jj + (has1 ? 1 : 0);
+                        const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
+                        const float4 G1 = bf.g[j1], H1 = bf.h[j1];
+                        // q of entries j, j+1 for this lane's pixel (normative a6 sequence per component)
+                        const float2 dx = sub2(bc2(cpxf), make_float2(G0.x, G1.x));
+                        const float2 dy = sub2(bc2(cpyf), make_float2(G0.y, G1.y));
+                        const float2 t1 = mul2(make_float2(G0.w, G1.w), dy);
+                        const float2 t2 = fma2(make_float2(G0.z, G1.z), dx, t1);
+                        const float2 t4 = mul2(mul2(make_float2(H0.x, H1.x), dy), dy);
+                        const float2 q = fma2(t2, dx, t4);
+                        const uint32_t b0 = __float_as_uint(hs ? H0.w : H0.z), b1 = __float_as_uint(hs ? H1.w : H1.z);
+                        const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : kInf;
+                        const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : kInf;
+                        if (kCounts) wk[2] += has1 ? 2 : 1;
+                        if (__any_sync(0xffffffffu, fminf(qm0, qm1) <= qmax)) {
+                            const float2 e = exp_det2(mul2(bc2(-0.5f), q));
+                            const float2 ae = mul2(make_float2(H0.y, H1.y), e);
+                            const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
+                            const float2 om = sub2(bc2(1.0f), a);
+                            const float2 sc = mul2(a, bc2(2048.0f));
+                            {
+                                const float Tn = fmul(T1, om.x);
+                                const bool ok = qm0 <= qmax && a.x >= amin;
+                                const bool in = ok && Tn >= teps;
+                                if (ok && !in) act1 = 0u;
+                                w0 = in ? fmul(sc.x, T1) : 0.0f;
+                                T1 = in ? Tn : T1;
+                                if (kCounts) nc1 += in ? 1 : 0;
+                            }
+                            {
+                                const float Tn = fmul(T1, om.y);
+                                const bool ok = act1 && qm1 <= qmax && a.y >= amin;
+                                const bool in = ok && Tn >= teps;
+                                if (ok && !in) act1 = 0u;
+                                w1 = in ? fmul(sc.y, T1) : 0.0f;
+                                T1 = in ? Tn : T1;
+                                if (kCounts) nc1 += in ? 1 : 0;
+                            }
+                        }
+                    }
+                    const __half2 hi = __floats2half2_rn(w0, w1);
+                    const float2 hf = __half22float2(hi);
+                    const __half2 lo = __floats2half2_rn(fsub(w0, hf.x), fsub(w1, hf.y));
+                    if (chas) {
+                        wh[jj * 2 * WP] = __low2half(hi);
+                        wh[(jj + 1) * 2 * WP] = __high2half(hi);
+                        wh[(16 + jj) * 2 * WP] = __low2half(lo);
+                        wh[(16 + jj + 1) * 2 * WP] = __high2half(lo);
+                    }
+                }
+            } else {
 #pragma unroll
             for (int jj = 0; jj < 16; jj += 2) {
                 float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
@@ -703,6 +813,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 wst[16 * WP + jj * WP] = *reinterpret_cast<const uint32_t*>(&l0);
                 wst[16 * WP + (jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&l1);
             }
+            }
             __syncwarp();
             // B fragments: feature rows j0 .. j0+15 (rows past cnt carry weight 0: clamp to a staged row)
             uint32_t bfr[NT][2];
@@ -729,7 +840,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 }
             }
             __syncwarp();
-            if (!__any_sync(0xffffffffu, (actA | actB) != 0u)) break;
+            if (!__any_sync(0xffffffffu, (actA | actB | act1) != 0u)) break;
         }
         __syncwarp();
     }
@@ -761,11 +872,16 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 #pragma unroll
     for (int hh = 0; hh < 2; hh++) {
         const int py = hh ? pyB : pyA;
-        if (px < W && py < H) {
+        if (px < W && py < H && !(hh ? movedB : movedA)) {        // moved pixels are written by their new lane
             const size_t pix = (size_t)py * W + px;
             Aout[pix] = fsub(1.0f, hh ? T.y : T.x);
             if (kCounts) ncontrib[pix] = hh ? ncB : ncA;
         }
+    }
+    if (modeB && chas) {
+        const size_t pix = (size_t)cpy * W + cpx;
+        Aout[pix] = fsub(1.0f, T1);
+        if (kCounts) ncontrib[pix] = nc1;
     }
 }
 

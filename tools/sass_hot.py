@@ -41,5 +41,5 @@ if len(sys.argv) > 2 and sys.argv[2] == 'blocks':
             cur = [i, i, e, p, 1]
     runs.append(cur)
     runs.sort(key=lambda r: -r[2] * r[4])
-    for r in runs[:40]:
+    for r in runs[:int(sys.argv[3]) if len(sys.argv) > 3 else 40]:
         print(f"  [{r[0]:5d}-{r[1]:5d}] n={r[4]:3d} exec={r[2]:>11,}  inst={r[2]*r[4]/tot*100:5.1f}%  samples={r[3]/max(ts,1)*100:5.1f}%   {recs[r[0]][1][:60]}")

@@ -12,6 +12,7 @@
 // normative fp32 sequence (DESIGN.md a6) bit for bit; the C accumulators are fp32 FMAs.
 // Warps retire when all their pixels stopped (__all_sync); the CTA leaves the list as soon
 // as every pixel stopped (__syncthreads_count).
+#include <type_traits>
 #include "common.cuh"
 #include "internal.h"
 
@@ -512,6 +513,10 @@ __device__ __forceinline__ float2 tstep(float2 qm, float2 a, float qmax, float a
     return w;
 }
 
+// Skip the exp / recurrence of an entry pair no pixel can take (saves ~13 % of pairs, but the
+// warp-wide vote + branch splits the unrolled loop into basic blocks the scheduler cannot overlap).
+constexpr bool kSkipEmptyPairs = false;
+
 template <int C, bool kCounts>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
@@ -734,7 +739,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : kInf;
                         const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : kInf;
                         if (kCounts) wk[2] += has1 ? 2 : 1;
-                        if (__any_sync(0xffffffffu, fminf(qm0, qm1) <= qmax)) {
+                        if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(qm0, qm1) <= qmax)) {
                             const float2 e = exp_det2(mul2(bc2(-0.5f), q));
                             const float2 ae = mul2(make_float2(H0.y, H1.y), e);
                             const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
@@ -771,48 +776,55 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                     }
                 }
             } else {
+                // full chunks (16 staged entries) take a branch-free copy of the pair loop, so the
+                // scheduler can overlap consecutive pairs; the last, partial chunk keeps the guards
+                auto pairs = [&](auto full) {
+                    constexpr bool kFull = decltype(full)::value;
 #pragma unroll
-            for (int jj = 0; jj < 16; jj += 2) {
-                float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
-                if (jj < nk) {                                   // warp-uniform
-                    const int j1 = j0 + jj + (jj + 1 < nk ? 1 : 0);
-                    const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
-                    const float4 G1 = bf.g[j1], H1 = bf.h[j1];
-                    // q of both entries for both pixels; qm = q where the pixel is in the entry's box and
-                    // still compositing, else +inf (so "qm <= q_max" is the whole per-pixel geometric test)
-                    const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
-                    const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : kInf,
-                                                   (__float_as_uint(H0.w) & actB) ? q0.y : kInf);
-                    float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : kInf,
-                                             (__float_as_uint(H1.w) & actB) ? q1.y : kInf);
-                    if (jj + 1 >= nk) qm1 = make_float2(kInf, kInf);
-                    if (kCounts) wk[2] += (jj + 1 < nk) ? 2 : 1;
-                    if (__any_sync(0xffffffffu, fminf(fminf(qm0.x, qm0.y), fminf(qm1.x, qm1.y)) <= qmax)) {
-                        // exp / alpha' of both entries are independent of T: computed side by side
-                        const float2 x0 = exp_det2(mul2(bc2(-0.5f), q0));
-                        const float2 x1 = exp_det2(mul2(bc2(-0.5f), q1));
-                        const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);
-                        const float2 a0 = make_float2(fminf(amax, ae0.x), fminf(amax, ae0.y));
-                        const float2 a1 = make_float2(fminf(amax, ae1.x), fminf(amax, ae1.y));
-                        if (kCounts) {
-                            wk[3] += __any_sync(0xffffffffu, fminf(qm0.x, qm0.y) <= qmax) ? 1 : 0;
-                            wk[3] += __any_sync(0xffffffffu, fminf(qm1.x, qm1.y) <= qmax) ? 1 : 0;
+                    for (int jj = 0; jj < 16; jj += 2) {
+                        float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
+                        if (kFull || jj < nk) {                          // warp-uniform
+                            const int j1 = j0 + jj + ((kFull || jj + 1 < nk) ? 1 : 0);
+                            const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
+                            const float4 G1 = bf.g[j1], H1 = bf.h[j1];
+                            // q of both entries for both pixels; qm = q where the pixel is in the entry's box and
+                            // still compositing, else +inf (so "qm <= q_max" is the whole per-pixel geometric test)
+                            const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
+                            const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : kInf,
+                                                           (__float_as_uint(H0.w) & actB) ? q0.y : kInf);
+                            float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : kInf,
+                                                     (__float_as_uint(H1.w) & actB) ? q1.y : kInf);
+                            if (!kFull && jj + 1 >= nk) qm1 = make_float2(kInf, kInf);
+                            if (kCounts) wk[2] += (kFull || jj + 1 < nk) ? 2 : 1;
+                            if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(fminf(qm0.x, qm0.y), fminf(qm1.x, qm1.y)) <= qmax)) {
+                                // exp / alpha' of both entries are independent of T: computed side by side
+                                const float2 x0 = exp_det2(mul2(bc2(-0.5f), q0));
+                                const float2 x1 = exp_det2(mul2(bc2(-0.5f), q1));
+                                const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);
+                                const float2 a0 = make_float2(fminf(amax, ae0.x), fminf(amax, ae0.y));
+                                const float2 a1 = make_float2(fminf(amax, ae1.x), fminf(amax, ae1.y));
+                                if (kCounts) {
+                                    wk[3] += __any_sync(0xffffffffu, fminf(qm0.x, qm0.y) <= qmax) ? 1 : 0;
+                                    wk[3] += __any_sync(0xffffffffu, fminf(qm1.x, qm1.y) <= qmax) ? 1 : 0;
+                                }
+                                w0 = tstep<kCounts>(qm0, a0, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                                // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
+                                qm1 = make_float2(actA ? qm1.x : kInf, actB ? qm1.y : kInf);
+                                w1 = tstep<kCounts>(qm1, a1, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                            }
                         }
-                        w0 = tstep<kCounts>(qm0, a0, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
-                        // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
-                        qm1 = make_float2(actA ? qm1.x : kInf, actB ? qm1.y : kInf);
-                        w1 = tstep<kCounts>(qm1, a1, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                        // split into fp16 hi / lo and store rows jj, jj+1
+                        const __half2 h0 = __floats2half2_rn(w0.x, w0.y), h1 = __floats2half2_rn(w1.x, w1.y);
+                        const float2 r0 = sub2(w0, __half22float2(h0)), r1 = sub2(w1, __half22float2(h1));
+                        const __half2 l0 = __floats2half2_rn(r0.x, r0.y), l1 = __floats2half2_rn(r1.x, r1.y);
+                        wst[jj * WP] = *reinterpret_cast<const uint32_t*>(&h0);
+                        wst[(jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&h1);
+                        wst[16 * WP + jj * WP] = *reinterpret_cast<const uint32_t*>(&l0);
+                        wst[16 * WP + (jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&l1);
                     }
-                }
-                // split into fp16 hi / lo and store rows jj, jj+1
-                const __half2 h0 = __floats2half2_rn(w0.x, w0.y), h1 = __floats2half2_rn(w1.x, w1.y);
-                const float2 r0 = sub2(w0, __half22float2(h0)), r1 = sub2(w1, __half22float2(h1));
-                const __half2 l0 = __floats2half2_rn(r0.x, r0.y), l1 = __floats2half2_rn(r1.x, r1.y);
-                wst[jj * WP] = *reinterpret_cast<const uint32_t*>(&h0);
-                wst[(jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&h1);
-                wst[16 * WP + jj * WP] = *reinterpret_cast<const uint32_t*>(&l0);
-                wst[16 * WP + (jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&l1);
-            }
+                };
+                if (nk == 16) pairs(std::integral_constant<bool, true>());
+                else pairs(std::integral_constant<bool, false>());
             }
             __syncwarp();
             // B fragments: feature rows j0 .. j0+15 (rows past cnt carry weight 0: clamp to a staged row)

@@ -24,6 +24,7 @@ struct DevBuf {
 // Scans per rasterize call: depth-sort passes 0..3 use status regions / counters 0..3, the
 // tile-offset scan uses 4.
 constexpr int kScanSlots = 6;   // + slot 5: debug tile-list scan
+constexpr size_t kTilesPerBin = (size_t)1 << (2 * (kCoarseShift - 4));   // 16 x 16 tiles per coarse bin
 
 }  // namespace
 
@@ -34,6 +35,7 @@ struct ta_context {
     std::string err;
     uint64_t launches = 0;
     DevBuf cs, status, rec, boxes, tile_order, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
+    DevBuf tlist, trng;           // per-tile lists (4 x the coarse-list capacity) and their (start, count)
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
     // last rasterize call
@@ -229,7 +231,8 @@ ta_status ta_context_destroy(ta_context* c) {
     if (!c) return TA_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->boxes, &c->tile_order, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
-                      &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list};
+                      &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list,
+                      &c->tlist, &c->trng};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -297,6 +300,7 @@ ta_status reserve_target(ta_context* c, const BinGeom& bg, int64_t cap, int H, i
     {
         const CompositeGeom cg0 = composite_geometry(bg, H, W);
         if ((st = grow(c, c->tile_order, (size_t)cg0.TX * cg0.TY * 4 + 64)) != TA_OK) return st;
+        if ((st = grow(c, c->trng, (size_t)cg0.TX * cg0.TY * 8 + 64)) != TA_OK) return st;
     }
     const size_t parts = ((size_t)std::max<int64_t>(cap, 1) + kSortKeysPerBlock - 1) / kSortKeysPerBlock;
     const CompositeGeom cg = composite_geometry(bg, H, W);
@@ -325,6 +329,7 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     if ((st = bin_geometry(c, H, W, max_gaussians, &bg)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, max_gaussians, H, W)) != TA_OK) return st;
     if ((st = grow(c, c->list, (size_t)std::max<int64_t>(max_entries, 1) * 4)) != TA_OK) return st;
+    if ((st = grow(c, c->tlist, c->list.bytes * kTilesPerBin)) != TA_OK) return st;
     return TA_OK;
 }
 
@@ -409,7 +414,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     if (g->feat_dtype != TA_F32 && g->feat_dtype != TA_F16) return fail(c, TA_ERR_UNSUPPORTED, "unknown dtype");
     if (n < -1 || (n == -1 && !g->n_dev)) return fail(c, TA_ERR_INVALID_ARG, "n = -1 needs g->n_dev");
     if (n > g->capacity) return fail(c, TA_ERR_INVALID_ARG, "n > capacity");
-    if (g->capacity >= (1ll << 31)) return fail(c, TA_ERR_CAPACITY, "capacity >= 2^31");
+    if (g->capacity > (int64_t)kListIdxMask) return fail(c, TA_ERR_CAPACITY, "capacity > 2^28 - 1 Gaussians");
     if ((n != 0) && (!g->pos_alpha || !g->cov || !g->feat)) return fail(c, TA_ERR_INVALID_ARG, "NULL Gaussian array");
     if ((((uintptr_t)g->pos_alpha) | ((uintptr_t)g->cov) | ((uintptr_t)g->feat) | ((uintptr_t)feat_out)) & 15)
         return fail(c, TA_ERR_INVALID_ARG, "Gaussian arrays / feat_out must be 16-byte aligned");
@@ -440,6 +445,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     if ((st = reserve_target(c, bg, cap, H, W)) != TA_OK) return st;
     if (counts && (st = grow(c, c->ncontrib, (size_t)H * W * 4)) != TA_OK) return st;
     if (!c->list.p && (st = grow(c, c->list, (size_t)std::max<int64_t>(cap, 1) * 16)) != TA_OK) return st;
+    if (c->tlist.bytes < c->list.bytes * kTilesPerBin && (st = grow(c, c->tlist, c->list.bytes * kTilesPerBin)) != TA_OK)
+        return st;
 
     TargetCam cam;
     cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
@@ -509,16 +516,23 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
         const uint64_t Kh = c->pinned[0];
         if (Kh > 0xffffffffull) return fail(c, TA_ERR_CAPACITY, "%llu tile entries exceed 2^32-1", (unsigned long long)Kh);
         if (Kh * 4 > c->list.bytes && (st = grow(c, c->list, (size_t)(Kh + Kh / 8 + 1024) * 4)) != TA_OK) return st;
+        if (c->tlist.bytes < c->list.bytes * kTilesPerBin &&
+            (st = grow(c, c->tlist, c->list.bytes * kTilesPerBin)) != TA_OK)
+            return st;
     }
     tm.end();
     tm.begin(TA_STAGE_BIN_PLACE);
     k_bin_place<<<bg.P, bg.nw * 32, smem_place, s>>>((const uint2*)c->boxes.p, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
                                                      (uint64_t)(c->list.bytes / 4));
     TA_LAUNCHED(c);
+    launch_tile_split(rec, (const uint32_t*)c->list.p, offs, cg, cs, (uint64_t)(c->list.bytes / 4), (uint32_t*)c->tlist.p,
+                      (uint64_t)(c->tlist.bytes / 4), (uint2*)c->trng.p, s);
+    TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);
-    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, rec, g->feat, (const uint32_t*)c->list.p,
-                                     offs, (uint32_t*)c->tile_order.p, cg, rc, cs, (uint64_t)(c->list.bytes / 4), feat_out, alpha_out,
+    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, rec, g->feat, (const uint32_t*)c->tlist.p,
+                                     (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
+                                     (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
                                      counts ? (int32_t*)c->ncontrib.p : nullptr, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "composite launch");
     c->launches += 2;   // k_tile_order + k_composite
@@ -544,17 +558,16 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     if (scan_tiles((uint32_t)T + 1) > c->status_region) return fail(c, TA_ERR_CAPACITY, "debug scan status too small");
     TA_CUDA(c, cudaMemsetAsync(status, 0, (size_t)c->status_region * 8, s));
     TA_CUDA(c, cudaMemsetAsync(&cs->scan_counter[5], 0, 4, s));
-    launch_debug_tile_lists((const uint4*)c->rec.p, (const uint32_t*)c->list.p, (const uint32_t*)c->bin_offs.p, cg, cs,
-                            (uint32_t*)c->dbg_offs.p, status, &cs->scan_counter[5], &cs->sort_total, nullptr, 0, 0, s);
+    launch_debug_tile_lists((const uint2*)c->trng.p, (const uint32_t*)c->tlist.p, cg, (uint32_t*)c->dbg_offs.p, status,
+                            &cs->scan_counter[5], &cs->sort_total, nullptr, 0, 0, s);
     TA_CUDA(c, cudaGetLastError());
     CallState h;
     TA_CUDA(c, cudaMemcpyAsync(&h, c->cs.p, sizeof(CallState), cudaMemcpyDeviceToHost, s));
     TA_CUDA(c, cudaStreamSynchronize(s));
     const uint64_t K = h.sort_total;
     if ((st = grow(c, c->dbg_list, (size_t)std::max<uint64_t>(K, 1) * 4)) != TA_OK) return st;
-    launch_debug_tile_lists((const uint4*)c->rec.p, (const uint32_t*)c->list.p, (const uint32_t*)c->bin_offs.p, cg, cs,
-                            (uint32_t*)c->dbg_offs.p, status, &cs->scan_counter[5], &cs->sort_total,
-                            (uint32_t*)c->dbg_list.p, K, 1, s);
+    launch_debug_tile_lists((const uint2*)c->trng.p, (const uint32_t*)c->tlist.p, cg, (uint32_t*)c->dbg_offs.p, status,
+                            &cs->scan_counter[5], &cs->sort_total, (uint32_t*)c->dbg_list.p, K, 1, s);
     TA_CUDA(c, cudaGetLastError());
     TA_CUDA(c, cudaStreamSynchronize(s));
     int passes = 0;

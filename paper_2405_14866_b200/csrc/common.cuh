@@ -13,6 +13,11 @@ namespace ta {
 
 constexpr int kTile = 16;
 constexpr int kCoarseShift = 5;        // coarse bins are 32 x 32 pixels (2 x 2 tiles)
+// coarse-list entries: Gaussian array index in the low kListIdxBits, the 4-bit mask of the bin's
+// 2 x 2 tiles covered by the Gaussian's pixel box above it
+constexpr int kListIdxBits = 28;
+constexpr uint32_t kListIdxMask = (1u << kListIdxBits) - 1u;
+static_assert(kCoarseShift == 5, "coarse-list tile masks assume 2 x 2 tiles per coarse bin");
 constexpr uint32_t kCulledKey = 0xffffffffu;
 constexpr uint32_t kEmptyRect = 1u;     // x0 = 1, x1 = 0  -> empty box
 

@@ -177,7 +177,7 @@ __device__ __forceinline__ uint32_t box_lane_mask(int gx0, int gx1, int gy0, int
 template <int C, typename FT, bool kCounts>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const uint32_t* __restrict__ clist,
-            const uint32_t* __restrict__ coffs, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
+            const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
             const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
             int32_t* __restrict__ ncontrib) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -186,10 +186,9 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
 
     const int tile = (int)order[blockIdx.x];           // heaviest tiles first (k_tile_order)
     const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
-    const int sb = cg.shift - 4;
-    const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
-    const uint32_t cstart = coffs[(size_t)bin * cg.P];
-    uint32_t cend = coffs[(size_t)(bin + 1) * cg.P];
+    const uint2 tr = trng[tile];                       // this tile's (depth, id)-ordered list (k_tile_split)
+    const uint32_t cstart = tr.x;
+    uint32_t cend = tr.x + tr.y;
     if (cend > list_cap) cend = (uint32_t)list_cap;   // overflowed async call: never read past the list
     const uint32_t n = cs->n;
     const int W = cg.W, H = cg.H;
@@ -377,20 +376,105 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
     }
 }
 
-// Launch order of the tile CTAs: by decreasing log2 of the tile's coarse-list length (longest
+// Per-tile lists from the coarse (2^shift-pixel) bin lists, in list order: the (tile, depth, id)
+// order of SURVEY a3-a5 (an entry belongs to tile t iff its pixel box covers t).  One 1024-thread
+// block per coarse bin; its list is cut into 32 contiguous segments, one per warp: pass 1 counts each
+// segment's entries per tile (the 2^sb x 2^sb tiles of the bin), an exclusive scan over the warps
+// gives every (segment, tile) write offset, pass 2 writes.  Tile q of bin b owns
+// tlist[2^(2 sb) cstart_b + q len_b, + len_b) (a tile list is a subsequence of the bin list);
+// trng[tile] = (start, count).
+constexpr int kSplitMaxTiles = 4;                  // tiles per coarse bin supported (sb <= 1)
+__global__ void __launch_bounds__(1024) k_tile_split(const uint4* __restrict__ rec, const uint32_t* __restrict__ clist,
+                                                     const uint32_t* __restrict__ coffs, CompositeGeom cg,
+                                                     const CallState* __restrict__ cs, uint64_t clist_cap,
+                                                     uint32_t* __restrict__ tlist, uint64_t tlist_cap,
+                                                     uint2* __restrict__ trng) {
+    __shared__ uint32_t s_cnt[32][kSplitMaxTiles];
+    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+    const int sb = cg.shift - 4;
+    const int nq = 1 << (2 * sb);
+    const int bin = blockIdx.x;
+    const int bxi = bin % cg.BX, byi = bin / cg.BX;
+    const uint32_t cstart = coffs[(size_t)bin * cg.P];
+    uint32_t cend = coffs[(size_t)(bin + 1) * cg.P];
+    if (cend > clist_cap) cend = (uint32_t)clist_cap;
+    const uint32_t len = cend > cstart ? cend - cstart : 0u;
+    const uint32_t segl = (((len + 31u) / 32u) + 31u) & ~31u;          // entries per warp (multiple of 32)
+    const uint32_t s0 = cstart + warp * segl, s1 = min(cend, s0 + segl);
+    const uint32_t lt = lanemask_lt();
+    int txq[kSplitMaxTiles], tyq[kSplitMaxTiles];
+#pragma unroll
+    for (int q = 0; q < kSplitMaxTiles; q++) {
+        txq[q] = (bxi << sb) + (q & ((1 << sb) - 1));
+        tyq[q] = (byi << sb) + (q >> sb);
+    }
+    constexpr int kU = 4;                                           // chunks of 32 entries in flight
+    // the tiles an entry covers come with it (k_bin_place, bits kListIdxBits..+3)
+    auto walk = [&](bool write, uint32_t (&run)[kSplitMaxTiles]) {
+        for (uint32_t pos = s0; pos < s1; pos += 32 * kU) {
+            uint32_t ent[kU];
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const uint32_t e = pos + 32 * u + lane;
+                ent[u] = e < s1 ? clist[e] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const uint32_t idx = ent[u] & kListIdxMask, tm = ent[u] >> kListIdxBits;
+#pragma unroll
+                for (int q = 0; q < kSplitMaxTiles; q++) {
+                    const bool ok = (tm >> q) & 1u;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                    if (write && ok) {
+                        const uint64_t p = ((uint64_t)cstart << (2 * sb)) + (uint64_t)q * len + run[q] + __popc(bal & lt);
+                        if (p < tlist_cap) tlist[p] = idx;
+                    }
+                    run[q] += __popc(bal);
+                }
+            }
+        }
+    };
+    uint32_t run[kSplitMaxTiles] = {0u, 0u, 0u, 0u};
+    walk(false, run);
+    if (lane < kSplitMaxTiles) s_cnt[warp][lane] = run[0] * (lane == 0) + run[1] * (lane == 1) + run[2] * (lane == 2) +
+                                                   run[3] * (lane == 3);
+    __syncthreads();
+    if (warp == 0) {                                              // exclusive scan over the 32 segments, per tile
+#pragma unroll
+        for (int q = 0; q < kSplitMaxTiles; q++) {
+            const uint32_t v = s_cnt[lane][q];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            s_cnt[lane][q] = x - v;
+            if (lane == 31 && q < nq) {
+                const int tx = txq[q], ty = tyq[q];
+                if (tx < cg.TX && ty < cg.TY)
+                    trng[ty * cg.TX + tx] = make_uint2((uint32_t)min(((uint64_t)cstart << (2 * sb)) + (uint64_t)q * len,
+                                                                     (uint64_t)0xffffffffu), x);
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSplitMaxTiles; q++) run[q] = s_cnt[warp][q];
+    walk(true, run);
+}
+
+// Launch order of the tile CTAs: by decreasing log2 of the tile's list length (longest
 // lists first, so the last wave is made of short tiles).  One block; order within a bucket is
 // arbitrary (it only affects scheduling, never results).
-__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict__ coffs, CompositeGeom cg,
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ trng, CompositeGeom cg,
                                                      uint32_t* __restrict__ order) {
     __shared__ uint32_t s_cnt[33], s_off[33];
     const int T = cg.TX * cg.TY;
     if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0u;
     __syncthreads();
-    const int sb = cg.shift - 4;
     auto bucket = [&](int t) {
-        const int tyi = t / cg.TX, txi = t - tyi * cg.TX;
-        const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
-        const uint32_t len = coffs[(size_t)(bin + 1) * cg.P] - coffs[(size_t)bin * cg.P];
+        const uint32_t len = trng[t].y;
         return 32 - (32 - __clz(len));                 // 32 - bit length: longer lists -> smaller bucket
     };
     for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_cnt[bucket(t)], 1u);
@@ -520,7 +604,7 @@ constexpr bool kSkipEmptyPairs = false;
 template <int C, bool kCounts>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
-               const uint32_t* __restrict__ coffs, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
+               const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
                const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
                int32_t* __restrict__ ncontrib) {
     constexpr int NT = C / 8;                 // n-tiles of 8 channels
@@ -532,10 +616,9 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 
     const int tile = (int)order[blockIdx.x];
     const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
-    const int sb = cg.shift - 4;
-    const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
-    const uint32_t cstart = coffs[(size_t)bin * cg.P];
-    uint32_t cend = coffs[(size_t)(bin + 1) * cg.P];
+    const uint2 tr = trng[tile];                       // this tile's (depth, id)-ordered list (k_tile_split)
+    const uint32_t cstart = tr.x;
+    uint32_t cend = tr.x + tr.y;
     if (cend > list_cap) cend = (uint32_t)list_cap;
     const uint32_t n = cs->n;
     const int W = cg.W, H = cg.H;
@@ -898,7 +981,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 }
 
 template <int C>
-static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, const uint32_t* list, const uint32_t* offs,
+static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, const uint32_t* list, const uint2* offs,
                              uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs, uint64_t list_cap,
                              float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
     const size_t smem = sizeof(TcBuf<C>) * kWarps;
@@ -922,7 +1005,7 @@ static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, cons
 
 template <int C, typename FT>
 static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, const uint32_t* list,
-                              const uint32_t* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc,
+                              const uint2* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc,
                               const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
                               cudaStream_t st) {
     const size_t smem = sizeof(WarpBuf<C>) * kWarps;
@@ -947,7 +1030,7 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
 }
 
 cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
-                             const uint32_t* list, const uint32_t* offs, uint32_t* order, CompositeGeom cg,
+                             const uint32_t* list, const uint2* offs, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                              int32_t* ncontrib, cudaStream_t st) {
 #define TA_CASE(CC)                                                                                           \
@@ -969,60 +1052,44 @@ cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, con
 
 namespace ta {
 
-// Debug / test only: materialise the per-tile lists exactly as the compositor's producer walks them
-// (coarse bin list filtered by tile box; without the conservative ellipse prefilter), pass 0 counts,
-// pass 1 writes.  One warp per tile.
-__global__ void __launch_bounds__(256) k_debug_tile_lists(const uint4* __restrict__ rec, const uint32_t* __restrict__ clist,
-                                                          const uint32_t* __restrict__ coffs, CompositeGeom cg,
-                                                          const CallState* __restrict__ cs, uint32_t* __restrict__ tile_offs,
+// Debug / test only: compact the per-tile lists the compositor walks (k_tile_split output) into one
+// array: pass 0 writes the counts (then scanned into offsets), pass 1 copies.  One warp per tile.
+__global__ void __launch_bounds__(256) k_debug_tile_lists(const uint2* __restrict__ trng, const uint32_t* __restrict__ tlist,
+                                                          CompositeGeom cg, uint32_t* __restrict__ tile_offs,
                                                           uint32_t* __restrict__ out, uint64_t out_cap, int pass) {
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     const int T = cg.TX * cg.TY;
     const int t = blockIdx.x * 8 + (int)warp;
     if (blockIdx.x == 0 && threadIdx.x == 0 && pass == 0) tile_offs[T] = 0u;
     if (t >= T) return;
-    const int tyi = t / cg.TX, txi = t - tyi * cg.TX;
-    const int sb = cg.shift - 4;
-    const int bin = (tyi >> sb) * cg.BX + (txi >> sb);
-    const uint32_t cstart = coffs[(size_t)bin * cg.P], cend = coffs[(size_t)(bin + 1) * cg.P];
-    const uint32_t n = cs->n;
-    const uint32_t lt = lanemask_lt();
-    uint32_t run = pass ? tile_offs[t] : 0u;
-    for (uint32_t pos = cstart; pos < cend; pos += 32) {
-        const uint32_t e = pos + lane;
-        bool ok = false;
-        uint32_t i = 0;
-        if (e < cend) {
-            i = clist[e];
-            if (i < n) {
-                const uint4 r1 = rec[2 * i + 1];
-                const int x0 = (int)(r1.z & 0xffff), x1 = (int)(r1.z >> 16);
-                const int y0 = (int)(r1.w & 0xffff), y1 = (int)(r1.w >> 16);
-                ok = x0 <= x1 && (x0 >> 4) <= txi && txi <= (x1 >> 4) && (y0 >> 4) <= tyi && tyi <= (y1 >> 4);
-            }
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-        if (pass && ok) {
-            const uint64_t p = (uint64_t)run + __popc(bal & lt);
-            if (p < out_cap) out[p] = i;
-        }
-        run += __popc(bal);
+    const uint2 tr = trng[t];
+    if (pass == 0) {
+        if (lane == 0) tile_offs[t] = tr.y;
+        return;
     }
-    if (pass == 0 && lane == 0) tile_offs[t] = run;
+    const uint32_t o = tile_offs[t];
+    for (uint32_t k = lane; k < tr.y; k += 32)
+        if ((uint64_t)o + k < out_cap) out[o + k] = tlist[(size_t)tr.x + k];
 }
 
-void launch_debug_tile_lists(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
-                             const CallState* cs, uint32_t* tile_offs, unsigned long long* status, uint32_t* counter,
-                             unsigned long long* total, uint32_t* out_list, uint64_t out_cap, int pass,
-                             cudaStream_t st) {
+void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, CompositeGeom cg, uint32_t* tile_offs,
+                             unsigned long long* status, uint32_t* counter, unsigned long long* total, uint32_t* out_list,
+                             uint64_t out_cap, int pass, cudaStream_t st) {
     const int T = cg.TX * cg.TY;
     const int blocks = (T + 7) / 8;
     if (pass == 0) {
-        k_debug_tile_lists<<<blocks, 256, 0, st>>>(rec, clist, coffs, cg, cs, tile_offs, out_list, out_cap, 0);
+        k_debug_tile_lists<<<blocks, 256, 0, st>>>(trng, tlist, cg, tile_offs, out_list, out_cap, 0);
         launch_scan(tile_offs, nullptr, (uint32_t)T + 1, status, counter, total, st);
     } else {
-        k_debug_tile_lists<<<blocks, 256, 0, st>>>(rec, clist, coffs, cg, cs, tile_offs, out_list, out_cap, 1);
+        k_debug_tile_lists<<<blocks, 256, 0, st>>>(trng, tlist, cg, tile_offs, out_list, out_cap, 1);
     }
+}
+
+void launch_tile_split(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg, const CallState* cs,
+                       uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng, cudaStream_t st) {
+    const int sb = cg.shift - 4;
+    const int NB = cg.BX * ((cg.TY + (1 << sb) - 1) >> sb);
+    k_tile_split<<<NB, 1024, 0, st>>>(rec, clist, coffs, cg, cs, clist_cap, tlist, tlist_cap, trng);
 }
 
 }  // namespace ta

@@ -81,15 +81,17 @@ struct CompositeGeom {
     int shift, BX;        // coarse bins: (1 << shift) pixels square, BX per row
     uint32_t P;           // coarse-binning partitions (columns of the bin-major offset matrix)
 };
+// per-tile lists (tile, depth, id) from the coarse bin lists: tlist + trng[tile] = (start, count)
+void launch_tile_split(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg, const CallState* cs,
+                       uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng, cudaStream_t st);
 cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
-                             const uint32_t* list, const uint32_t* offs, uint32_t* order, CompositeGeom cg,
+                             const uint32_t* tlist, const uint2* trng, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                              int32_t* ncontrib, cudaStream_t st);
-// debug: materialise the per-tile (tile, depth, id) lists the compositor walks (a3/a5 check)
-void launch_debug_tile_lists(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
-                             const CallState* cs, uint32_t* tile_offs, unsigned long long* status, uint32_t* counter,
-                             unsigned long long* total, uint32_t* out_list, uint64_t out_cap, int pass,
-                             cudaStream_t st);
+// debug: compact the per-tile (tile, depth, id) lists the compositor walks into one array (a3/a5 check)
+void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, CompositeGeom cg, uint32_t* tile_offs,
+                             unsigned long long* status, uint32_t* counter, unsigned long long* total, uint32_t* out_list,
+                             uint64_t out_cap, int pass, cudaStream_t st);
 
 // unproject.cu
 __global__ void k_unproject_count(ViewTable vt, uint32_t* counts);

@@ -347,10 +347,16 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
         uint32_t idx = 0u;
         int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
         bool ok = false;
+        uint2 pb = make_uint2(kEmptyRect, kEmptyRect);
         if (r < wr1) {
-            ok = box_bins(boxes[r], bg.shift, &x0, &x1, &y0, &y1);
+            pb = boxes[r];
+            ok = box_bins(pb, bg.shift, &x0, &x1, &y0, &y1);
             idx = sorted[r];
         }
+        // 16 x 16 tiles covered by the pixel box: the list entry carries, above the index, which of the
+        // 2 x 2 tiles of its coarse bin the box covers (read by k_tile_split)
+        const int tx0 = (int)(pb.x & 0xffff) >> 4, tx1 = (int)(pb.x >> 16) >> 4;
+        const int ty0 = (int)(pb.y & 0xffff) >> 4, ty1 = (int)(pb.y >> 16) >> 4;
         const int tw = x1 - x0 + 1;
         const int cnt = ok ? tw * (y1 - y0 + 1) : 0;
         const int maxc = __reduce_max_sync(0xffffffffu, cnt);
@@ -365,13 +371,17 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
         }
         __syncwarp();
 #pragma unroll 1
-        for (int i = 0, xi = 0, t = t0; i < maxc; i++) {
+        for (int i = 0, xi = 0, yi = 0, t = t0; i < maxc; i++) {
             if (i < cnt) {
                 const uint32_t pos = s_cnt[rbase + t] + __popc(s_cnt[mbase + t] & lt);
-                if (pos < cap32) list[pos] = idx;
+                const int cx = 2 * (x0 + xi), cy = 2 * (y0 + yi);
+                const uint32_t mx = (uint32_t)(cx >= tx0 && cx <= tx1) | ((uint32_t)(cx + 1 >= tx0 && cx + 1 <= tx1) << 1);
+                const uint32_t my = (uint32_t)(cy >= ty0 && cy <= ty1) | ((uint32_t)(cy + 1 >= ty0 && cy + 1 <= ty1) << 1);
+                const uint32_t tm = ((my & 1u) ? mx : 0u) | ((my & 2u) ? (mx << 2) : 0u);
+                if (pos < cap32) list[pos] = idx | (tm << kListIdxBits);
                 else overflow = 1u;
                 t++;
-                if (++xi == tw) { xi = 0; t += stride; }
+                if (++xi == tw) { xi = 0; yi++; t += stride; }
             }
         }
         __syncwarp();

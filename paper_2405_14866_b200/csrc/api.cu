@@ -501,7 +501,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const size_t smem_place = (size_t)bg.nw * NB * 8;
     tm.begin(TA_STAGE_BIN_COUNT);
     if (cap_blocks > 0) {
-        k_gather_boxes<<<(unsigned)cap_blocks, 256, 0, s>>>(rec, v0, v1, cs, (uint2*)c->boxes.p);
+        k_gather_boxes<<<(unsigned)std::min<int64_t>(cap_blocks, 2 * c->num_sms), 256, 0, s>>>(rec, v0, v1, cs,
+                                                                                            (uint2*)c->boxes.p);
         TA_LAUNCHED(c);
     }
     k_bin_count<<<bg.P, bg.nw * 32, smem_count, s>>>((const uint2*)c->boxes.p, cs, bg, offs);

@@ -263,10 +263,10 @@ __global__ void __launch_bounds__(256) k_gather_boxes(const uint4* __restrict__ 
                                                       const uint32_t* __restrict__ vals_b,
                                                       const CallState* __restrict__ cs, uint2* __restrict__ boxes) {
     if (sort_passes(cs) > 0) return;
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= cs->n) return;
-    const uint4 q = rec[2 * vals_a[r] + 1];
-    boxes[r] = make_uint2(q.z, q.w);
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < cs->n; r += gridDim.x * blockDim.x) {
+        const uint4 q = rec[2 * vals_a[r] + 1];
+        boxes[r] = make_uint2(q.z, q.w);
+    }
 }
 
 __device__ __forceinline__ bool box_bins(uint2 bx, int sh, int* bx0, int* bx1, int* by0, int* by1) {

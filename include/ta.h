@@ -161,8 +161,7 @@ ta_status ta_rasterize(ta_context* ctx, const ta_gaussians* g, int64_t n, const 
  *   order       [n] uint32: array index of the Gaussian of depth rank r
  *   tile_offsets [T + 1] uint32: list of tile t is tile_list[tile_offsets[t] .. tile_offsets[t+1])
  *   tile_list   [K] uint32 array indices ordered by (tile, depth, id) -- the sequence the compositor
- *               walks for each tile (its coarse 32x32 bin list filtered by the tile box), materialised
- *               by this call (the hot path never writes per-tile lists)
+ *               walks for each tile (k_tile_split's per-tile lists, compacted into one array by this call)
  *   n_contrib   [H][W] int32 composited pairs per pixel (only with TA_FLAG_DEBUG_COUNTS)
  * The host fields (n, K, P, tiles_x, tiles_y, sort_passes) are filled by a synchronising read.
  */
@@ -175,7 +174,7 @@ typedef struct {
     const uint32_t* tile_offsets;
     const uint32_t* tile_list;
     const int32_t* n_contrib;
-    /* compositor work counters (only with TA_FLAG_DEBUG_COUNTS): [0] coarse-list entries read,
+    /* compositor work counters (only with TA_FLAG_DEBUG_COUNTS): [0] tile-list entries read,
        [1] entries staged, [2] staged entries evaluated, [3] evaluated with some q <= q_max,
        [4] accumulated, [5] composited (pixel, Gaussian) pairs, [6] warps, [7] fill rounds */
     int64_t work[8];

@@ -253,7 +253,7 @@ def run_ours(args):
     assert not any(cx.check_overflow() for cx in ctxs), "reserved tile-entry capacity overflowed"
 
     # ---------------- timed region (device time, CUDA events on the launching stream)
-    if not args.no_stage_events:
+    if not args.no_stage_events and nstr == 1:
         ctx.profile(True)
         ctx.profile_read(reset=True)
     clocks = ClockSampler(local)
@@ -272,7 +272,28 @@ def run_ours(args):
     clk = clocks.stop()
     launches = int(sum_over_ranks(sum(cx.launches for cx in ctxs) - launches0))
     ms = max_over_ranks(ms_local)
-    prof = ctx.profile_read(reset=True) if not args.no_stage_events else None
+    prof = None
+    stage_timing = "stage events of context 0 inside the timed region (single stream)"
+    if not args.no_stage_events:
+        if nstr == 1:
+            prof = ctx.profile_read(reset=True)
+        else:
+            # With several streams the kernels of different views overlap, so a stage's event pair
+            # brackets other views' work too.  Per-kernel launch durations are therefore taken from
+            # a serialized replay of the same K steps on one stream (CUDA events on that stream).
+            ctx.profile(True)
+            ctx.profile_read(reset=True)
+            torch.cuda.synchronize()
+            for _ in range(args.steps):
+                if rank == 0:
+                    ctx.unproject(views, params_sync, g, stream)
+                broadcast()
+                for (Ki, Ri), (F, A) in zip(cams, outs):
+                    ctx.rasterize(g, -1, Ki, Ri, H, W, params, F, A, stream)
+            torch.cuda.synchronize()
+            prof = ctx.profile_read(reset=True)
+            stage_timing = ("stage events over a single-stream replay of the K timed steps (the timed multi-stream "
+                            "step overlaps kernels of different views, so per-kernel durations are not defined there)")
     ctx.profile(False)
     overflow = any(cx.check_overflow() for cx in ctxs)
     value = n_views * args.steps / (ms / 1e3)
@@ -288,10 +309,12 @@ def run_ours(args):
     if prof is not None and rank == 0:
         stages = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
         line["stages_ms_per_call"] = {k: round(v, 4) for k, v in stages.items()}
+        line["stages_timing"] = stage_timing
         share = {k: v[0] for k, v in prof.items()}
         tot = sum(share.values())
         line["stages_share"] = {k: round(v / tot, 4) for k, v in share.items()} if tot else {}
-        line["roofline"] = roofline(ctx, g, cams[0], outs[0], H, W, C_, stages, n_g, stream)
+        line["roofline"] = roofline(ctx, g, cams[0], outs[0], H, W, C_, stages, n_g, stream,
+                                    ms_per_view=ms / (args.steps * n_views))
 
     # ---------------- end to end through the C ABI with host buffers
     if not args.no_e2e:
@@ -315,7 +338,7 @@ def run_ours(args):
     return 0
 
 
-def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
+def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None):
     """Algorithmic bytes / flops per launch over the live
     per-launch time of each stage; the dominant stage is reported."""
     import numpy as np
@@ -378,7 +401,7 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream):
               "algorithmic_bytes_per_launch": bytes_alg[dom], "composited_pairs_per_view": pairs,
               "visible_gaussians": nvis, "entries_per_view": K, "coarse_entries_per_view": Kc})
     # whole-view roofline: all per-view algorithmic bytes vs the summed per-view stage time
-    view_ms = sum(v for k, v in stages.items() if k != "unproject")
+    view_ms = ms_per_view if ms_per_view else sum(v for k, v in stages.items() if k != "unproject")
     b_view = n_g * 48 + nvis * fb + 16 * K + 4 * H * W * (C_ + 1)
     r["view"] = {"ms": view_ms, "alg_bytes": b_view, "hbm_frac": b_view / (view_ms / 1e3) / 1e9 / hbm,
                  "fp32_frac": flops_comp / (view_ms / 1e3) / 1e12 / fp32_tflops}

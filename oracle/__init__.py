@@ -69,6 +69,8 @@ def lib():
         _lib.tao_tile_lists.argtypes = [i64, P, P, P, P, i32, i32, P, P]
         _lib.tao_composite_tiles.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, i64, P, P,
                                              P, P]
+        _lib.tao_zbuffer_view.argtypes = [i32, i32, P, P, P, P, C.c_float, P, i64, P, P, i32, i32, i32, P]
+        _lib.tao_zbuffer_resolve.argtypes = [i64, P, C.c_float, C.c_float, P, P]
         _lib.tao_composite_bruteforce.argtypes = [i32, i32, i32, i32, i64, P, P, P, P, P, P, P, P, P,
                                                   i32, i32, P, P, P]
     return _lib
@@ -212,3 +214,27 @@ def rasterize(g, cam, params=None, tiles=None):
     ranges, lst = tile_lists(pr, g["ids"], cam.H, cam.W)
     F, A, nc, ne = composite(g, pr, ranges, lst, cam.H, cam.W, params, tiles)
     return dict(proj=pr, ranges=ranges, list=lst, F=F, A=A, n_contrib=nc, n_eval=ne)
+
+
+def zbuffer(views, cam, baseline_tgt, radius=1, params=None):
+    """NEXT #2 (R23): lift the valid pixels of the
+    source views (synthgen.SourceView list, source index = running pixel offset over the views),
+    splat min-z (tie-break lowest source index) into `cam` with splat radius `radius`.
+    Returns (zkey[H,W] uint64, depth[H,W] f32 (0 = empty), disparity[H,W] f32 = fx*B/z (0 = empty))."""
+    p = params or make_params()
+    zkey = np.full(cam.H * cam.W, np.iinfo(np.uint64).max, np.uint64)
+    Kt, Rt, tt = _cam(cam)
+    off = 0
+    for v in views:
+        K, R, t = _cam(v.cam)
+        disp = np.ascontiguousarray(v.disparity, np.float32)
+        mask = None if v.mask is None else np.ascontiguousarray(v.mask, np.uint8)
+        lib().tao_zbuffer_view(v.cam.H, v.cam.W, _p(disp), _p(mask), C.byref(_intr(K)), C.byref(_extr(R, t)),
+                               float(np.float32(v.baseline)), C.byref(p), off, C.byref(_intr(Kt)),
+                               C.byref(_extr(Rt, tt)), cam.H, cam.W, int(radius), _p(zkey))
+        off += v.cam.H * v.cam.W
+    depth = np.empty(cam.H * cam.W, np.float32)
+    disp = np.empty(cam.H * cam.W, np.float32)
+    lib().tao_zbuffer_resolve(zkey.size, _p(zkey), float(np.float32(cam.fx)), float(np.float32(baseline_tgt)),
+                              _p(depth), _p(disp))
+    return zkey.reshape(cam.H, cam.W), depth.reshape(cam.H, cam.W), disp.reshape(cam.H, cam.W)

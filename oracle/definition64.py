@@ -130,3 +130,40 @@ def composite(g, pr, H, W, alpha_max=0.99, alpha_min=1.0 / 255.0, t_eps=1e-4, cu
             A[py, px] = 1.0 - Tb[m]
             NC[py, px] = m
     return F, A, NC
+
+
+def zbuffer(views, cam, radius=1, z_near=0.01, d_min=0.0):
+    """NEXT #2 in float64 with array ops: lift every valid
+    pixel, project with K [R | t], nearest pixel by np.rint, min z over the (2r+1)^2 splat.
+    Returns depth[H, W] float64 (0 = no point)."""
+    H, W = cam.H, cam.W
+    best = np.full((H, W), np.inf)
+    R2 = np.asarray(cam.R, np.float32).astype(np.float64)
+    t2 = np.asarray(cam.t, np.float32).astype(np.float64)
+    f2 = np.float64(np.float32(cam.fx)), np.float64(np.float32(cam.fy))
+    c2 = np.float64(np.float32(cam.cx)), np.float64(np.float32(cam.cy))
+    for v in views:
+        sc = v.cam
+        d = v.disparity.astype(np.float64)
+        keep = np.isfinite(d) & (d > d_min)
+        if v.mask is not None:
+            keep &= v.mask != 0
+        ys, xs = np.nonzero(keep)
+        fx, fy = np.float64(np.float32(sc.fx)), np.float64(np.float32(sc.fy))
+        cx, cy = np.float64(np.float32(sc.cx)), np.float64(np.float32(sc.cy))
+        z = fx * np.float64(np.float32(v.baseline)) / d[ys, xs]
+        Xc = np.stack([(xs - cx) / fx * z, (ys - cy) / fy * z, z], axis=1)
+        R = np.asarray(sc.R, np.float32).astype(np.float64)
+        t = np.asarray(sc.t, np.float32).astype(np.float64)
+        Xw = (Xc - t) @ R
+        X = Xw @ R2.T + t2
+        ok = X[:, 2] > z_near
+        X = X[ok]
+        px = np.rint(f2[0] * X[:, 0] / X[:, 2] + c2[0]).astype(np.int64)
+        py = np.rint(f2[1] * X[:, 1] / X[:, 2] + c2[1]).astype(np.int64)
+        for dy in range(-radius, radius + 1):
+            for dx in range(-radius, radius + 1):
+                qx, qy = px + dx, py + dy
+                inb = (qx >= 0) & (qx < W) & (qy >= 0) & (qy < H)
+                np.minimum.at(best, (qy[inb], qx[inb]), X[inb, 2])
+    return np.where(np.isfinite(best), best, 0.0)

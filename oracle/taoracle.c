@@ -426,3 +426,76 @@ void tao_composite_bruteforce(int H, int W, int C, int feat_bytes, int64_t n,
 void tao_exp_det_array(int64_t n, const float* x, float* y) {
     for (int64_t i = 0; i < n; i++) y[i] = tao_exp_det(x[i]);
 }
+
+/* ----------------------------------------------- NEXT: cascade Z-buffer */
+/*
+ * "The predicted disparity of cam0 is converted to a depth map and then
+ * lifted to a 3D point cloud.  These points are rasterized to the viewpoints of cam2 and cam3.
+ * Z-buffers are extracted and converted back to disparity maps d_init."
+ * (points_zbuffer): per-pixel minimum camera-space z of all points splatted nearest-pixel with a
+ * splat radius r (default 1 px); pixels with no point are invalid; min-z with tie-break by the
+ * lowest source-pixel index.  DESIGN.md reading R23 fixes the arithmetic: lifting
+ * is the a1 sequence (z = fx*B/d, X_w = R^T (X_c - t)), projection the a2 sequence
+ * (X = R X_w + t, cull Z <= z_near, mu = fma(f, X/Z, c)), nearest pixel = rintf(mu) (ties to even),
+ * splat to every pixel of [px - r, px + r] x [py - r, py + r] inside the target.
+ *
+ * One source view: lifts its valid pixels (mask != 0, finite d > d_min) and min-accumulates the
+ * 64-bit key (bits(Z) << 32 | source index) into zkey[Ht*Wt] (caller fills it with ~0 first).
+ * Source index = idx0 + y*W + x (idx0: running pixel offset over the views).
+ */
+void tao_zbuffer_view(int H, int W, const float* disp, const uint8_t* mask, const tao_intr* K,
+                      const tao_extr* RT, float baseline, const tao_params* p, int64_t idx0,
+                      const tao_intr* Kt, const tao_extr* RTt, int Ht, int Wt, int r, uint64_t* zkey) {
+    const float* R = RT->R;
+    const float* t = RT->t;
+    const float* Rt = RTt->R;
+    const float* tt = RTt->t;
+    for (int y = 0; y < H; y++) {
+        for (int x = 0; x < W; x++) {
+            int64_t pix = (int64_t)y * W + x;
+            float d = disp[pix];
+            if (mask && mask[pix] == 0) continue;
+            if (!isfinite(d) || !(d > p->d_min)) continue;
+            /* a1: depth, camera-space point, world point */
+            float z = (K->fx * baseline) / d;
+            float xc = (((float)x - K->cx) / K->fx) * z;
+            float yc = (((float)y - K->cy) / K->fy) * z;
+            float p0 = xc - t[0], p1 = yc - t[1], p2 = z - t[2];
+            float w0 = dot3(R[0], R[3], R[6], p0, p1, p2);
+            float w1 = dot3(R[1], R[4], R[7], p0, p1, p2);
+            float w2 = dot3(R[2], R[5], R[8], p0, p1, p2);
+            /* a2: target camera space, cull, pixel centre */
+            float X = dot3(Rt[0], Rt[1], Rt[2], w0, w1, w2) + tt[0];
+            float Y = dot3(Rt[3], Rt[4], Rt[5], w0, w1, w2) + tt[1];
+            float Z = dot3(Rt[6], Rt[7], Rt[8], w0, w1, w2) + tt[2];
+            if (!(Z > p->z_near)) continue;
+            float mx = fmaf(Kt->fx, X / Z, Kt->cx);
+            float my = fmaf(Kt->fy, Y / Z, Kt->cy);
+            float fpx = rintf(mx), fpy = rintf(my);
+            if (!(fpx >= (float)(-r) && fpx <= (float)(Wt - 1 + r) && fpy >= (float)(-r) && fpy <= (float)(Ht - 1 + r)))
+                continue;
+            int px = (int)fpx, py = (int)fpy;
+            uint64_t key = ((uint64_t)float_bits(Z) << 32) | (uint64_t)(uint32_t)(idx0 + pix);
+            for (int j = py - r; j <= py + r; j++) {
+                if (j < 0 || j >= Ht) continue;
+                for (int i = px - r; i <= px + r; i++) {
+                    if (i < 0 || i >= Wt) continue;
+                    uint64_t* zk = zkey + (int64_t)j * Wt + i;
+                    if (key < *zk) *zk = key;
+                }
+            }
+        }
+    }
+}
+
+/* Z-buffer -> depth (Z of the nearest point, 0 where none) and disparity fx*B/Z (0 where none). */
+void tao_zbuffer_resolve(int64_t n, const uint64_t* zkey, float fx, float baseline, float* depth, float* dispo) {
+    for (int64_t i = 0; i < n; i++) {
+        if (zkey[i] == ~(uint64_t)0) { depth[i] = 0.0f; if (dispo) dispo[i] = 0.0f; continue; }
+        uint32_t zb = (uint32_t)(zkey[i] >> 32);
+        float z;
+        memcpy(&z, &zb, 4);
+        depth[i] = z;
+        if (dispo) dispo[i] = (fx * baseline) / z;
+    }
+}

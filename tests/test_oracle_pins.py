@@ -444,3 +444,77 @@ def test_composite_matches_float64_model(oracle_lib, which):
         assert same.mean() >= 0.995
         assert np.abs(r["F"] - F64)[same].max() <= 1e-4
         assert np.abs(r["A"] - A64)[same].max() <= 1e-5
+
+
+# ------------------------------------------------------------------ NEXT #2: cascade Z-buffer (R23)
+# PAPER.md P:351-352 ("lifted to a 3D point cloud ... rasterized to the viewpoints of cam2 and cam3.
+# Z-buffers are extracted and converted back to disparity maps"), SPEC.md S:86-94 (points_zbuffer).
+
+def _single_point_view(H, W, fx, cx, cy, px, py, z, B=0.1, R=None, t=None):
+    disp = np.zeros((H, W), np.float32)
+    disp[py, px] = np.float32(fx * B / z)
+    cam = sg.Camera(fx=fx, fy=fx, cx=cx, cy=cy, R=np.eye(3) if R is None else R,
+                    t=np.zeros(3) if t is None else t, H=H, W=W)
+    return sg.SourceView(cam=cam, baseline=B, disparity=disp, mask=None, scale=None, quat=None,
+                         opacity=None, feat=np.zeros((H, W, 8), np.float32))
+
+
+def test_zbuffer_point_on_axis(oracle_lib):
+    """one point on the optical axis at z = 2 -> single valid pixel at the principal point
+    with depth 2 (splat radius 0); its disparity is fx*B/2."""
+    import oracle
+    v = _single_point_view(1, 1, 100.0, 0.0, 0.0, 0, 0, 2.0, B=0.2)
+    tgt = sg.Camera(fx=100.0, fy=100.0, cx=7.0, cy=5.0, R=np.eye(3), t=np.zeros(3), H=11, W=15)
+    _, depth, disp = oracle.zbuffer([v], tgt, 0.2, radius=0)
+    assert np.count_nonzero(depth) == 1
+    assert depth[5, 7] == np.float32(2.0)
+    assert disp[5, 7] == np.float32(100.0 * 0.2 / 2.0)
+    _, depth1, _ = oracle.zbuffer([v], tgt, 0.2, radius=1)      # radius 1: the 3 x 3 neighbourhood
+    assert np.count_nonzero(depth1) == 9 and np.all(depth1[4:7, 6:9] == np.float32(2.0))
+
+
+def test_zbuffer_min_z_and_tie_break(oracle_lib):
+    """two points projecting to the same pixel with z = 1 and z = 3 -> depth 1, whatever
+    the order of the views; equal depths resolve to the lowest source index."""
+    import oracle
+    tgt = sg.Camera(fx=100.0, fy=100.0, cx=4.0, cy=4.0, R=np.eye(3), t=np.zeros(3), H=9, W=9)
+    a = _single_point_view(1, 1, 100.0, 0.0, 0.0, 0, 0, 1.0)
+    b = _single_point_view(1, 1, 100.0, 0.0, 0.0, 0, 0, 3.0)
+    for vs in ([a, b], [b, a]):
+        zk, depth, _ = oracle.zbuffer(vs, tgt, 0.1, radius=0)
+        assert depth[4, 4] == np.float32(1.0)
+    zk, _, _ = oracle.zbuffer([a, a], tgt, 0.1, radius=0)
+    assert int(zk[4, 4]) & 0xffffffff == 0                     # tie: the first view's pixel wins
+
+
+def test_zbuffer_cascade_matches_ground_truth_depth(oracle_lib):
+    """S:94 (derived): cam0's depth of the synthetic upper body warped into cam2 matches cam2's
+    analytic (ray-cast) depth: median |error| < 5 mm on pixels both see."""
+    import oracle
+    s = sg.make_config("c3", res=256)
+    cam0, cam2 = s.views[0], s.views[2]
+    _, depth, disp = oracle.zbuffer([cam0], cam2.cam, cam2.baseline, radius=1)
+    gt = np.where(cam2.mask != 0, np.float32(cam2.cam.fx * cam2.baseline) / cam2.disparity, 0.0)
+    both = (depth > 0) & (gt > 0)
+    assert both.mean() > 0.15
+    err = np.abs(depth[both] - gt[both])
+    assert np.median(err) < 0.005, np.median(err)
+    # the disparity map is fx * B / z of the same pixels
+    assert np.allclose(disp[both], np.float32(cam2.cam.fx) * np.float32(cam2.baseline) / depth[both], rtol=1e-6)
+
+
+def test_zbuffer_matches_float64_model(oracle_lib):
+    """Whole-rig z-buffer vs the independent float64 model (oracle/definition64.py): identical
+    occupancy and depths within 1e-5 relative except where fp32 and float64 round a pixel centre
+    to different pixels (mu within ~1e-5 px of a half-integer), which must be rare."""
+    import oracle
+    import oracle.definition64 as d64
+    s = sg.make_config("c2", res=128)
+    tgt = s.targets[0]
+    _, depth, _ = oracle.zbuffer(s.views, tgt, 0.1, radius=1)
+    ref = d64.zbuffer(s.views, tgt, radius=1)
+    occ = (depth > 0) != (ref > 0)
+    assert occ.mean() < 1e-3
+    both = (depth > 0) & (ref > 0)
+    rel = np.abs(depth[both] - ref[both]) / ref[both]
+    assert np.mean(rel < 1e-5) > 0.999, np.mean(rel < 1e-5)

@@ -152,6 +152,28 @@ ta_status ta_rasterize(ta_context* ctx, const ta_gaussians* g, int64_t n, const 
                        float* feat_out, float* alpha_out, void* stream);
 
 /*
+ * cascade depth initialisation (cam0's disparity "is
+ * converted to a depth map and then lifted to a 3D point cloud.  These points are rasterized to the
+ * viewpoints of cam2 and cam3.  Z-buffers are extracted and converted back to disparity maps";
+ * SPEC.md l.86-94 points_zbuffer; reading R23).
+ * Every valid pixel (mask != 0, finite d > params->d_min) of the V source views is lifted (a1
+ * arithmetic, opacity / scale / features ignored), projected into (K_tgt, RT_tgt) (a2 arithmetic,
+ * culled unless z > params->z_near) and splatted to the (2 r + 1)^2 pixels around its nearest pixel
+ * (rint of the pixel centre, ties to even) with r = splat_radius in [0, 8].  Each target pixel keeps
+ * the point of minimum camera-space z, ties to the lowest source index (running pixel index over the
+ * views, view-major, row-major) -- independent of execution order.
+ *   depth_out  device float [H][W]: that z, 0 where no point lands (required)
+ *   disp_out   device float [H][W] or NULL: fx_tgt * baseline_tgt / z, 0 where no point lands
+ *              (the d_init of the lower pair; baseline_tgt > 0 required when disp_out != NULL)
+ * Scratch: one 64-bit z-buffer word per target pixel (context-owned, grown on demand).
+ * Errors: TA_ERR_INVALID_ARG for NULL depth_out / views, bad sizes, radius outside [0, 8],
+ * non-finite or non-orthonormal cameras, baseline_tgt <= 0 with disp_out.
+ */
+ta_status ta_zbuffer(ta_context* ctx, const ta_source_view* views, int32_t V, const ta_raster_params* params,
+                     const ta_intrinsics* K_tgt, const ta_extrinsics* RT_tgt, int32_t H, int32_t W,
+                     int32_t splat_radius, float baseline_tgt, float* depth_out, float* disp_out, void* stream);
+
+/*
  * Introspection of the LAST ta_rasterize call on this context (device pointers into context
  * scratch, valid until the next call; read them on the same stream after it completes).
  *   records     [n][8] 32-bit words per Gaussian (array order): mean_x, mean_y, conic a, conic 2b,

@@ -65,6 +65,7 @@ class Profile(C.Structure):
 
 
 EXPORTS = ("ta_profile_enable", "ta_profile_read", "ta_default_params", "ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject",
+           "ta_zbuffer",
            "ta_rasterize", "ta_debug_last", "ta_check_overflow", "ta_launch_count", "ta_status_string",
            "ta_last_error", "ta_build_info")
 
@@ -91,6 +92,8 @@ def lib(build_if_stale: bool = False):
     L.ta_rasterize.argtypes = [P, C.POINTER(Gaussians), i64, C.POINTER(Intrinsics), C.POINTER(Extrinsics), i32, i32,
                                C.POINTER(RasterParams), P, P, P]
     L.ta_debug_last.argtypes = [P, C.POINTER(DebugView), P]
+    L.ta_zbuffer.argtypes = [P, C.POINTER(SourceView), i32, C.POINTER(RasterParams), C.POINTER(Intrinsics),
+                             C.POINTER(Extrinsics), i32, i32, i32, C.c_float, P, P, P]
     L.ta_check_overflow.argtypes = [P, P, C.POINTER(i32)]
     L.ta_profile_enable.argtypes = [P, i32]
     L.ta_profile_read.argtypes = [P, C.POINTER(Profile), i32]
@@ -101,7 +104,7 @@ def lib(build_if_stale: bool = False):
     L.ta_last_error.argtypes = [P]
     L.ta_last_error.restype = C.c_char_p
     L.ta_build_info.restype = C.c_char_p
-    for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize",
+    for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize", "ta_zbuffer",
                  "ta_debug_last", "ta_check_overflow", "ta_profile_enable", "ta_profile_read"):
         getattr(L, name).restype = i32
     _lib = L
@@ -176,6 +179,14 @@ class Context:
         arr = (SourceView * len(views))(*views)
         gs = g.struct()
         self._check(lib().ta_unproject(self._h, arr, len(views), C.byref(params), C.byref(gs), _stream(stream)))
+
+    def zbuffer(self, views, params: RasterParams, K: Intrinsics, RT: Extrinsics, H, W, radius, baseline_tgt,
+                depth_out, disp_out=None, stream=None):
+        """NEXT #2 cascade Z-buffer (include/ta.h ta_zbuffer): views = SourceView structs."""
+        arr = (SourceView * len(views))(*views)
+        self._check(lib().ta_zbuffer(self._h, arr, len(views), C.byref(params), C.byref(K), C.byref(RT), int(H),
+                                     int(W), int(radius), float(baseline_tgt), _ptr(depth_out), _ptr(disp_out),
+                                     _stream(stream)))
 
     def rasterize(self, g: "GaussianBuffers", n, K: Intrinsics, RT: Extrinsics, H, W, params: RasterParams,
                   feat_out, alpha_out, stream=None):

@@ -36,6 +36,7 @@ struct ta_context {
     uint64_t launches = 0;
     DevBuf cs, status, rec, boxes, tile_order, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
     DevBuf tlist, trng;           // per-tile lists (4 x the coarse-list capacity) and their (start, count)
+    DevBuf zkey;                  // ta_zbuffer: 64-bit z-buffer words
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
     // last rasterize call
@@ -232,7 +233,7 @@ ta_status ta_context_destroy(ta_context* c) {
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->boxes, &c->tile_order, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
                       &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list,
-                      &c->tlist, &c->trng};
+                      &c->tlist, &c->trng, &c->zkey};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -313,6 +314,51 @@ ta_status reserve_target(ta_context* c, const BinGeom& bg, int64_t cap, int H, i
     return TA_OK;
 }
 
+// Validates V source views and fills the kernels' view table (unprojection-block ranges, running
+// pixel offsets, 128-bit-load eligibility).  need_feat: the views must carry 16-byte aligned features.
+ta_status build_view_table(ta_context* c, const ta_source_view* views, int32_t V, const ta_raster_params* p,
+                           bool need_feat, int C, int fbytes, ViewTable* vtp, int64_t* pixels_out, uint32_t* blocks_out) {
+    ViewTable& vt = *vtp;
+    memset(&vt, 0, sizeof(vt));
+    vt.V = V;
+    vt.C = C;
+    vt.fbytes = fbytes;
+    vt.d_min = p->d_min;
+    vt.default_scale = p->default_scale;
+    vt.default_opacity = p->default_opacity;
+    int64_t pixels = 0;
+    uint32_t blocks = 0;
+    for (int v = 0; v < V; v++) {
+        const ta_source_view& s = views[v];
+        if (s.H < 1 || s.W < 1 || s.H > 32767 || s.W > 32767)
+            return fail(c, TA_ERR_INVALID_ARG, "view %d: bad size %d x %d", v, s.H, s.W);
+        if (!s.disparity || (need_feat && !s.feat)) return fail(c, TA_ERR_INVALID_ARG, "view %d: NULL disparity/feat", v);
+        if (!(s.baseline > 0.0f) || !std::isfinite(s.baseline))
+            return fail(c, TA_ERR_INVALID_ARG, "view %d: baseline must be > 0", v);
+        ta_status cst;
+        if (!finite_cam(s.K, s.RT, c, &cst)) return cst;
+        if (need_feat && (((uintptr_t)s.feat) & 15)) return fail(c, TA_ERR_INVALID_ARG, "view %d: feat not 16-byte aligned", v);
+        ViewDesc& d = vt.v[v];
+        d.disp = s.disparity; d.mask = s.mask; d.scale = s.scale; d.quat = s.quat; d.opacity = s.opacity; d.feat = s.feat;
+        d.fx = s.K.fx; d.fy = s.K.fy; d.cx = s.K.cx; d.cy = s.K.cy;
+        memcpy(d.R, s.RT.R, sizeof(d.R));
+        memcpy(d.t, s.RT.t, sizeof(d.t));
+        d.baseline = s.baseline;
+        d.H = s.H; d.W = s.W;
+        d.blk_begin = blocks;
+        d.idx0 = (uint32_t)pixels;
+        const int64_t HW = (int64_t)s.H * s.W;
+        const bool al = ((((uintptr_t)s.disparity) | ((uintptr_t)s.opacity) | ((uintptr_t)s.quat)) & 15) == 0 &&
+                        (((uintptr_t)s.mask) & 3) == 0;
+        d.vec4 = (HW % 4 == 0 && al) ? 1 : 0;
+        blocks += (uint32_t)((HW + kUnprojPix - 1) / kUnprojPix);
+        pixels += HW;
+    }
+    *pixels_out = pixels;
+    *blocks_out = blocks;
+    return TA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -347,40 +393,10 @@ ta_status ta_unproject(ta_context* c, const ta_source_view* views, int32_t V, co
     cudaSetDevice(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     ViewTable vt;
-    memset(&vt, 0, sizeof(vt));
-    vt.V = V;
-    vt.C = out->C;
-    vt.fbytes = out->feat_dtype == TA_F16 ? 2 : 4;
-    vt.d_min = p->d_min;
-    vt.default_scale = p->default_scale;
-    vt.default_opacity = p->default_opacity;
     int64_t pixels = 0;
     uint32_t blocks = 0;
-    for (int v = 0; v < V; v++) {
-        const ta_source_view& s = views[v];
-        if (s.H < 1 || s.W < 1 || s.H > 32767 || s.W > 32767)
-            return fail(c, TA_ERR_INVALID_ARG, "view %d: bad size %d x %d", v, s.H, s.W);
-        if (!s.disparity || !s.feat) return fail(c, TA_ERR_INVALID_ARG, "view %d: NULL disparity/feat", v);
-        if (!(s.baseline > 0.0f) || !std::isfinite(s.baseline))
-            return fail(c, TA_ERR_INVALID_ARG, "view %d: baseline must be > 0", v);
-        ta_status cst;
-        if (!finite_cam(s.K, s.RT, c, &cst)) return cst;
-        if (((uintptr_t)s.feat) & 15) return fail(c, TA_ERR_INVALID_ARG, "view %d: feat not 16-byte aligned", v);
-        ViewDesc& d = vt.v[v];
-        d.disp = s.disparity; d.mask = s.mask; d.scale = s.scale; d.quat = s.quat; d.opacity = s.opacity; d.feat = s.feat;
-        d.fx = s.K.fx; d.fy = s.K.fy; d.cx = s.K.cx; d.cy = s.K.cy;
-        memcpy(d.R, s.RT.R, sizeof(d.R));
-        memcpy(d.t, s.RT.t, sizeof(d.t));
-        d.baseline = s.baseline;
-        d.H = s.H; d.W = s.W;
-        d.blk_begin = blocks;
-        const int64_t HW = (int64_t)s.H * s.W;
-        const bool al = ((((uintptr_t)s.disparity) | ((uintptr_t)s.opacity) | ((uintptr_t)s.quat)) & 15) == 0 &&
-                        (((uintptr_t)s.mask) & 3) == 0;
-        d.vec4 = (HW % 4 == 0 && al) ? 1 : 0;
-        blocks += (uint32_t)((HW + kUnprojPix - 1) / kUnprojPix);
-        pixels += HW;
-    }
+    ta_status vst = build_view_table(c, views, V, p, true, out->C, out->feat_dtype == TA_F16 ? 2 : 4, &vt, &pixels, &blocks);
+    if (vst != TA_OK) return vst;
     if (pixels > out->capacity)
         return fail(c, TA_ERR_CAPACITY, "capacity %lld < %lld source pixels", (long long)out->capacity, (long long)pixels);
     if (pixels >= (1ll << 31)) return fail(c, TA_ERR_CAPACITY, "more than 2^31 source pixels");
@@ -542,6 +558,48 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     c->last_TX = cg.TX; c->last_TY = cg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;
     c->last_cg = cg;
     c->last_counts = counts;
+    return TA_OK;
+}
+
+ta_status ta_zbuffer(ta_context* c, const ta_source_view* views, int32_t V, const ta_raster_params* p,
+                     const ta_intrinsics* K, const ta_extrinsics* RT, int32_t H, int32_t W, int32_t radius,
+                     float baseline_tgt, float* depth_out, float* disp_out, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!views || !p || !K || !RT || !depth_out) return fail(c, TA_ERR_INVALID_ARG, "ta_zbuffer: NULL argument");
+    if (V < 1 || V > TA_MAX_VIEWS) return fail(c, TA_ERR_UNSUPPORTED, "ta_zbuffer: V = %d not in [1, %d]", V, TA_MAX_VIEWS);
+    if (H < 1 || W < 1 || H > 32767 || W > 32767) return fail(c, TA_ERR_INVALID_ARG, "bad target size %d x %d", H, W);
+    if (radius < 0 || radius > 8) return fail(c, TA_ERR_INVALID_ARG, "splat radius %d not in [0, 8]", radius);
+    if (disp_out && !(baseline_tgt > 0.0f && std::isfinite(baseline_tgt)))
+        return fail(c, TA_ERR_INVALID_ARG, "baseline_tgt must be > 0 when disp_out is given");
+    if (!std::isfinite(p->z_near) || !std::isfinite(p->d_min)) return fail(c, TA_ERR_INVALID_ARG, "non-finite params");
+    ta_status st;
+    if (!finite_cam(*K, *RT, c, &st)) return st;
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    ViewTable vt;
+    int64_t pixels = 0;
+    uint32_t blocks = 0;
+    if ((st = build_view_table(c, views, V, p, false, 8, 4, &vt, &pixels, &blocks)) != TA_OK) return st;
+    if (pixels >= (1ll << 32)) return fail(c, TA_ERR_CAPACITY, "more than 2^32 source pixels");
+    const uint32_t npix = (uint32_t)H * (uint32_t)W;
+    if ((st = grow(c, c->zkey, (size_t)npix * 8)) != TA_OK) return st;
+    TargetCam cam;
+    cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
+    memcpy(cam.R, RT->R, sizeof(cam.R));
+    memcpy(cam.t, RT->t, sizeof(cam.t));
+    cam.W = W; cam.H = H;
+    cam.Wm1f = (float)(W - 1);
+    cam.Hm1f = (float)(H - 1);
+    unsigned long long* zk = (unsigned long long*)c->zkey.p;
+    const unsigned grid = (unsigned)std::min<uint32_t>((npix + 255) / 256, 8u * (uint32_t)c->num_sms);
+    k_zb_clear<<<grid, 256, 0, s>>>(zk, npix);
+    TA_LAUNCHED(c);
+    if (blocks > 0) {
+        k_zb_splat<<<blocks, kUnprojThreads, 0, s>>>(vt, cam, p->z_near, radius, zk);
+        TA_LAUNCHED(c);
+    }
+    k_zb_resolve<<<grid, 256, 0, s>>>(zk, npix, K->fx, baseline_tgt, depth_out, disp_out);
+    TA_LAUNCHED(c);
     return TA_OK;
 }
 

@@ -37,6 +37,7 @@ struct ViewDesc {
     float baseline;
     int H, W;
     uint32_t blk_begin;   // first unprojection block of this view
+    uint32_t idx0;        // running pixel offset of this view (z-buffer source index)
     int vec4;             // 1: H*W % 4 == 0 and all maps 16-byte aligned -> 128-bit loads
 };
 
@@ -92,6 +93,12 @@ cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, con
 void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, CompositeGeom cg, uint32_t* tile_offs,
                              unsigned long long* status, uint32_t* counter, unsigned long long* total, uint32_t* out_list,
                              uint64_t out_cap, int pass, cudaStream_t st);
+
+// zbuffer.cu
+__global__ void k_zb_clear(unsigned long long* zk, uint32_t n);
+__global__ void k_zb_splat(ViewTable vt, TargetCam cam, float z_near, int radius, unsigned long long* zk);
+__global__ void k_zb_resolve(const unsigned long long* zk, uint32_t n, float fx, float baseline, float* depth,
+                             float* disp);
 
 // unproject.cu
 __global__ void k_unproject_count(ViewTable vt, uint32_t* counts);

@@ -71,6 +71,7 @@ def lib():
                                              P, P]
         _lib.tao_zbuffer_view.argtypes = [i32, i32, P, P, P, P, C.c_float, P, i64, P, P, i32, i32, i32, P]
         _lib.tao_zbuffer_resolve.argtypes = [i64, P, C.c_float, C.c_float, P, P]
+        _lib.tao_blend.argtypes = [i32, P, P, P, P, P, i32, i32, P, P, P]
         _lib.tao_composite_bruteforce.argtypes = [i32, i32, i32, i32, i64, P, P, P, P, P, P, P, P, P,
                                                   i32, i32, P, P, P]
     return _lib
@@ -238,3 +239,46 @@ def zbuffer(views, cam, baseline_tgt, radius=1, params=None):
     lib().tao_zbuffer_resolve(zkey.size, _p(zkey), float(np.float32(cam.fx)), float(np.float32(baseline_tgt)),
                               _p(depth), _p(disp))
     return zkey.reshape(cam.H, cam.W), depth.reshape(cam.H, cam.W), disp.reshape(cam.H, cam.W)
+
+
+class _BView(C.Structure):
+    _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("disp", C.c_void_p), ("mask", C.c_void_p),
+                ("K", C.c_float * 4), ("R", C.c_float * 9), ("t", C.c_float * 3), ("baseline", C.c_float),
+                ("color", C.c_void_p)]
+
+
+class _BParams(C.Structure):
+    _fields_ = [("delta", C.c_float), ("edge_tau", C.c_float), ("w_min", C.c_float)]
+
+
+def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, params=None):
+    """NEXT #1 (Eqs. 6-10; R24): occlusion-aware blending of the input
+    views' colours into `cam` over the fused depth z_fused[H, W] (0 = none, e.g. zbuffer(...)[1]).
+    colors: list of [H_i, W_i, 3] float32.  Returns (rgb[H, W, 3] f32, wsum[H, W] f32)."""
+    p = params or make_params()
+    keep = []
+    arr = (_BView * len(views))()
+    for k, (v, col) in enumerate(zip(views, colors)):
+        K, R, t = _cam(v.cam)
+        disp = np.ascontiguousarray(v.disparity, np.float32)
+        mask = None if v.mask is None else np.ascontiguousarray(v.mask, np.uint8)
+        col = np.ascontiguousarray(col, np.float32)
+        keep += [disp, mask, col]
+        b = arr[k]
+        b.H, b.W = v.cam.H, v.cam.W
+        b.disp, b.mask, b.color = disp.ctypes.data, (None if mask is None else mask.ctypes.data), col.ctypes.data
+        for j in range(4):
+            b.K[j] = float(K[j])
+        for j in range(9):
+            b.R[j] = float(R.reshape(-1)[j])
+        for j in range(3):
+            b.t[j] = float(t[j])
+        b.baseline = float(np.float32(v.baseline))
+    bp = _BParams(float(delta), float(edge_tau), float(w_min))
+    Kn, Rn, tn = _cam(cam)
+    zf = np.ascontiguousarray(z_fused, np.float32)
+    rgb = np.empty((cam.H, cam.W, 3), np.float32)
+    ws = np.empty((cam.H, cam.W), np.float32)
+    lib().tao_blend(len(views), arr, C.byref(p), C.byref(bp), C.byref(_intr(Kn)), C.byref(_extr(Rn, tn)), cam.H,
+                    cam.W, _p(zf), _p(rgb), _p(ws))
+    return rgb, ws

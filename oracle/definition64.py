@@ -167,3 +167,78 @@ def zbuffer(views, cam, radius=1, z_near=0.01, d_min=0.0):
                 inb = (qx >= 0) & (qx < W) & (qy >= 0) & (qy < H)
                 np.minimum.at(best, (qy[inb], qx[inb]), X[inb, 2])
     return np.where(np.isfinite(best), best, 0.0)
+
+
+def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, z_near=0.01, d_min=0.0):
+    """NEXT #1 (Eqs. 6-10) in float64 with array operations: lift every pixel of
+    z_fused, project into each view, bilinear colour / depth, Occ, edge mask, finite-difference
+    normal, cos / distance weights, normalised sum.  Returns (rgb[H, W, 3], wsum[H, W]) float64."""
+    H, W = cam.H, cam.W
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    R, t = f32(cam.R), f32(cam.t)
+    fx, fy, cx, cy = (np.float64(np.float32(v)) for v in (cam.fx, cam.fy, cam.cx, cam.cy))
+    vv, uu = np.nonzero(z_fused > 0)
+    z = z_fused[vv, uu].astype(np.float64)
+    Xc = np.stack([(uu - cx) / fx * z, (vv - cy) / fy * z, z], 1)
+    Xw = (Xc - t) @ R
+    C0 = -t @ R
+    ray = Xw - C0
+    ray /= np.linalg.norm(ray, axis=1, keepdims=True)
+    acc = np.zeros((len(z), 3))
+    ws = np.zeros(len(z))
+    for v, col in zip(views, colors):
+        sc = v.cam
+        Ri, ti = f32(sc.R), f32(sc.t)
+        fxi, fyi, cxi, cyi = (np.float64(np.float32(a)) for a in (sc.fx, sc.fy, sc.cx, sc.cy))
+        d = v.disparity.astype(np.float64)
+        valid = np.isfinite(d) & (d > d_min)
+        if v.mask is not None:
+            valid &= v.mask != 0
+        zmap = np.where(valid, fxi * np.float64(np.float32(v.baseline)) / np.where(valid, d, 1.0), np.nan)
+        Hi, Wi = sc.H, sc.W
+        X = Xw @ Ri.T + ti
+        Z = X[:, 2]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            us = fxi * X[:, 0] / Z + cxi
+            vs = fyi * X[:, 1] / Z + cyi
+        ok = (Z > z_near) & (us >= 0) & (us <= Wi - 1) & (vs >= 0) & (vs <= Hi - 1)
+        x0 = np.clip(np.floor(np.where(ok, us, 0)).astype(int), 0, max(Wi - 2, 0))
+        y0 = np.clip(np.floor(np.where(ok, vs, 0)).astype(int), 0, max(Hi - 2, 0))
+        x1, y1 = np.minimum(x0 + 1, Wi - 1), np.minimum(y0 + 1, Hi - 1)
+        ax, ay = us - x0, vs - y0
+        taps = [zmap[y0, x0], zmap[y0, x1], zmap[y1, x0], zmap[y1, x1]]
+        ok &= np.all(np.isfinite(np.stack(taps)), axis=0)
+        zs = (taps[0] * (1 - ax) + taps[1] * ax) * (1 - ay) + (taps[2] * (1 - ax) + taps[3] * ax) * ay
+        ok &= np.abs(Z - zs) < delta
+        px = np.clip(np.rint(np.where(ok, us, 0)).astype(int), 0, Wi - 1)
+        py = np.clip(np.rint(np.where(ok, vs, 0)).astype(int), 0, Hi - 1)
+        inb = (px >= 1) & (px <= Wi - 2) & (py >= 1) & (py <= Hi - 2)
+        ok &= inb
+        pxs, pys = np.clip(px, 1, Wi - 2), np.clip(py, 1, Hi - 2)
+
+        def P(x, y):
+            zz = zmap[y, x]
+            return np.stack([(x - cxi) / fxi * zz, (y - cyi) / fyi * zz, zz], 1)
+        zl, zr, zu, zd = zmap[pys, pxs - 1], zmap[pys, pxs + 1], zmap[pys - 1, pxs], zmap[pys + 1, pxs]
+        ok &= np.isfinite(zl) & np.isfinite(zr) & np.isfinite(zu) & np.isfinite(zd) & np.isfinite(zmap[pys, pxs])
+        with np.errstate(invalid="ignore"):
+            ok &= np.maximum(np.abs(zr - zl), np.abs(zd - zu)) * 0.5 <= edge_tau
+        n = np.cross(P(pxs + 1, pys) - P(pxs - 1, pys), P(pxs, pys + 1) - P(pxs, pys - 1))
+        n /= np.linalg.norm(n, axis=1, keepdims=True)
+        flip = np.einsum("ij,ij->i", n, P(pxs, pys)) > 0
+        n[flip] *= -1
+        nw = n @ Ri
+        cs = -np.einsum("ij,ij->i", ray, nw)
+        ok &= cs > 0
+        w = np.where(ok, cs / np.linalg.norm(X, axis=1), 0.0)
+        c = col.astype(np.float64)
+        cb = ((c[y0, x0] * (1 - ax)[:, None] + c[y0, x1] * ax[:, None]) * (1 - ay)[:, None] +
+              (c[y1, x0] * (1 - ax)[:, None] + c[y1, x1] * ax[:, None]) * ay[:, None])
+        acc += w[:, None] * np.nan_to_num(cb)
+        ws += w
+    rgb = np.zeros((H, W, 3))
+    wsum = np.zeros((H, W))
+    good = ws >= w_min
+    rgb[vv[good], uu[good]] = acc[good] / ws[good, None]
+    wsum[vv, uu] = ws
+    return rgb, wsum

@@ -499,3 +499,149 @@ void tao_zbuffer_resolve(int64_t n, const uint64_t* zkey, float fx, float baseli
         if (dispo) dispo[i] = (fx * baseline) / z;
     }
 }
+
+/* ------------------------------------- NEXT: occlusion-aware input-view blending */
+/*
+ * PAPER.md l.420-444 (Eqs. 6-10): each pixel of the fused depth z_fused (the min-z warp of all
+ * input depth maps into the novel view, tao_zbuffer_view) is lifted (Pi_novel^-1) and projected into
+ * every input view i (Eq. 6); colour c_i and depth z_i are bilinearly sampled there (Eq. 7); the
+ * weight is w_i = M_i(x_i.uv) * Occ(x_i) * cos<r(u,v), n_i> / ||x_i^cam|| (Eq. 8) with
+ * Occ = [|x_i.z - z_i| < delta] (Eq. 9); I_blend = sum w_i c_i / sum w_i (Eq. 10).
+ * reading R24 fixes what the paper leaves open, in this order:
+ *   - input depth z = fx*B/d where the pixel is valid (mask != 0, finite d > d_min), as in a1;
+ *   - sample valid iff the projected centre lies inside [0, W-1] x [0, H-1] and Z > z_near;
+ *     bilinear taps x0 = min(floor(u), W-2) (0 when W == 1), x1 = min(x0+1, W-1), likewise y;
+ *     lerp(a, b, t) = fma(t, b - a, a), rows first; all four depth taps must be valid;
+ *   - M_i: the input mask (through tap validity), the edge mask max(|z_r - z_l|, |z_d - z_u|)/2
+ *     <= edge_tau at the nearest pixel rint(x_i.uv), and a valid normal there (4 neighbours valid);
+ *     the appearance-consistency mask of l.433 is not defined by the paper and not applied;
+ *   - n_i: cross product of the central differences of the lifted camera-space points
+ *     (SPEC.md l.120), normalised, flipped to face camera i, rotated to world (R_i^T n);
+ *   - cos<r, n_i> = max(0, -r_hat . n_w) with r_hat the unit ray from the novel centre to the point;
+ *   - ||x_i^cam|| = the Euclidean norm of the point in camera i's frame;
+ *   - views accumulate in index order; sum w < w_min -> hole: colour 0.
+ * Outputs: rgb[H][W][3], wsum[H][W] (the denominator, 0 on holes of z_fused).
+ */
+typedef struct {
+    int H, W;
+    const float* disp;
+    const uint8_t* mask;
+    tao_intr K;
+    tao_extr RT;
+    float baseline;
+    const float* color;   /* [H][W][3] */
+} tao_bview;
+
+typedef struct { float delta, edge_tau, w_min; } tao_bparams;
+
+static int bview_depth(const tao_bview* v, int x, int y, const tao_params* p, float* z) {
+    if (x < 0 || y < 0 || x >= v->W || y >= v->H) return 0;
+    int64_t i = (int64_t)y * v->W + x;
+    if (v->mask && v->mask[i] == 0) return 0;
+    float d = v->disp[i];
+    if (!isfinite(d) || !(d > p->d_min)) return 0;
+    *z = (v->K.fx * v->baseline) / d;
+    return 1;
+}
+
+static float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
+
+void tao_blend(int V, const tao_bview* views, const tao_params* p, const tao_bparams* bp, const tao_intr* K,
+               const tao_extr* RT, int H, int W, const float* zf, float* rgb, float* wsum) {
+    const float* R = RT->R;
+    const float* t = RT->t;
+    /* novel camera centre C = R^T (0 - t) */
+    float c0 = dot3(R[0], R[3], R[6], -t[0], -t[1], -t[2]);
+    float c1 = dot3(R[1], R[4], R[7], -t[0], -t[1], -t[2]);
+    float c2 = dot3(R[2], R[5], R[8], -t[0], -t[1], -t[2]);
+    for (int v = 0; v < H; v++) {
+        for (int u = 0; u < W; u++) {
+            int64_t pix = (int64_t)v * W + u;
+            float acc[3] = {0.0f, 0.0f, 0.0f}, ws = 0.0f;
+            float z = zf[pix];
+            if (z > 0.0f) {
+                /* Eq. 6: Pi_novel^-1(u, v, z_fused) */
+                float xc = (((float)u - K->cx) / K->fx) * z;
+                float yc = (((float)v - K->cy) / K->fy) * z;
+                float q0 = xc - t[0], q1 = yc - t[1], q2 = z - t[2];
+                float w0 = dot3(R[0], R[3], R[6], q0, q1, q2);
+                float w1 = dot3(R[1], R[4], R[7], q0, q1, q2);
+                float w2 = dot3(R[2], R[5], R[8], q0, q1, q2);
+                float r0 = w0 - c0, r1 = w1 - c1, r2 = w2 - c2;
+                float rl = sqrtf(dot3(r0, r1, r2, r0, r1, r2));
+                r0 = r0 / rl; r1 = r1 / rl; r2 = r2 / rl;
+                for (int i = 0; i < V; i++) {
+                    const tao_bview* bv = views + i;
+                    const float* Ri = bv->RT.R;
+                    const float* ti = bv->RT.t;
+                    float X = dot3(Ri[0], Ri[1], Ri[2], w0, w1, w2) + ti[0];
+                    float Y = dot3(Ri[3], Ri[4], Ri[5], w0, w1, w2) + ti[1];
+                    float Z = dot3(Ri[6], Ri[7], Ri[8], w0, w1, w2) + ti[2];
+                    if (!(Z > p->z_near)) continue;
+                    float us = fmaf(bv->K.fx, X / Z, bv->K.cx);
+                    float vs = fmaf(bv->K.fy, Y / Z, bv->K.cy);
+                    if (!(us >= 0.0f && us <= (float)(bv->W - 1) && vs >= 0.0f && vs <= (float)(bv->H - 1))) continue;
+                    /* Eq. 7: bilinear taps */
+                    int x0 = (int)floorf(us), y0 = (int)floorf(vs);
+                    if (x0 > bv->W - 2) x0 = bv->W >= 2 ? bv->W - 2 : 0;
+                    if (y0 > bv->H - 2) y0 = bv->H >= 2 ? bv->H - 2 : 0;
+                    int x1 = x0 + 1 < bv->W ? x0 + 1 : x0, y1 = y0 + 1 < bv->H ? y0 + 1 : y0;
+                    float ax = us - (float)x0, ay = vs - (float)y0;
+                    float z00, z10, z01, z11;
+                    if (!bview_depth(bv, x0, y0, p, &z00) || !bview_depth(bv, x1, y0, p, &z10) ||
+                        !bview_depth(bv, x0, y1, p, &z01) || !bview_depth(bv, x1, y1, p, &z11))
+                        continue;
+                    float zs = lerpf(lerpf(z00, z10, ax), lerpf(z01, z11, ax), ay);
+                    /* Eq. 9: occlusion (SDF) check */
+                    if (!(fabsf(Z - zs) < bp->delta)) continue;
+                    /* M_i edge mask + normal at the nearest pixel */
+                    int px = (int)rintf(us), py = (int)rintf(vs);
+                    float zc, zl, zr, zu, zd;
+                    if (!bview_depth(bv, px, py, p, &zc) || !bview_depth(bv, px - 1, py, p, &zl) ||
+                        !bview_depth(bv, px + 1, py, p, &zr) || !bview_depth(bv, px, py - 1, p, &zu) ||
+                        !bview_depth(bv, px, py + 1, p, &zd))
+                        continue;
+                    if (fmaxf(fabsf(zr - zl), fabsf(zd - zu)) * 0.5f > bp->edge_tau) continue;
+                    const tao_intr* Ki = &bv->K;
+                    float lx = (((float)(px - 1) - Ki->cx) / Ki->fx) * zl, ly = (((float)py - Ki->cy) / Ki->fy) * zl;
+                    float rx = (((float)(px + 1) - Ki->cx) / Ki->fx) * zr, ry = (((float)py - Ki->cy) / Ki->fy) * zr;
+                    float ux = (((float)px - Ki->cx) / Ki->fx) * zu, uy = (((float)(py - 1) - Ki->cy) / Ki->fy) * zu;
+                    float dx = (((float)px - Ki->cx) / Ki->fx) * zd, dy = (((float)(py + 1) - Ki->cy) / Ki->fy) * zd;
+                    float tx0 = rx - lx, tx1 = ry - ly, tx2 = zr - zl;
+                    float ty0 = dx - ux, ty1 = dy - uy, ty2 = zd - zu;
+                    float n0 = fmaf(tx1, ty2, -(tx2 * ty1));
+                    float n1 = fmaf(tx2, ty0, -(tx0 * ty2));
+                    float n2 = fmaf(tx0, ty1, -(tx1 * ty0));
+                    float nl = sqrtf(dot3(n0, n1, n2, n0, n1, n2));
+                    if (!(nl > 0.0f)) continue;
+                    n0 = n0 / nl; n1 = n1 / nl; n2 = n2 / nl;
+                    float pcx = (((float)px - Ki->cx) / Ki->fx) * zc, pcy = (((float)py - Ki->cy) / Ki->fy) * zc;
+                    if (dot3(n0, n1, n2, pcx, pcy, zc) > 0.0f) { n0 = -n0; n1 = -n1; n2 = -n2; }
+                    float m0 = dot3(Ri[0], Ri[3], Ri[6], n0, n1, n2);
+                    float m1 = dot3(Ri[1], Ri[4], Ri[7], n0, n1, n2);
+                    float m2 = dot3(Ri[2], Ri[5], Ri[8], n0, n1, n2);
+                    /* Eq. 8 */
+                    float cs = -dot3(r0, r1, r2, m0, m1, m2);
+                    if (!(cs > 0.0f)) continue;
+                    float dist = sqrtf(dot3(X, Y, Z, X, Y, Z));
+                    float w = cs / dist;
+                    const float* col = bv->color;
+                    for (int k = 0; k < 3; k++) {
+                        float a00 = col[((int64_t)y0 * bv->W + x0) * 3 + k], a10 = col[((int64_t)y0 * bv->W + x1) * 3 + k];
+                        float a01 = col[((int64_t)y1 * bv->W + x0) * 3 + k], a11 = col[((int64_t)y1 * bv->W + x1) * 3 + k];
+                        float ck = lerpf(lerpf(a00, a10, ax), lerpf(a01, a11, ax), ay);
+                        acc[k] = fmaf(w, ck, acc[k]);
+                    }
+                    ws = ws + w;
+                }
+            }
+            /* Eq. 10 */
+            if (ws >= bp->w_min) {
+                for (int k = 0; k < 3; k++) rgb[pix * 3 + k] = acc[k] / ws;
+            } else {
+                for (int k = 0; k < 3; k++) rgb[pix * 3 + k] = 0.0f;
+            }
+            if (wsum) wsum[pix] = ws;
+        }
+    }
+}

@@ -153,6 +153,37 @@ def _raycast_depth(cam: Camera):
     return z, fg
 
 
+# Procedural surface colour (input-view blending): an RGB pattern fixed in world
+# space, so every view sees the same colour at the same surface point (a Lambertian scene) and the
+# novel view's ground truth is the pattern at its own ray-cast hit.
+_TEX_DIRS = np.array([[1.0, 0.3, 0.2], [-0.2, 1.0, 0.4], [0.3, -0.5, 1.0]])
+_TEX_PHASE = np.array([0.3, 1.7, 2.9])
+TEX_WAVELENGTH = 0.06      # metres
+
+
+def texture(Xw: np.ndarray) -> np.ndarray:
+    """RGB in [0.15, 0.85] of world points (..., 3) -> (..., 3) float64."""
+    arg = 2.0 * np.pi * (Xw @ _TEX_DIRS.T) / TEX_WAVELENGTH + _TEX_PHASE
+    return 0.5 + 0.35 * np.sin(arg)
+
+
+def raycast_points(cam: Camera):
+    """World point of the first hit (ellipsoids, else the background plane) per pixel + fg mask."""
+    z, fg = _raycast_depth(cam)
+    H, W = cam.H, cam.W
+    xs = (np.arange(W, dtype=np.float64) - cam.cx) / cam.fx
+    ys = (np.arange(H, dtype=np.float64) - cam.cy) / cam.fy
+    Xc = np.stack(np.broadcast_arrays(xs[None, :] * z, ys[:, None] * z, z), axis=-1)
+    Xw = (Xc - cam.t) @ cam.R
+    return Xw, fg
+
+
+def view_colors(cam: Camera) -> np.ndarray:
+    """The RGB image [H][W][3] float32 a camera sees of the textured synthetic scene."""
+    Xw, _ = raycast_points(cam)
+    return texture(Xw).astype(np.float32)
+
+
 def _rig_view(name: str, res: int, rng, log_mu: float, alpha_lo: float, C: int) -> SourceView:
     centre, baseline = RIG_CAMS[name]
     R, t = look_at(centre, RIG_LOOK)

@@ -174,6 +174,30 @@ ta_status ta_zbuffer(ta_context* ctx, const ta_source_view* views, int32_t V, co
                      int32_t splat_radius, float baseline_tgt, float* depth_out, float* disp_out, void* stream);
 
 /*
+ * occlusion-aware input-view blending (Eqs. 6-10;
+ * DESIGN.md reading R24).  For every pixel (u, v) of the novel camera (K_tgt, RT_tgt, H x W) with
+ * z_fused > 0 (device float [H][W], e.g. ta_zbuffer of all input views into the novel camera):
+ * lift (Eq. 6), project into each of the V input views, sample colour and depth bilinearly (Eq. 7),
+ * weight w_i = M_i * Occ * cos<r, n_i> / ||x_i^cam|| (Eqs. 8-9) and write
+ * I_blend = sum w_i c_i / sum w_i (Eq. 10); sum w_i < w_min leaves a hole (colour 0).
+ *   views      the input views: disparity (z = fx*B/d), mask, K, RT, baseline are read
+ *   colors     host array of V device pointers, view i's colour image float [H_i][W_i][3]
+ *   rgb_out    device float [H][W][3];  wsum_out  device float [H][W] (the denominator) or NULL
+ * Reads params->d_min, z_near.  Errors: TA_ERR_INVALID_ARG for NULL pointers, bad sizes, bad cameras,
+ * delta <= 0, edge_tau <= 0, w_min < 0.
+ */
+typedef struct {
+    float delta;       /* Eq. 9 SDF threshold (m), default 0.01 */
+    float edge_tau;    /* edge mask: max central depth gradient (m / px), default 0.02 */
+    float w_min;       /* hole threshold on sum w_i, default 1e-4 */
+} ta_blend_params;
+void ta_default_blend_params(ta_blend_params* bp);
+ta_status ta_blend(ta_context* ctx, const ta_source_view* views, int32_t V, const float* const* colors,
+                   const ta_raster_params* params, const ta_blend_params* bp, const ta_intrinsics* K_tgt,
+                   const ta_extrinsics* RT_tgt, int32_t H, int32_t W, const float* z_fused, float* rgb_out,
+                   float* wsum_out, void* stream);
+
+/*
  * Introspection of the LAST ta_rasterize call on this context (device pointers into context
  * scratch, valid until the next call; read them on the same stream after it completes).
  *   records     [n][8] 32-bit words per Gaussian (array order): mean_x, mean_y, conic a, conic 2b,

@@ -13,6 +13,7 @@ package is the thin Python binding (argument marshalling) plus the multi-GPU har
 from __future__ import annotations
 
 from ._lib import (TA_FLAG_ASYNC, TA_FLAG_DEBUG_COUNTS, Context, GaussianBuffers, TaError, default_params,
+                   default_blend_params,
                    extrinsics, intrinsics, lib, source_view)
 
 __all__ = ["Context", "GaussianBuffers", "TaError", "default_params", "unproject", "rasterize", "views_to_device",

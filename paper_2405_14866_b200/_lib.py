@@ -49,6 +49,10 @@ class RasterParams(C.Structure):
                 ("default_scale", C.c_float), ("default_opacity", C.c_float), ("flags", C.c_uint32)]
 
 
+class BlendParams(C.Structure):
+    _fields_ = [("delta", C.c_float), ("edge_tau", C.c_float), ("w_min", C.c_float)]
+
+
 class DebugView(C.Structure):
     _fields_ = [("n", C.c_int64), ("K", C.c_int64), ("Kc", C.c_int64), ("P", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("sort_passes", C.c_int32), ("records", C.c_void_p),
@@ -65,7 +69,7 @@ class Profile(C.Structure):
 
 
 EXPORTS = ("ta_profile_enable", "ta_profile_read", "ta_default_params", "ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject",
-           "ta_zbuffer",
+           "ta_zbuffer", "ta_blend", "ta_default_blend_params",
            "ta_rasterize", "ta_debug_last", "ta_check_overflow", "ta_launch_count", "ta_status_string",
            "ta_last_error", "ta_build_info")
 
@@ -92,6 +96,9 @@ def lib(build_if_stale: bool = False):
     L.ta_rasterize.argtypes = [P, C.POINTER(Gaussians), i64, C.POINTER(Intrinsics), C.POINTER(Extrinsics), i32, i32,
                                C.POINTER(RasterParams), P, P, P]
     L.ta_debug_last.argtypes = [P, C.POINTER(DebugView), P]
+    L.ta_default_blend_params.argtypes = [C.POINTER(BlendParams)]
+    L.ta_blend.argtypes = [P, C.POINTER(SourceView), i32, C.POINTER(P), C.POINTER(RasterParams), C.POINTER(BlendParams),
+                           C.POINTER(Intrinsics), C.POINTER(Extrinsics), i32, i32, P, P, P, P]
     L.ta_zbuffer.argtypes = [P, C.POINTER(SourceView), i32, C.POINTER(RasterParams), C.POINTER(Intrinsics),
                              C.POINTER(Extrinsics), i32, i32, i32, C.c_float, P, P, P]
     L.ta_check_overflow.argtypes = [P, P, C.POINTER(i32)]
@@ -104,7 +111,7 @@ def lib(build_if_stale: bool = False):
     L.ta_last_error.argtypes = [P]
     L.ta_last_error.restype = C.c_char_p
     L.ta_build_info.restype = C.c_char_p
-    for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize", "ta_zbuffer",
+    for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize", "ta_zbuffer", "ta_blend",
                  "ta_debug_last", "ta_check_overflow", "ta_profile_enable", "ta_profile_read"):
         getattr(L, name).restype = i32
     _lib = L
@@ -188,6 +195,14 @@ class Context:
                                      int(W), int(radius), float(baseline_tgt), _ptr(depth_out), _ptr(disp_out),
                                      _stream(stream)))
 
+    def blend(self, views, colors, params: RasterParams, bp: "BlendParams", K: Intrinsics, RT: Extrinsics, H, W,
+              z_fused, rgb_out, wsum_out=None, stream=None):
+        """NEXT #1 occlusion-aware blending (include/ta.h ta_blend): colors = CUDA tensors [H_i, W_i, 3]."""
+        arr = (SourceView * len(views))(*views)
+        cp = (C.c_void_p * len(colors))(*[c.data_ptr() for c in colors])
+        self._check(lib().ta_blend(self._h, arr, len(views), cp, C.byref(params), C.byref(bp), C.byref(K), C.byref(RT),
+                                   int(H), int(W), _ptr(z_fused), _ptr(rgb_out), _ptr(wsum_out), _stream(stream)))
+
     def rasterize(self, g: "GaussianBuffers", n, K: Intrinsics, RT: Extrinsics, H, W, params: RasterParams,
                   feat_out, alpha_out, stream=None):
         gs = g.struct()
@@ -244,3 +259,11 @@ def source_view(H, W, disparity, mask, K, R, t, baseline, scale, quat, opacity, 
     """Marshal one source view of device tensors (None -> NULL) into the C struct."""
     return SourceView(int(H), int(W), _ptr(disparity), _ptr(mask), intrinsics(K), extrinsics(R, t), float(baseline),
                       _ptr(scale), _ptr(quat), _ptr(opacity), _ptr(feat))
+
+
+def default_blend_params(**kw) -> BlendParams:
+    bp = BlendParams()
+    lib().ta_default_blend_params(C.byref(bp))
+    for k, v in kw.items():
+        setattr(bp, k, v)
+    return bp

@@ -603,6 +603,64 @@ ta_status ta_zbuffer(ta_context* c, const ta_source_view* views, int32_t V, cons
     return TA_OK;
 }
 
+void ta_default_blend_params(ta_blend_params* bp) {
+    if (!bp) return;
+    bp->delta = 0.01f;
+    bp->edge_tau = 0.02f;
+    bp->w_min = 1e-4f;
+}
+
+ta_status ta_blend(ta_context* c, const ta_source_view* views, int32_t V, const float* const* colors,
+                   const ta_raster_params* p, const ta_blend_params* bp, const ta_intrinsics* K,
+                   const ta_extrinsics* RT, int32_t H, int32_t W, const float* z_fused, float* rgb_out,
+                   float* wsum_out, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!views || !colors || !p || !bp || !K || !RT || !z_fused || !rgb_out)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_blend: NULL argument");
+    if (V < 1 || V > TA_MAX_VIEWS) return fail(c, TA_ERR_UNSUPPORTED, "ta_blend: V = %d not in [1, %d]", V, TA_MAX_VIEWS);
+    if (H < 1 || W < 1 || H > 32767 || W > 32767) return fail(c, TA_ERR_INVALID_ARG, "bad target size %d x %d", H, W);
+    if (!(bp->delta > 0.0f) || !(bp->edge_tau > 0.0f) || !(bp->w_min >= 0.0f) || !std::isfinite(bp->delta) ||
+        !std::isfinite(bp->edge_tau) || !std::isfinite(bp->w_min))
+        return fail(c, TA_ERR_INVALID_ARG, "blend params: delta > 0, edge_tau > 0, w_min >= 0");
+    if (!std::isfinite(p->z_near) || !std::isfinite(p->d_min)) return fail(c, TA_ERR_INVALID_ARG, "non-finite params");
+    ta_status st;
+    if (!finite_cam(*K, *RT, c, &st)) return st;
+    BlendTable bt;
+    memset(&bt, 0, sizeof(bt));
+    bt.V = V;
+    bt.d_min = p->d_min; bt.z_near = p->z_near;
+    bt.delta = bp->delta; bt.edge_tau = bp->edge_tau; bt.w_min = bp->w_min;
+    for (int i = 0; i < V; i++) {
+        const ta_source_view& s = views[i];
+        if (s.H < 1 || s.W < 1 || s.H > 32767 || s.W > 32767)
+            return fail(c, TA_ERR_INVALID_ARG, "view %d: bad size %d x %d", i, s.H, s.W);
+        if (!s.disparity || !colors[i]) return fail(c, TA_ERR_INVALID_ARG, "view %d: NULL disparity / colour", i);
+        if (!(s.baseline > 0.0f) || !std::isfinite(s.baseline))
+            return fail(c, TA_ERR_INVALID_ARG, "view %d: baseline must be > 0", i);
+        if (!finite_cam(s.K, s.RT, c, &st)) return st;
+        BlendView& b = bt.v[i];
+        b.disp = s.disparity; b.mask = s.mask; b.color = colors[i];
+        b.fx = s.K.fx; b.fy = s.K.fy; b.cx = s.K.cx; b.cy = s.K.cy;
+        b.fxB = s.K.fx * s.baseline;            // the oracle's (fx * B), one fp32 product
+        memcpy(b.R, s.RT.R, sizeof(b.R));
+        memcpy(b.t, s.RT.t, sizeof(b.t));
+        b.H = s.H; b.W = s.W;
+    }
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    TargetCam cam;
+    cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
+    memcpy(cam.R, RT->R, sizeof(cam.R));
+    memcpy(cam.t, RT->t, sizeof(cam.t));
+    cam.W = W; cam.H = H;
+    cam.Wm1f = (float)(W - 1);
+    cam.Hm1f = (float)(H - 1);
+    const uint32_t npix = (uint32_t)H * (uint32_t)W;
+    k_blend<<<(npix + 255) / 256, 256, 0, s>>>(bt, cam, z_fused, rgb_out, wsum_out);
+    TA_LAUNCHED(c);
+    return TA_OK;
+}
+
 ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     if (!c || !out) return TA_ERR_INVALID_ARG;
     if (!c->have_last) return fail(c, TA_ERR_INVALID_ARG, "no rasterize call yet");

@@ -94,6 +94,22 @@ void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, Composite
                              unsigned long long* status, uint32_t* counter, unsigned long long* total, uint32_t* out_list,
                              uint64_t out_cap, int pass, cudaStream_t st);
 
+// blend.cu
+struct BlendView {
+    const float* disp;
+    const uint8_t* mask;
+    const float* color;   // [H][W][3]
+    float fx, fy, cx, cy, fxB;
+    float R[9], t[3];
+    int H, W;
+};
+struct BlendTable {
+    BlendView v[kMaxViews];
+    int V;
+    float d_min, z_near, delta, edge_tau, w_min;
+};
+__global__ void k_blend(BlendTable bt, TargetCam cam, const float* zf, float* rgb, float* wsum);
+
 // zbuffer.cu
 __global__ void k_zb_clear(unsigned long long* zk, uint32_t n);
 __global__ void k_zb_splat(ViewTable vt, TargetCam cam, float z_near, int radius, unsigned long long* zk);

@@ -28,7 +28,7 @@ __all__ = [
     "rot_y", "make_random_scene",
 ]
 
-CONFIG_NAMES = ("tiny", "c2", "c3", "c4", "c5")
+CONFIG_NAMES = ("tiny", "c2", "c3", "c4", "c5", "paper")
 
 
 @dataclass
@@ -276,7 +276,32 @@ def make_config(name: str, seed: int = 0, res: Optional[int] = None,
         th, tw = target_hw or (r, r)
         return make_rig_scene("c5", r, ("cam0", "cam1", "cam2", "cam3"), 64, math.log(0.008), 0.2,
                               _parallax_targets(n_targets or 8, tw, th), seed)
+    if name == "paper":
+        # SURVEY 8(f) NEXT #3, the paper-exact variant: the three lifted views cam0, cam2, cam3
+        # (P:358), rotation = identity (no quaternion map, so Sigma_w is diagonal), and the
+        # two eye targets of one viewer per frame (left / right eye 64 mm apart on the c3 arc,
+        # looking at S).  Same depth / scale / opacity / feature distributions as c3.
+        r = res or 1024
+        th, tw = target_hw or (r, r)
+        sc = make_rig_scene("paper", r, ("cam0", "cam2", "cam3"), 32, math.log(0.004), 0.5, eye_targets(tw, th), seed)
+        for v in sc.views:
+            v.quat = None
+        return sc
     raise ValueError(f"unknown config {name!r}; expected one of {CONFIG_NAMES}")
+
+
+IPD = 0.064   # metres between the two eye targets of the paper-exact variant
+
+
+def eye_targets(W: int, H: int) -> List[Camera]:
+    """Left and right eye cameras: the c3 target centre moved -/+ IPD/2 along the display's x axis,
+    both looking at S."""
+    c = _arc_centre()
+    out = []
+    for sgn in (-1.0, 1.0):
+        R, t = look_at(c + np.array([sgn * IPD / 2.0, 0.0, 0.0]), RIG_LOOK)
+        out.append(_pinhole(W, H, FOCAL_SCALE, R, t))
+    return out
 
 
 def make_random_scene(seed: int, H: int = 48, W: int = 48, C: int = 8, n_src: int = 24,
@@ -337,6 +362,10 @@ def make_targets(name: str, res: Optional[int] = None, target_hw: Optional[tuple
         r = res or 2048
         th, tw = target_hw or (r, r)
         return _parallax_targets(n_targets or 8, tw, th)
+    if name == "paper":
+        r = res or 1024
+        th, tw = target_hw or (r, r)
+        return eye_targets(tw, th)
     return make_config(name, res=res, target_hw=target_hw, n_targets=n_targets).targets
 
 

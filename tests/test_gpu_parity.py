@@ -95,6 +95,33 @@ def test_c3_full_size_sampled_tiles(ctx, oracle_lib):
     assert out["n"] == 1666464
 
 
+@pytest.mark.parametrize("eye", [0, 1])
+def test_paper_variant_reduced(ctx, oracle_lib, eye):
+    """SURVEY 8(f) NEXT #3, the paper-exact variant: cam0 + cam2 + cam3 lifted
+    with R = I (diagonal Sigma_w), both eye targets -- every stage, every pixel at 256^2."""
+    s = sg.make_config("paper", res=256)
+    assert len(s.views) == 3 and all(v.quat is None for v in s.views)
+    full_parity(ctx, oracle_lib, s, tidx=eye)
+
+
+def test_paper_variant_full_size_sampled_tiles(ctx, oracle_lib):
+    """The paper-exact variant at 1024^2 (3 x 1024^2 sources), right eye: a1-a5 bit-exact in full,
+    a6 on the 6 longest tile lists + 10 seeded random non-empty tiles."""
+    s = sg.make_config("paper")
+    cam = s.targets[1]
+    import oracle as O
+    op = P.oracle_params(s)
+    go = O.unproject(s, op)
+    K, R, t = sg.cam_arrays(cam)
+    pr = O.project(go, K, R, t, cam.H, cam.W, op)
+    ranges, _ = O.tile_lists(pr, go["ids"], cam.H, cam.W)
+    lens = ranges[:, 1].astype(np.int64) - ranges[:, 0]
+    rng = np.random.default_rng(3)
+    tiles = np.unique(np.concatenate([np.argsort(lens)[-6:],
+                                      rng.choice(np.nonzero(lens)[0], 10, replace=False)])).astype(np.int32)
+    full_parity(ctx, oracle_lib, s, tidx=1, tiles=tiles)
+
+
 def test_c4_views_vs_single_view(ctx, oracle_lib):
     """configs[3]: one Gaussian set, several parallax targets on one context; each equals the oracle
     on sampled tiles (the 32-view batch at reduced source resolution)."""

@@ -90,21 +90,21 @@ static float dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
 /*
  * exp_det -- DESIGN.md reading R13.  exp(x) for x <= 0 by a fixed fp32 sequence:
  * k = the integer nearest (ties to even) to the exact product x*log2 e, obtained with one
- * rounding as fma(x, log2 e, 1.5*2^23) - 1.5*2^23; Cody-Waite reduction r = x - k*ln2 (hi/lo split); degree-7
- * Taylor polynomial in Horner form with fmaf; scale by 2^k (exact).  Pinned in
+ * rounding as fma(x, log2 e, 1.5*2^23) - 1.5*2^23; reduction r = fma(-k, fl(ln 2), x) (one
+ * constant: |k| <= 7 on the used range x >= -4.5, so the ln 2 rounding costs < 0.25 ulp);
+ * p = 1 + r + c2 r^2 + ... + c6 r^6 (relative-error minimax on [-ln2/2, ln2/2], fp32
+ * coefficients, max error 0.07 ulp) in Horner form with fmaf; scale by 2^k (exact).  Pinned in
  * tests/test_oracle_pins.py against float64 exp over [-4.5, 0] (<= 2 ulp).
  */
 float tao_exp_det(float x) {
     if (x < -80.0f) x = -80.0f;
     float k = fmaf(x, 1.44269502162933349609375f, 12582912.0f) - 12582912.0f;   /* float(log2 e) */
-    float r = fmaf(-k, 0.693145751953125f, x);                  /* ln2 hi */
-    r = fmaf(-k, 1.428606765330187045037746429443359375e-06f, r); /* ln2 lo */
-    float p = 1.98412698412698412698e-4f;                       /* 1/5040 */
-    p = fmaf(p, r, 1.38888888888888888889e-3f);                 /* 1/720 */
-    p = fmaf(p, r, 8.33333333333333333333e-3f);                 /* 1/120 */
-    p = fmaf(p, r, 4.16666666666666666667e-2f);                 /* 1/24 */
-    p = fmaf(p, r, 1.66666666666666666667e-1f);                 /* 1/6 */
-    p = fmaf(p, r, 0.5f);
+    float r = fmaf(-k, 0.693147182464599609375f, x);                             /* float(ln 2) */
+    float p = 1.3814548728987575e-3f;
+    p = fmaf(p, r, 8.36869515478611e-3f);
+    p = fmaf(p, r, 4.166838899254799e-2f);
+    p = fmaf(p, r, 1.666652113199234e-1f);
+    p = fmaf(p, r, 4.999999403953552e-1f);
     p = fmaf(p, r, 1.0f);
     p = fmaf(p, r, 1.0f);
     uint32_t sb = (uint32_t)((int)k + 127) << 23;

@@ -14,7 +14,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "-diag-suppress", "550"]
+         "-diag-suppress", "550", *os.environ.get("TA_NVCC_EXTRA", "").split()]
 SOURCES = ["api.cu", "raster.cu", "composite.cu", "unproject.cu", "zbuffer.cu", "blend.cu"]
 
 

@@ -34,18 +34,17 @@ __device__ __forceinline__ float dot3(float a0, float a1, float a2, float b0, fl
     return ffma(a2, b2, ffma(a1, b1, fmul(a0, b0)));
 }
 
-// DESIGN.md R13 exp_det: exp(x), x <= 0, by a fixed fp32 sequence (Cody-Waite + degree-7 Taylor).
+// DESIGN.md R13 exp_det: exp(x), x <= 0, by a fixed fp32 sequence (nearest-even k, one-constant
+// reduction, degree-6 relative minimax polynomial).
 __device__ __forceinline__ float exp_det(float x) {
     x = fmaxf(x, -80.0f);
     const float k = fsub(ffma(x, 1.44269502162933349609375f, 12582912.0f), 12582912.0f);   // nearest-even of x*log2e
-    float r = ffma(-k, 0.693145751953125f, x);
-    r = ffma(-k, 1.428606765330187045037746429443359375e-06f, r);
-    float p = 1.98412698412698412698e-4f;
-    p = ffma(p, r, 1.38888888888888888889e-3f);
-    p = ffma(p, r, 8.33333333333333333333e-3f);
-    p = ffma(p, r, 4.16666666666666666667e-2f);
-    p = ffma(p, r, 1.66666666666666666667e-1f);
-    p = ffma(p, r, 0.5f);
+    const float r = ffma(-k, 0.693147182464599609375f, x);
+    float p = 1.3814548728987575e-3f;
+    p = ffma(p, r, 8.36869515478611e-3f);
+    p = ffma(p, r, 4.166838899254799e-2f);
+    p = ffma(p, r, 1.666652113199234e-1f);
+    p = ffma(p, r, 4.999999403953552e-1f);
     p = ffma(p, r, 1.0f);
     p = ffma(p, r, 1.0f);
     const float s = __int_as_float(((int)k + 127) << 23);

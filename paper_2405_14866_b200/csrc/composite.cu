@@ -127,14 +127,12 @@ __device__ __forceinline__ float2 exp_det2(float2 x) {
     const float2 t = fma2(x, bc2(1.44269502162933349609375f), bc2(kMagic));
     const float2 k = sub2(t, bc2(kMagic));
     const float2 nk = make_float2(-k.x, -k.y);
-    float2 r = fma2(nk, bc2(0.693145751953125f), x);
-    r = fma2(nk, bc2(1.428606765330187045037746429443359375e-06f), r);
-    float2 p = bc2(1.98412698412698412698e-4f);
-    p = fma2(p, r, bc2(1.38888888888888888889e-3f));
-    p = fma2(p, r, bc2(8.33333333333333333333e-3f));
-    p = fma2(p, r, bc2(4.16666666666666666667e-2f));
-    p = fma2(p, r, bc2(1.66666666666666666667e-1f));
-    p = fma2(p, r, bc2(0.5f));
+    const float2 r = fma2(nk, bc2(0.693147182464599609375f), x);
+    float2 p = bc2(1.3814548728987575e-3f);
+    p = fma2(p, r, bc2(8.36869515478611e-3f));
+    p = fma2(p, r, bc2(4.166838899254799e-2f));
+    p = fma2(p, r, bc2(1.666652113199234e-1f));
+    p = fma2(p, r, bc2(4.999999403953552e-1f));
     p = fma2(p, r, bc2(1.0f));
     p = fma2(p, r, bc2(1.0f));
     const int kx = __float_as_int(t.x) - 0x4b400000, ky = __float_as_int(t.y) - 0x4b400000;
@@ -600,9 +598,13 @@ __device__ __forceinline__ float2 tstep(float2 qm, float2 a, float qmax, float a
 // Skip the exp / recurrence of an entry pair no pixel can take (saves ~13 % of pairs, but the
 // warp-wide vote + branch splits the unrolled loop into basic blocks the scheduler cannot overlap).
 constexpr bool kSkipEmptyPairs = false;
+#ifndef TA_TC_MIN_BLOCKS
+#define TA_TC_MIN_BLOCKS 4
+#endif
+constexpr int kTcMinBlocks = TA_TC_MIN_BLOCKS;   // CTAs per SM the register budget targets
 
 template <int C, bool kCounts>
-__global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
+__global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : kTcMinBlocks))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
                const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
                const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256) k_project(const float4* __restrict__ pos_
                                                  uint32_t* __restrict__ val0) {
     __shared__ uint32_t s_or[8], s_and[8], s_cnt[8];
     const uint32_t n = cs->n;
+    if (blockIdx.x * blockDim.x >= n) return;              // whole block past the count (uniform)
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     bool vis = false;
     uint32_t key = kCulledKey;

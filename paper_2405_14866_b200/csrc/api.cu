@@ -488,7 +488,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
 
     StageTimer tm(c, s);
     tm.begin(TA_STAGE_PROJECT);
-    k_init<<<std::min(1024, (n_status + 255) / 256 + 1), 256, 0, s>>>(cs, status, n_status, n, g->n_dev, bin_len);
+    k_init<<<std::min(1024, (n_status + 255) / 256 + 1), 256, 0, s>>>(cs, status, n_status, n, g->n_dev,
+                                                                       kBinTileRanks(bg.nw), (uint32_t)NB);
     TA_LAUNCHED(c);
     const int64_t cap_blocks = (cap + 255) / 256;
     if (cap_blocks > 0) {
@@ -525,7 +526,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_BIN_SCAN);
-    launch_scan(offs, nullptr, bin_len, status + (size_t)4 * region, &cs->scan_counter[4], &cs->K, s);
+    launch_scan(offs, &cs->bin_len, bin_len, status + (size_t)4 * region, &cs->scan_counter[4], &cs->K, s);
     TA_LAUNCHED(c);
     if (!async) {
         TA_CUDA(c, cudaMemcpyAsync(c->pinned, &cs->K, 8, cudaMemcpyDeviceToHost, s));
@@ -698,7 +699,7 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     out->n = h.n;
     out->K = (int64_t)K;
     out->Kc = (int64_t)h.K;
-    out->P = (int32_t)c->last_P;
+    out->P = (int32_t)h.bin_P;
     out->tiles_x = cg.TX;
     out->tiles_y = cg.TY;
     out->sort_passes = passes;

@@ -93,7 +93,8 @@ struct CallState {
     uint32_t key_or, key_and;      // OR / AND of visible depth keys -> varying bit range
     uint32_t sort_parts;           // depth-sort partitions (blocks): ceil(n / kSortKeysPerBlock)
     uint32_t sort_len;             // 256 * sort_parts
-    uint32_t bin_len;              // coarse bins + 1 (bin_start entries)
+    uint32_t bin_len;              // NB * bin_P + 1 (bin-major run starts + the total)
+    uint32_t bin_P;                // rank tiles of this call (ceil(n / ranks per tile))
     uint32_t overflow;             // sticky: entries exceeded the list capacity (not reset by k_init)
     uint32_t scan_counter[8];      // tile counters of the look-back scans (one per scan)
     unsigned long long work[8];    // compositor work counters (TA_FLAG_DEBUG_COUNTS only, reset by k_init)

@@ -393,8 +393,9 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint4* __restrict__ r
     const int nq = 1 << (2 * sb);
     const int bin = blockIdx.x;
     const int bxi = bin % cg.BX, byi = bin / cg.BX;
-    const uint32_t cstart = coffs[(size_t)bin * cg.P];
-    uint32_t cend = coffs[(size_t)(bin + 1) * cg.P];
+    const uint32_t P = cs->bin_P;                     // bin-major [NB x P] run starts (this call's P)
+    const uint32_t cstart = coffs[(size_t)bin * P];
+    uint32_t cend = coffs[(size_t)(bin + 1) * P];
     if (cend > clist_cap) cend = (uint32_t)clist_cap;
     const uint32_t len = cend > cstart ? cend - cstart : 0u;
     const uint32_t segl = (((len + 31u) / 32u) + 31u) & ~31u;          // entries per warp (multiple of 32)

@@ -55,7 +55,7 @@ constexpr int kUnprojPix = 4 * kUnprojThreads;   // pixels per block
 
 // raster.cu
 __global__ void k_init(CallState* cs, unsigned long long* status, int n_status, int64_t n_host,
-                       const int64_t* n_dev, uint32_t bin_len);
+                       const int64_t* n_dev, uint32_t bin_ranks, uint32_t nbins);
 __global__ void k_project(const float4* pos_alpha, const float4* cov, TargetCam cam, RasterConsts rc,
                           CallState* cs, uint4* rec, uint32_t* key0, uint32_t* val0);
 __global__ void k_sort_hist(const uint32_t* keys_a, const uint32_t* keys_b, int pass, const CallState* cs,

@@ -19,7 +19,7 @@ namespace ta {
 
 // ----------------------------------------------------------------------------- k_init
 __global__ void k_init(CallState* __restrict__ cs, unsigned long long* __restrict__ status, int n_status,
-                       int64_t n_host, const int64_t* __restrict__ n_dev, uint32_t bin_len) {
+                       int64_t n_host, const int64_t* __restrict__ n_dev, uint32_t bin_ranks, uint32_t nbins) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     for (int k = i; k < n_status; k += gridDim.x * blockDim.x) status[k] = 0ull;
     if (i == 0) {
@@ -32,7 +32,9 @@ __global__ void k_init(CallState* __restrict__ cs, unsigned long long* __restric
         cs->key_and = 0xffffffffu;
         cs->sort_parts = (uint32_t)((n + kSortKeysPerBlock - 1) / kSortKeysPerBlock);
         cs->sort_len = 256u * cs->sort_parts;
-        cs->bin_len = bin_len;
+        cs->bin_P = (uint32_t)((n + bin_ranks - 1) / bin_ranks);    // rank tiles of this call's n
+        if (cs->bin_P == 0) cs->bin_P = 1;
+        cs->bin_len = nbins * cs->bin_P + 1;
         for (int k = 0; k < 8; k++) cs->scan_counter[k] = 0u;
         for (int k = 0; k < 8; k++) cs->work[k] = 0ull;
     }
@@ -291,7 +293,8 @@ __global__ void __launch_bounds__(256) k_bin_count(const uint2* __restrict__ box
                                                    BinGeom bg, uint32_t* __restrict__ counts) {
     extern __shared__ uint32_t s_h[];
     const int NB = bg.TX * bg.TY;
-    const uint32_t tile = blockIdx.x, P = gridDim.x;
+    const uint32_t tile = blockIdx.x, P = cs->bin_P;
+    if (tile >= P) return;                                  // grid sized for the capacity
     for (int k = threadIdx.x; k < NB; k += blockDim.x) s_h[k] = 0u;
     if (tile == 0 && threadIdx.x == 0) counts[(size_t)NB * P] = 0u;
     __syncthreads();
@@ -312,7 +315,8 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
     const int nw = blockDim.x >> 5;
     const int NB = bg.TX * bg.TY;
     const uint32_t n = cs->n;
-    const uint32_t tile = blockIdx.x, P = gridDim.x;
+    const uint32_t tile = blockIdx.x, P = cs->bin_P;
+    if (tile >= P) return;
     for (int k = threadIdx.x; k < (nw * NB) / 2; k += blockDim.x)       // 2 nw NB words (NB even or not)
         reinterpret_cast<uint4*>(s_cnt)[k] = make_uint4(0u, 0u, 0u, 0u);
     if (threadIdx.x == 0 && (nw * NB) % 2) { s_cnt[2 * nw * NB - 2] = 0u; s_cnt[2 * nw * NB - 1] = 0u; }

@@ -72,6 +72,7 @@ def lib():
         _lib.tao_zbuffer_view.argtypes = [i32, i32, P, P, P, P, C.c_float, P, i64, P, P, i32, i32, i32, P]
         _lib.tao_zbuffer_resolve.argtypes = [i64, P, C.c_float, C.c_float, P, P]
         _lib.tao_blend.argtypes = [i32, P, P, P, P, P, i32, i32, P, P, P]
+        _lib.tao_composite_backward.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P]
         _lib.tao_composite_bruteforce.argtypes = [i32, i32, i32, i32, i64, P, P, P, P, P, P, P, P, P,
                                                   i32, i32, P, P, P]
     return _lib
@@ -282,3 +283,19 @@ def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, pa
     lib().tao_blend(len(views), arr, C.byref(p), C.byref(bp), C.byref(_intr(Kn)), C.byref(_extr(Rn, tn)), cam.H,
                     cam.W, _p(zf), _p(rgb), _p(ws))
     return rgb, ws
+
+
+def composite_backward(g, pr, ranges, lst, H, W, GF, GA, params=None):
+    """NEXT #4 (R25): gradients of L = sum G_F . F + G_A A of the tiled a6 forward with
+    respect to each Gaussian's mean2 [n,2], conic (ca, cb2, cc) [n,3], alpha [n] and feature row
+    [n,C] (array order; float64 sums of fp32 per-pixel terms)."""
+    p = params or make_params()
+    feat = np.ascontiguousarray(g["feat"])
+    n, Cc = feat.shape
+    out = dict(mean2=np.zeros((n, 2)), conic=np.zeros((n, 3)), alpha=np.zeros(n), feat=np.zeros((n, Cc)))
+    lib().tao_composite_backward(H, W, Cc, feat.dtype.itemsize, _p(np.ascontiguousarray(g["alpha"], np.float32)),
+                                 _p(pr["mean2"]), _p(pr["conic"]), _p(pr["rect"]), _p(feat), _p(ranges),
+                                 _p(np.ascontiguousarray(lst, np.int64)), C.byref(p),
+                                 _p(np.ascontiguousarray(GF, np.float32)), _p(np.ascontiguousarray(GA, np.float32)),
+                                 _p(out["mean2"]), _p(out["conic"]), _p(out["alpha"]), _p(out["feat"]))
+    return out

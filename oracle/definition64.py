@@ -242,3 +242,38 @@ def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, z_
     rgb[vv[good], uu[good]] = acc[good] / ws[good, None]
     wsum[vv, uu] = ws
     return rgb, wsum
+
+
+def composite2d(mean, conic, alpha, feat, rect, order, H, W, alpha_max=0.99, alpha_min=1.0 / 255.0, t_eps=1e-4,
+                cull_sigma=3.0):
+    """a6 in float64 from 2D splat parameters (mean [n,2], conic (ca, cb2, cc) [n,3] with
+    q = ca dx^2 + cb2 dx dy + cc dy^2, alpha, feat, pixel box rect [n,4]) composited in `order`
+    (array indices, front to back).  Returns (F[H,W,C], A[H,W], set) where set[(py, px)] is the tuple
+    of composited indices (to detect decision flips).  Used by the backward-pass pins."""
+    order = np.asarray(order)
+    m, cn, al, f, rc = mean[order], conic[order], alpha[order], feat[order], rect[order]
+    C = f.shape[1]
+    F = np.zeros((H, W, C))
+    A = np.zeros((H, W))
+    used = {}
+    for py in range(H):
+        for px in range(W):
+            sel = np.nonzero((rc[:, 0] <= px) & (px <= rc[:, 1]) & (rc[:, 2] <= py) & (py <= rc[:, 3]))[0]
+            if len(sel) == 0:
+                continue
+            dx = px - m[sel, 0]
+            dy = py - m[sel, 1]
+            q = cn[sel, 0] * dx * dx + cn[sel, 1] * dx * dy + cn[sel, 2] * dy * dy
+            a = np.minimum(alpha_max, al[sel] * np.exp(-0.5 * q))
+            use = (q <= cull_sigma ** 2) & (a >= alpha_min)
+            sel, a = sel[use], a[use]
+            if len(sel) == 0:
+                continue
+            Tn = np.cumprod(1.0 - a)
+            stop = np.nonzero(Tn < t_eps)[0]
+            k = stop[0] if len(stop) else len(a)
+            Tb = np.concatenate([[1.0], Tn[:k]])
+            F[py, px] = (a[:k] * Tb[:k]) @ f[sel[:k]]
+            A[py, px] = 1.0 - Tb[k]
+            used[(py, px)] = tuple(order[sel[:k]])
+    return F, A, used

@@ -645,3 +645,99 @@ void tao_blend(int V, const tao_bview* views, const tao_params* p, const tao_bpa
         }
     }
 }
+
+/* --------------------------------------------- NEXT: compositing backward pass */
+/*
+ * Gradients of L = sum_p G_F(p) . F(p) + G_A(p) A(p) with respect to each Gaussian's 2D splat
+ * parameters (mean2, conic (ca, cb2, cc) as in the records, alpha) and its feature row, for the a6
+ * forward of P:386 (the differentiable rasterizer of [kerbl20233d]).  DESIGN.md reading R25:
+ * the per-pixel decisions (box, q <= q_max, alpha' >= alpha_min, the stop) are piecewise constant in
+ * the parameters and held fixed; the clamp alpha' = min(alpha_max, alpha e) passes no gradient where
+ * it binds.  With w_j = alpha'_j T_j, g_j = G_F . f_j, S = sum_j w_j g_j, T_end = T after the last
+ * composited entry:
+ *   dL/df_j      += w_j G_F
+ *   dL/dalpha'_j  = T_j g_j - (S - sum_{k<=j} w_k g_k) / (1 - alpha'_j) + G_A T_end / (1 - alpha'_j)
+ *   dL/dalpha_j  += dL/dalpha'_j e_j (unclamped);  dL/dq_j = dL/dalpha'_j alpha_j (-e_j / 2)
+ *   dL/d(ca, cb2, cc) += dL/dq (dx^2, dx dy, dy^2);  dL/dmean2 += dL/dq (-(2 ca dx + cb2 dy), -(cb2 dx + 2 cc dy))
+ * Per-pixel terms in fp32 following the forward sequence; the sums over pixels in double.
+ */
+void tao_composite_backward(int H, int W, int C, int feat_bytes, const float* alpha, const float* mean2,
+                            const float* conic, const int32_t* rect, const void* feat, const uint32_t* ranges,
+                            const int64_t* list, const tao_params* p, const float* GF, const float* GA,
+                            double* d_mean2, double* d_conic, double* d_alpha, double* d_feat) {
+    int TX = (W + TAO_TILE - 1) / TAO_TILE, TY = (H + TAO_TILE - 1) / TAO_TILE;
+    float qmax = p->cull_sigma * p->cull_sigma;
+    int64_t maxlen = 1;
+    for (int t = 0; t < TX * TY; t++)
+        if ((int64_t)(ranges[2 * t + 1] - ranges[2 * t]) > maxlen) maxlen = ranges[2 * t + 1] - ranges[2 * t];
+    int64_t* cg = (int64_t*)malloc(sizeof(int64_t) * (size_t)maxlen);
+    float* ca_ = (float*)malloc(sizeof(float) * (size_t)maxlen * 6);   /* a', T, e, dx, dy, clamped */
+    for (int t = 0; t < TX * TY; t++) {
+        int tx = t % TX, ty = t / TX;
+        uint32_t s0 = ranges[2 * t], s1 = ranges[2 * t + 1];
+        for (int py = ty * TAO_TILE; py < ty * TAO_TILE + TAO_TILE && py < H; py++)
+            for (int px = tx * TAO_TILE; px < tx * TAO_TILE + TAO_TILE && px < W; px++) {
+                int64_t pix = (int64_t)py * W + px;
+                const float* gf = GF + pix * C;
+                /* forward (the a6 sequence): the composited entries and their T, alpha', e */
+                float T = 1.0f;
+                int64_t m = 0;
+                for (uint32_t k = s0; k < s1; k++) {
+                    int64_t g = list[k];
+                    const int32_t* r = rect + g * 4;
+                    if (px < r[0] || px > r[1] || py < r[2] || py > r[3]) continue;
+                    float dx = (float)px - mean2[g * 2 + 0];
+                    float dy = (float)py - mean2[g * 2 + 1];
+                    float q = fmaf(fmaf(conic[g * 3 + 0], dx, conic[g * 3 + 1] * dy), dx, (conic[g * 3 + 2] * dy) * dy);
+                    if (!(q <= qmax)) continue;
+                    float e = tao_exp_det(-0.5f * q);
+                    float ae = alpha[g] * e;
+                    float a = fminf(p->alpha_max, ae);
+                    if (a < p->alpha_min) continue;
+                    float Tn = T * (1.0f - a);
+                    if (Tn < p->t_eps) break;
+                    cg[m] = g;
+                    float* rec = ca_ + m * 6;
+                    rec[0] = a; rec[1] = T; rec[2] = e; rec[3] = dx; rec[4] = dy; rec[5] = ae > p->alpha_max ? 1.0f : 0.0f;
+                    m++;
+                    T = Tn;
+                }
+                float Tend = T;
+                /* S = sum w_j g_j */
+                float S = 0.0f;
+                for (int64_t j = 0; j < m; j++) {
+                    int64_t g = cg[j];
+                    float gj = 0.0f;
+                    for (int c = 0; c < C; c++) gj = fmaf(gf[c], feat_at(feat, feat_bytes, C, g, c), gj);
+                    S = fmaf(ca_[j * 6 + 0] * ca_[j * 6 + 1], gj, S);
+                }
+                float Sup = 0.0f, ga = GA[pix];
+                for (int64_t j = 0; j < m; j++) {
+                    int64_t g = cg[j];
+                    const float* rec = ca_ + j * 6;
+                    float a = rec[0], Tj = rec[1], e = rec[2], dx = rec[3], dy = rec[4];
+                    float w = a * Tj;
+                    float gj = 0.0f;
+                    for (int c = 0; c < C; c++) {
+                        float fc = feat_at(feat, feat_bytes, C, g, c);
+                        gj = fmaf(gf[c], fc, gj);
+                        d_feat[g * C + c] += (double)(w * gf[c]);
+                    }
+                    Sup = fmaf(w, gj, Sup);
+                    float oma = 1.0f - a;
+                    float dadash = Tj * gj - (S - Sup) / oma + ga * Tend / oma;
+                    if (rec[5] != 0.0f) continue;                 /* clamp binds: no gradient */
+                    d_alpha[g] += (double)(dadash * e);
+                    float dq = dadash * alpha[g] * (-0.5f * e);
+                    const float* cn = conic + g * 3;
+                    d_conic[g * 3 + 0] += (double)(dq * dx * dx);
+                    d_conic[g * 3 + 1] += (double)(dq * dx * dy);
+                    d_conic[g * 3 + 2] += (double)(dq * dy * dy);
+                    d_mean2[g * 2 + 0] += (double)(dq * -(2.0f * cn[0] * dx + cn[1] * dy));
+                    d_mean2[g * 2 + 1] += (double)(dq * -(cn[1] * dx + 2.0f * cn[2] * dy));
+                }
+            }
+    }
+    free(cg);
+    free(ca_);
+}

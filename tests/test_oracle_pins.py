@@ -619,3 +619,61 @@ def test_blend_matches_float64_model(oracle_lib):
     assert ((ws >= 1e-4) != (ws64 >= 1e-4)).mean() < 1e-3
     close = np.all(np.abs(rgb - rgb64) < 1e-4, axis=-1) & np.isclose(ws, ws64, rtol=1e-4)
     assert close[both].mean() > 0.995, close[both].mean()
+
+
+# ----------------------------------------------------- NEXT #4: compositing backward pass (R25)
+
+def test_backward_matches_finite_differences(oracle_lib):
+    """The oracle's analytic gradients of L = sum G_F . F + G_A A (R25) against central
+    finite differences of the independent float64 forward (definition64.composite2d) on a small
+    random scene, for the parameters with the largest gradients (perturbations that flip a per-pixel
+    decision are skipped: the gradient is defined with the decisions held fixed)."""
+    import oracle
+    import oracle.definition64 as d64
+    s = sg.make_random_scene(3, H=24, W=20, C=4, n_src=14)
+    s.views[0].feat = s.views[0].feat.astype(np.float32)
+    op = oracle.make_params(default_scale=s.default_scale, default_opacity=s.default_opacity)
+    g = oracle.unproject(s, op)
+    cam = s.targets[0]
+    K, R, t = sg.cam_arrays(cam)
+    pr = oracle.project(g, K, R, t, cam.H, cam.W, op)
+    ranges, lst = oracle.tile_lists(pr, g["ids"], cam.H, cam.W)
+    rng = np.random.default_rng(7)
+    GF = rng.standard_normal((cam.H, cam.W, s.C)).astype(np.float32)
+    GA = rng.standard_normal((cam.H, cam.W)).astype(np.float32)
+    grads = oracle.composite_backward(g, pr, ranges, lst, cam.H, cam.W, GF, GA, op)
+    vis = np.nonzero(pr["visible"])[0]
+    order = vis[np.lexsort((g["ids"][vis], pr["dkey"][vis]))]
+    mean = pr["mean2"].astype(np.float64)
+    conic = pr["conic"].astype(np.float64)
+    alpha = g["alpha"].astype(np.float64)
+    feat = g["feat"].astype(np.float64)
+    rect = pr["rect"]
+
+    def loss(mean_, conic_, alpha_, feat_):
+        F, A, used = d64.composite2d(mean_, conic_, alpha_, feat_, rect, order, cam.H, cam.W)
+        return float(np.sum(F * GF) + np.sum(A * GA)), used
+
+    _, used0 = loss(mean, conic, alpha, feat)
+    checked = 0
+    for name, arr in (("mean2", mean), ("conic", conic), ("alpha", alpha), ("feat", feat)):
+        an = grads[name]
+        flat = np.argsort(-np.abs(an).reshape(-1))[:6]
+        for fi in flat:
+            idx = np.unravel_index(fi, an.shape)
+            eps = 1e-4 * max(1.0, abs(arr[idx]))
+            vals = []
+            flipped = False
+            for sgn in (1, -1):
+                pert = [mean.copy(), conic.copy(), alpha.copy(), feat.copy()]
+                k = ("mean2", "conic", "alpha", "feat").index(name)
+                pert[k][idx] += sgn * eps
+                L, used = loss(*pert)
+                flipped |= used != used0
+                vals.append(L)
+            if flipped:
+                continue
+            fd = (vals[0] - vals[1]) / (2 * eps)
+            assert abs(fd - an[idx]) <= 2e-3 * max(1.0, abs(fd)), (name, idx, fd, an[idx])
+            checked += 1
+    assert checked >= 16, checked

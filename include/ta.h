@@ -198,6 +198,24 @@ ta_status ta_blend(ta_context* ctx, const ta_source_view* views, int32_t V, cons
                    float* wsum_out, void* stream);
 
 /*
+ * backward pass of the compositing step (the
+ * differentiable rasterizer of [kerbl20233d]; reading R25).  Gradients of
+ * L = sum_p grad_F(p) . F(p) + grad_A(p) A(p) with respect to each Gaussian's 2D splat parameters,
+ * with the per-pixel decisions (box, q <= cull_sigma^2, alpha' >= alpha_min, the stop) held fixed and
+ * no gradient through a binding alpha clamp.  Must follow the ta_rasterize of the same Gaussian set,
+ * n, camera, size and params on the same context (it reuses that call's splat records and tile lists).
+ *   grad_F  device float [H][W][C], grad_A device float [H][W]   (inputs)
+ *   d_mean2 [n][2]   d/d(pixel centre x, y)
+ *   d_conic [n][3]   d/d(ca, cb2, cc) of q = ca dx^2 + cb2 dx dy + cc dy^2 (the record's conic)
+ *   d_alpha [n]      d/d(opacity)      d_feat [n][C]  d/d(feature row)       (device float, overwritten)
+ * Sums over pixels use fp32 atomics (order not fixed).  Errors: TA_ERR_INVALID_ARG for NULL pointers
+ * or no matching forward call.
+ */
+ta_status ta_rasterize_backward(ta_context* ctx, const ta_gaussians* g, int64_t n, int32_t H, int32_t W,
+                                const ta_raster_params* params, const float* grad_F, const float* grad_A,
+                                float* d_mean2, float* d_conic, float* d_alpha, float* d_feat, void* stream);
+
+/*
  * Introspection of the LAST ta_rasterize call on this context (device pointers into context
  * scratch, valid until the next call; read them on the same stream after it completes).
  *   records     [n][8] 32-bit words per Gaussian (array order): mean_x, mean_y, conic a, conic 2b,

@@ -69,7 +69,7 @@ class Profile(C.Structure):
 
 
 EXPORTS = ("ta_profile_enable", "ta_profile_read", "ta_default_params", "ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject",
-           "ta_zbuffer", "ta_blend", "ta_default_blend_params",
+           "ta_zbuffer", "ta_blend", "ta_default_blend_params", "ta_rasterize_backward",
            "ta_rasterize", "ta_debug_last", "ta_check_overflow", "ta_launch_count", "ta_status_string",
            "ta_last_error", "ta_build_info")
 
@@ -97,6 +97,8 @@ def lib(build_if_stale: bool = False):
                                C.POINTER(RasterParams), P, P, P]
     L.ta_debug_last.argtypes = [P, C.POINTER(DebugView), P]
     L.ta_default_blend_params.argtypes = [C.POINTER(BlendParams)]
+    L.ta_rasterize_backward.argtypes = [P, C.POINTER(Gaussians), i64, i32, i32, C.POINTER(RasterParams), P, P, P, P, P,
+                                        P, P]
     L.ta_blend.argtypes = [P, C.POINTER(SourceView), i32, C.POINTER(P), C.POINTER(RasterParams), C.POINTER(BlendParams),
                            C.POINTER(Intrinsics), C.POINTER(Extrinsics), i32, i32, P, P, P, P]
     L.ta_zbuffer.argtypes = [P, C.POINTER(SourceView), i32, C.POINTER(RasterParams), C.POINTER(Intrinsics),
@@ -111,7 +113,7 @@ def lib(build_if_stale: bool = False):
     L.ta_last_error.argtypes = [P]
     L.ta_last_error.restype = C.c_char_p
     L.ta_build_info.restype = C.c_char_p
-    for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize", "ta_zbuffer", "ta_blend",
+    for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize", "ta_zbuffer", "ta_blend", "ta_rasterize_backward",
                  "ta_debug_last", "ta_check_overflow", "ta_profile_enable", "ta_profile_read"):
         getattr(L, name).restype = i32
     _lib = L
@@ -202,6 +204,14 @@ class Context:
         cp = (C.c_void_p * len(colors))(*[c.data_ptr() for c in colors])
         self._check(lib().ta_blend(self._h, arr, len(views), cp, C.byref(params), C.byref(bp), C.byref(K), C.byref(RT),
                                    int(H), int(W), _ptr(z_fused), _ptr(rgb_out), _ptr(wsum_out), _stream(stream)))
+
+    def rasterize_backward(self, g: "GaussianBuffers", n, H, W, params: RasterParams, grad_F, grad_A, d_mean2, d_conic,
+                           d_alpha, d_feat, stream=None):
+        """NEXT #4 (include/ta.h ta_rasterize_backward): after ta_rasterize of the same inputs."""
+        gs = g.struct()
+        self._check(lib().ta_rasterize_backward(self._h, C.byref(gs), int(n), int(H), int(W), C.byref(params),
+                                                _ptr(grad_F), _ptr(grad_A), _ptr(d_mean2), _ptr(d_conic),
+                                                _ptr(d_alpha), _ptr(d_feat), _stream(stream)))
 
     def rasterize(self, g: "GaussianBuffers", n, K: Intrinsics, RT: Extrinsics, H, W, params: RasterParams,
                   feat_out, alpha_out, stream=None):

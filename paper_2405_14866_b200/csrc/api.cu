@@ -662,6 +662,34 @@ ta_status ta_blend(ta_context* c, const ta_source_view* views, int32_t V, const 
     return TA_OK;
 }
 
+ta_status ta_rasterize_backward(ta_context* c, const ta_gaussians* g, int64_t n, int32_t H, int32_t W,
+                                const ta_raster_params* p, const float* grad_F, const float* grad_A, float* d_mean2,
+                                float* d_conic, float* d_alpha, float* d_feat, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!g || !p || !grad_F || !grad_A || !d_mean2 || !d_conic || !d_alpha || !d_feat)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_rasterize_backward: NULL argument");
+    if (!c->have_last || c->last_H != H || c->last_W != W)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_rasterize_backward needs the matching ta_rasterize on this context first");
+    if (!supported_C(g->C)) return fail(c, TA_ERR_UNSUPPORTED, "C = %d not in {8,16,32,64}", g->C);
+    if (n < -1 || (n == -1 && !g->n_dev) || n > g->capacity) return fail(c, TA_ERR_INVALID_ARG, "bad n");
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t cap = n >= 0 ? n : g->capacity;
+    RasterConsts rc;
+    rc.dilation = p->dilation; rc.alpha_max = p->alpha_max; rc.alpha_min = p->alpha_min; rc.t_eps = p->t_eps;
+    rc.cull_sigma = p->cull_sigma; rc.z_near = p->z_near;
+    rc.q_max = p->cull_sigma * p->cull_sigma;
+    (void)cap;   // the outputs hold the call's n Gaussians: zeroed on the device from its count
+    const CompositeGeom& cg = c->last_cg;
+    cudaError_t e = launch_composite_bwd(g->C, g->feat_dtype == TA_F16 ? 2 : 4, cg.TX * cg.TY, (const uint4*)c->rec.p,
+                                         g->feat, (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p, cg, rc,
+                                         (const CallState*)c->cs.p, (uint64_t)(c->tlist.bytes / 4), grad_F, grad_A,
+                                         d_mean2, d_conic, d_alpha, d_feat, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "backward launch");
+    c->launches += 2;   // k_bwd_zero + k_composite_bwd
+    return TA_OK;
+}
+
 ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     if (!c || !out) return TA_ERR_INVALID_ARG;
     if (!c->have_last) return fail(c, TA_ERR_INVALID_ARG, "no rasterize call yet");

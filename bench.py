@@ -391,7 +391,7 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         kname = {"project": "k_project", "bin_count": "k_bin_count", "bin_place": "k_bin_place",
-                 "composite": "k_composite_tc", "sort": "k_sort_scatter"}.get(dom)
+                 "composite": "k_composite_tc", "sort": "k_sort_pass"}.get(dom)
         if kname in tj:
             traffic = tj[kname]["dram_bytes"]
             r["traffic_source"] = "profiles/traffic.json <- " + tj[kname]["source"] + " (ncu --set full, one launch)"

@@ -50,8 +50,8 @@ typedef enum {
     TA_ERR_UNSUPPORTED = 2,    /* C not in {8, 16, 32, 64}, unknown dtype, > TA_MAX_VIEWS views */
     TA_ERR_CUDA = 3,           /* a CUDA runtime error (message in ta_last_error) */
     TA_ERR_OUT_OF_MEMORY = 4,  /* scratch growth failed */
-    TA_ERR_CAPACITY = 5        /* output Gaussian capacity < sum of view pixels, or > 2^32-1 tile entries,
-                                  or (TA_FLAG_ASYNC) reserved entry capacity exceeded */
+    TA_ERR_CAPACITY = 5        /* output Gaussian capacity < sum of view pixels, > 2^28 Gaussians rasterized,
+                                  > 2^32-1 tile entries, or (TA_FLAG_ASYNC) reserved entry capacity exceeded */
 } ta_status;
 
 typedef enum { TA_F32 = 0, TA_F16 = 1 } ta_dtype;

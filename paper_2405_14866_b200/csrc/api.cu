@@ -24,7 +24,6 @@ struct DevBuf {
 // Scans per rasterize call: depth-sort passes 0..3 use status regions / counters 0..3, the
 // tile-offset scan uses 4.
 constexpr int kScanSlots = 6;   // + slot 5: debug tile-list scan
-constexpr size_t kTilesPerBin = (size_t)1 << (2 * (kCoarseShift - 4));   // 16 x 16 tiles per coarse bin
 
 }  // namespace
 
@@ -35,7 +34,8 @@ struct ta_context {
     std::string err;
     uint64_t launches = 0;
     DevBuf cs, status, rec, boxes, tile_order, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
-    DevBuf tlist, trng;           // per-tile lists (4 x the coarse-list capacity) and their (start, count)
+    uint32_t sort_epoch = 0;      // per-call tag of the depth-sort look-back words (sort_hist)
+    DevBuf tlist, trng;           // per-tile lists (tiles-per-bin x the coarse-list capacity) and their (start, count)
     DevBuf zkey;                  // ta_zbuffer: 64-bit z-buffer words
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
@@ -247,12 +247,16 @@ ta_status ta_context_destroy(ta_context* c) {
 
 namespace {
 
-// Coarse-binning geometry for an H x W target and up to cap Gaussians: 32 x 32-pixel bins, warps per
-// binning block (per-warp [NB] cursors + lane masks must fit in shared memory), P = rank tiles of
-// nw * 256 ranks.
+// Coarse-binning geometry for an H x W target and up to cap Gaussians: 32 x 32-pixel bins up to 1024
+// pixels on a side, 64 x 64 beyond when the Gaussian indices fit the 24 index bits of such bins' list
+// entries (keeps the bin count, and with it the per-warp shared-memory cursors of k_bin_place, at
+// ~1024 for 2048^2), warps per binning block (per-warp [NB] cursors + lane masks must fit in shared
+// memory), P = rank tiles of nw * 256 ranks.
 ta_status bin_geometry(ta_context* c, int H, int W, int64_t cap, BinGeom* bg) {
-    bg->shift = kCoarseShift;
-    const int bs = 1 << kCoarseShift;
+    bg->shift = (std::max(H, W) > 1024 && cap <= ((int64_t)1 << list_idx_bits(kMaxCoarseShift))) ? kMaxCoarseShift : 5;
+    if (cap > ((int64_t)1 << list_idx_bits(5)))
+        return fail(c, TA_ERR_CAPACITY, "more than 2^%d Gaussians", list_idx_bits(5));
+    const int bs = 1 << bg->shift;
     bg->TX = (W + bs - 1) / bs;
     bg->TY = (H + bs - 1) / bs;
     const int NB = bg->TX * bg->TY;
@@ -279,6 +283,20 @@ CompositeGeom composite_geometry(const BinGeom& bg, int H, int W) {
     return cg;
 }
 
+// Coarse list (entries x 4 B) and the per-tile lists (tiles per bin x 4 B).
+ta_status reserve_lists(ta_context* c, size_t entries, int shift) {
+    ta_status st;
+    const size_t nq = (size_t)1 << (2 * (shift - 4));
+    entries = std::max<size_t>(entries, 1);
+    if ((st = grow(c, c->list, entries * 4)) != TA_OK) return st;
+    return grow(c, c->tlist, entries * 4 * nq);
+}
+
+bool lists_reserved(const ta_context* c, size_t entries, int shift) {
+    const size_t nq = (size_t)1 << (2 * (shift - 4));
+    return c->list.bytes >= entries * 4 && c->tlist.bytes >= entries * 4 * nq;
+}
+
 ta_status reserve_gaussians(ta_context* c, int64_t cap) {
     ta_status st;
     const size_t n = (size_t)std::max<int64_t>(cap, 1);
@@ -289,7 +307,12 @@ ta_status reserve_gaussians(ta_context* c, int64_t cap) {
     if ((st = grow(c, c->vals0, n * 4)) != TA_OK) return st;
     if ((st = grow(c, c->vals1, n * 4)) != TA_OK) return st;
     const size_t parts = (n + kSortKeysPerBlock - 1) / kSortKeysPerBlock;
-    if ((st = grow(c, c->sort_hist, 256 * parts * 4 + 64)) != TA_OK) return st;
+    const size_t lb_bytes = 4 * 256 * parts * 8;       // depth-sort look-back words, 4 passes
+    if (c->sort_hist.bytes < lb_bytes) {
+        if ((st = grow(c, c->sort_hist, lb_bytes)) != TA_OK) return st;
+        if (cudaMemset(c->sort_hist.p, 0, c->sort_hist.bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+            return fail(c, TA_ERR_CUDA, "cudaMemset");
+    }
     return TA_OK;
 }
 
@@ -374,9 +397,7 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     BinGeom bg;
     if ((st = bin_geometry(c, H, W, max_gaussians, &bg)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, max_gaussians, H, W)) != TA_OK) return st;
-    if ((st = grow(c, c->list, (size_t)std::max<int64_t>(max_entries, 1) * 4)) != TA_OK) return st;
-    if ((st = grow(c, c->tlist, c->list.bytes * kTilesPerBin)) != TA_OK) return st;
-    return TA_OK;
+    return reserve_lists(c, (size_t)std::max<int64_t>(max_entries, 1), bg.shift);
 }
 
 ta_status ta_unproject(ta_context* c, const ta_source_view* views, int32_t V, const ta_raster_params* p,
@@ -430,7 +451,6 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     if (g->feat_dtype != TA_F32 && g->feat_dtype != TA_F16) return fail(c, TA_ERR_UNSUPPORTED, "unknown dtype");
     if (n < -1 || (n == -1 && !g->n_dev)) return fail(c, TA_ERR_INVALID_ARG, "n = -1 needs g->n_dev");
     if (n > g->capacity) return fail(c, TA_ERR_INVALID_ARG, "n > capacity");
-    if (g->capacity > (int64_t)kListIdxMask) return fail(c, TA_ERR_CAPACITY, "capacity > 2^28 - 1 Gaussians");
     if ((n != 0) && (!g->pos_alpha || !g->cov || !g->feat)) return fail(c, TA_ERR_INVALID_ARG, "NULL Gaussian array");
     if ((((uintptr_t)g->pos_alpha) | ((uintptr_t)g->cov) | ((uintptr_t)g->feat) | ((uintptr_t)feat_out)) & 15)
         return fail(c, TA_ERR_INVALID_ARG, "Gaussian arrays / feat_out must be 16-byte aligned");
@@ -454,14 +474,15 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const CompositeGeom cg = composite_geometry(bg, H, W);
     const int T = cg.TX * cg.TY;                       // 16 x 16 tiles
     if (async) {
-        if (c->rec.bytes < (size_t)cap * 32 || c->bin_offs.bytes < (size_t)bin_len * 4 || !c->list.p)
+        if (c->rec.bytes < (size_t)cap * 32 || c->bin_offs.bytes < (size_t)bin_len * 4 || !c->list.p ||
+            !lists_reserved(c, c->list.bytes / 4, bg.shift))
             return fail(c, TA_ERR_CAPACITY, "TA_FLAG_ASYNC needs ta_reserve() for this size first");
     }
     if ((st = reserve_gaussians(c, cap)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, cap, H, W)) != TA_OK) return st;
     if (counts && (st = grow(c, c->ncontrib, (size_t)H * W * 4)) != TA_OK) return st;
-    if (!c->list.p && (st = grow(c, c->list, (size_t)std::max<int64_t>(cap, 1) * 16)) != TA_OK) return st;
-    if (c->tlist.bytes < c->list.bytes * kTilesPerBin && (st = grow(c, c->tlist, c->list.bytes * kTilesPerBin)) != TA_OK)
+    if ((st = reserve_lists(c, c->list.p ? c->list.bytes / 4 : (size_t)std::max<int64_t>(cap, 1) * 4, bg.shift)) !=
+        TA_OK)
         return st;
 
     TargetCam cam;
@@ -482,7 +503,9 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const int n_status = (int)(region * kScanSlots);
     uint32_t* k0 = (uint32_t*)c->keys0.p; uint32_t* k1 = (uint32_t*)c->keys1.p;
     uint32_t* v0 = (uint32_t*)c->vals0.p; uint32_t* v1 = (uint32_t*)c->vals1.p;
-    uint32_t* hist = (uint32_t*)c->sort_hist.p;
+    unsigned long long* sort_lb = (unsigned long long*)c->sort_hist.p;
+    if (++c->sort_epoch == 0) c->sort_epoch = 1;     // 0 would match zeroed look-back words
+    const uint32_t epoch = c->sort_epoch;
     uint32_t* offs = (uint32_t*)c->bin_offs.p;
     uint4* rec = (uint4*)c->rec.p;
 
@@ -502,14 +525,12 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const uint32_t parts_max = (uint32_t)((cap + kSortKeysPerBlock - 1) / kSortKeysPerBlock);
     const uint32_t sort_blocks = parts_max;
     if (sort_blocks > 0) {
+        k_sort_digits<<<(unsigned)((cap + 2047) / 2048), 256, 0, s>>>(k0, cs);
+        TA_LAUNCHED(c);
         for (int pass = 0; pass < 4; pass++) {
-            k_sort_hist<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, pass, cs, hist);
-            TA_LAUNCHED(c);
-            launch_scan(hist, &cs->sort_len, 256 * parts_max, status + (size_t)pass * region, &cs->scan_counter[pass],
-                        &cs->sort_total, s);
-            TA_LAUNCHED(c);
-            k_sort_scatter<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs, hist, rec,
-                                                                   (uint2*)c->boxes.p);
+            k_sort_pass<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs,
+                                                                sort_lb + (size_t)pass * 256 * parts_max, epoch, rec,
+                                                                (uint2*)c->boxes.p);
             TA_LAUNCHED(c);
         }
     }
@@ -533,9 +554,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
         TA_CUDA(c, cudaStreamSynchronize(s));
         const uint64_t Kh = c->pinned[0];
         if (Kh > 0xffffffffull) return fail(c, TA_ERR_CAPACITY, "%llu tile entries exceed 2^32-1", (unsigned long long)Kh);
-        if (Kh * 4 > c->list.bytes && (st = grow(c, c->list, (size_t)(Kh + Kh / 8 + 1024) * 4)) != TA_OK) return st;
-        if (c->tlist.bytes < c->list.bytes * kTilesPerBin &&
-            (st = grow(c, c->tlist, c->list.bytes * kTilesPerBin)) != TA_OK)
+        if (!lists_reserved(c, (size_t)Kh, bg.shift) &&
+            (st = reserve_lists(c, std::max<size_t>(c->list.bytes / 4, (size_t)(Kh + Kh / 8 + 1024)), bg.shift)) != TA_OK)
             return st;
     }
     tm.end();
@@ -543,7 +563,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     k_bin_place<<<bg.P, bg.nw * 32, smem_place, s>>>((const uint2*)c->boxes.p, v0, v1, cs, bg, offs, (uint32_t*)c->list.p,
                                                      (uint64_t)(c->list.bytes / 4));
     TA_LAUNCHED(c);
-    launch_tile_split(rec, (const uint32_t*)c->list.p, offs, cg, cs, (uint64_t)(c->list.bytes / 4), (uint32_t*)c->tlist.p,
+    launch_tile_split((const uint32_t*)c->list.p, offs, cg, cs, (uint64_t)(c->list.bytes / 4), (uint32_t*)c->tlist.p,
                       (uint64_t)(c->tlist.bytes / 4), (uint2*)c->trng.p, s);
     TA_LAUNCHED(c);
     tm.end();

@@ -12,12 +12,13 @@
 namespace ta {
 
 constexpr int kTile = 16;
-constexpr int kCoarseShift = 5;        // coarse bins are 32 x 32 pixels (2 x 2 tiles)
-// coarse-list entries: Gaussian array index in the low kListIdxBits, the 4-bit mask of the bin's
-// 2 x 2 tiles covered by the Gaussian's pixel box above it
-constexpr int kListIdxBits = 28;
-constexpr uint32_t kListIdxMask = (1u << kListIdxBits) - 1u;
-static_assert(kCoarseShift == 5, "coarse-list tile masks assume 2 x 2 tiles per coarse bin");
+// Coarse bins are 2^shift-pixel squares of 2^sb x 2^sb tiles (sb = shift - 4): 32 x 32 pixels for
+// targets up to 1024 pixels on a side, 64 x 64 beyond (api.cu bin_geometry), so the bin count stays
+// ~1024.  A coarse-list entry is the Gaussian's array index in the low 32 - 4 sb bits and, above it,
+// the bin's tiles its pixel box covers: for sb = 1 the 4-bit mask of the 2 x 2 tiles (bit qy*2+qx),
+// for sb = 2 the bin-local tile rectangle x0 | x1 << 2 | y0 << 4 | y1 << 6.
+constexpr int kMaxCoarseShift = 6;
+__host__ __device__ constexpr int list_idx_bits(int shift) { return 32 - 4 * (shift - 4); }
 constexpr uint32_t kCulledKey = 0xffffffffu;
 constexpr uint32_t kEmptyRect = 1u;     // x0 = 1, x1 = 0  -> empty box
 
@@ -98,6 +99,7 @@ struct CallState {
     uint32_t overflow;             // sticky: entries exceeded the list capacity (not reset by k_init)
     uint32_t scan_counter[8];      // tile counters of the look-back scans (one per scan)
     unsigned long long work[8];    // compositor work counters (TA_FLAG_DEBUG_COUNTS only, reset by k_init)
+    uint32_t digit_hist[4][256];   // depth sort: global digit histogram of each pass (k_sort_digits)
 };
 
 constexpr int kSortWarps = 8;                                  // warps per block in the sort kernels

@@ -377,20 +377,19 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
 // Per-tile lists from the coarse (2^shift-pixel) bin lists, in list order: the (tile, depth, id)
 // order of SURVEY a3-a5 (an entry belongs to tile t iff its pixel box covers t).  One 1024-thread
 // block per coarse bin; its list is cut into 32 contiguous segments, one per warp: pass 1 counts each
-// segment's entries per tile (the 2^sb x 2^sb tiles of the bin), an exclusive scan over the warps
-// gives every (segment, tile) write offset, pass 2 writes.  Tile q of bin b owns
-// tlist[2^(2 sb) cstart_b + q len_b, + len_b) (a tile list is a subsequence of the bin list);
-// trng[tile] = (start, count).
-constexpr int kSplitMaxTiles = 4;                  // tiles per coarse bin supported (sb <= 1)
-__global__ void __launch_bounds__(1024) k_tile_split(const uint4* __restrict__ rec, const uint32_t* __restrict__ clist,
+// segment's entries per tile (the NQ = 2^sb x 2^sb tiles of the bin, from the tile rectangle
+// k_bin_place stored above the entry's index), an exclusive scan over the warps gives every (segment, tile) write
+// offset, pass 2 writes.  Tile q of bin b owns tlist[NQ cstart_b + q len_b, + len_b) (a tile list
+// is a subsequence of the bin list); trng[tile] = (start, count).
+template <int NQ>
+__global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict__ clist,
                                                      const uint32_t* __restrict__ coffs, CompositeGeom cg,
                                                      const CallState* __restrict__ cs, uint64_t clist_cap,
                                                      uint32_t* __restrict__ tlist, uint64_t tlist_cap,
                                                      uint2* __restrict__ trng) {
-    __shared__ uint32_t s_cnt[32][kSplitMaxTiles];
+    constexpr int SB = NQ == 4 ? 1 : 2, TPB = 1 << SB, IB = list_idx_bits(SB + 4);
+    __shared__ uint32_t s_cnt[32][NQ];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    const int sb = cg.shift - 4;
-    const int nq = 1 << (2 * sb);
     const int bin = blockIdx.x;
     const int bxi = bin % cg.BX, byi = bin / cg.BX;
     const uint32_t P = cs->bin_P;                     // bin-major [NB x P] run starts (this call's P)
@@ -401,31 +400,35 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint4* __restrict__ r
     const uint32_t segl = (((len + 31u) / 32u) + 31u) & ~31u;          // entries per warp (multiple of 32)
     const uint32_t s0 = cstart + warp * segl, s1 = min(cend, s0 + segl);
     const uint32_t lt = lanemask_lt();
-    int txq[kSplitMaxTiles], tyq[kSplitMaxTiles];
-#pragma unroll
-    for (int q = 0; q < kSplitMaxTiles; q++) {
-        txq[q] = (bxi << sb) + (q & ((1 << sb) - 1));
-        tyq[q] = (byi << sb) + (q >> sb);
-    }
+    const uint64_t tbase = (uint64_t)cstart * NQ;
     constexpr int kU = 4;                                           // chunks of 32 entries in flight
-    // the tiles an entry covers come with it (k_bin_place, bits kListIdxBits..+3)
-    auto walk = [&](bool write, uint32_t (&run)[kSplitMaxTiles]) {
+    auto walk = [&](bool write, uint32_t (&run)[NQ]) {
         for (uint32_t pos = s0; pos < s1; pos += 32 * kU) {
             uint32_t ent[kU];
 #pragma unroll
             for (int u = 0; u < kU; u++) {
                 const uint32_t e = pos + 32 * u + lane;
-                ent[u] = e < s1 ? clist[e] : 0u;
+                ent[u] = e < s1 ? clist[e] : 0u;          // 0: no tiles (padding)
             }
 #pragma unroll
             for (int u = 0; u < kU; u++) {
-                const uint32_t idx = ent[u] & kListIdxMask, tm = ent[u] >> kListIdxBits;
+                const uint32_t idx = ent[u] & ((1u << IB) - 1u), r = ent[u] >> IB;
+                uint32_t tm = r;                                   // sb = 1: the tile mask
+                if (SB == 2) {                                     // sb = 2: tile rectangle -> 16-bit mask
+                    const uint32_t x0 = r & 3u, x1 = (r >> 2) & 3u, y0 = (r >> 4) & 3u, y1 = r >> 6;
+                    const uint32_t mx = (2u << x1) - (1u << x0);
+                    tm = 0u;
 #pragma unroll
-                for (int q = 0; q < kSplitMaxTiles; q++) {
+                    for (int qy = 0; qy < TPB; qy++)
+                        if ((uint32_t)qy >= y0 && (uint32_t)qy <= y1) tm |= mx << (qy * TPB);
+                    if (pos + 32 * u + lane >= s1) tm = 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
                     const bool ok = (tm >> q) & 1u;
                     const uint32_t bal = __ballot_sync(0xffffffffu, ok);
                     if (write && ok) {
-                        const uint64_t p = ((uint64_t)cstart << (2 * sb)) + (uint64_t)q * len + run[q] + __popc(bal & lt);
+                        const uint64_t p = tbase + (uint64_t)q * len + run[q] + __popc(bal & lt);
                         if (p < tlist_cap) tlist[p] = idx;
                     }
                     run[q] += __popc(bal);
@@ -433,14 +436,17 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint4* __restrict__ r
             }
         }
     };
-    uint32_t run[kSplitMaxTiles] = {0u, 0u, 0u, 0u};
+    uint32_t run[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; q++) run[q] = 0u;
     walk(false, run);
-    if (lane < kSplitMaxTiles) s_cnt[warp][lane] = run[0] * (lane == 0) + run[1] * (lane == 1) + run[2] * (lane == 2) +
-                                                   run[3] * (lane == 3);
+#pragma unroll
+    for (int q = 0; q < NQ; q++)
+        if (lane == (uint32_t)q) s_cnt[warp][q] = run[q];
     __syncthreads();
     if (warp == 0) {                                              // exclusive scan over the 32 segments, per tile
 #pragma unroll
-        for (int q = 0; q < kSplitMaxTiles; q++) {
+        for (int q = 0; q < NQ; q++) {
             const uint32_t v = s_cnt[lane][q];
             uint32_t x = v;
 #pragma unroll
@@ -449,17 +455,16 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint4* __restrict__ r
                 if (lane >= (uint32_t)o) x += y;
             }
             s_cnt[lane][q] = x - v;
-            if (lane == 31 && q < nq) {
-                const int tx = txq[q], ty = tyq[q];
+            if (lane == 31) {
+                const int tx = (bxi << SB) + (q & ((1 << SB) - 1)), ty = (byi << SB) + (q >> SB);
                 if (tx < cg.TX && ty < cg.TY)
-                    trng[ty * cg.TX + tx] = make_uint2((uint32_t)min(((uint64_t)cstart << (2 * sb)) + (uint64_t)q * len,
-                                                                     (uint64_t)0xffffffffu), x);
+                    trng[ty * cg.TX + tx] = make_uint2((uint32_t)min(tbase + (uint64_t)q * len, (uint64_t)0xffffffffu), x);
             }
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < kSplitMaxTiles; q++) run[q] = s_cnt[warp][q];
+    for (int q = 0; q < NQ; q++) run[q] = s_cnt[warp][q];
     walk(true, run);
 }
 
@@ -1088,11 +1093,15 @@ void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, Composite
     }
 }
 
-void launch_tile_split(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg, const CallState* cs,
-                       uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng, cudaStream_t st) {
+void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
+                       const CallState* cs, uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng,
+                       cudaStream_t st) {
     const int sb = cg.shift - 4;
     const int NB = cg.BX * ((cg.TY + (1 << sb) - 1) >> sb);
-    k_tile_split<<<NB, 1024, 0, st>>>(rec, clist, coffs, cg, cs, clist_cap, tlist, tlist_cap, trng);
+    if (sb == 1)
+        k_tile_split<4><<<NB, 1024, 0, st>>>(clist, coffs, cg, cs, clist_cap, tlist, tlist_cap, trng);
+    else
+        k_tile_split<16><<<NB, 1024, 0, st>>>(clist, coffs, cg, cs, clist_cap, tlist, tlist_cap, trng);
 }
 
 }  // namespace ta

@@ -58,10 +58,9 @@ __global__ void k_init(CallState* cs, unsigned long long* status, int n_status, 
                        const int64_t* n_dev, uint32_t bin_ranks, uint32_t nbins);
 __global__ void k_project(const float4* pos_alpha, const float4* cov, TargetCam cam, RasterConsts rc,
                           CallState* cs, uint4* rec, uint32_t* key0, uint32_t* val0);
-__global__ void k_sort_hist(const uint32_t* keys_a, const uint32_t* keys_b, int pass, const CallState* cs,
-                            uint32_t* hist);
-__global__ void k_sort_scatter(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int pass,
-                               const CallState* cs, const uint32_t* offs, const uint4* rec, uint2* boxes);
+__global__ void k_sort_digits(const uint32_t* keys, CallState* cs);
+__global__ void k_sort_pass(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int pass,
+                            CallState* cs, unsigned long long* lb, uint32_t epoch, const uint4* rec, uint2* boxes);
 __global__ void k_gather_boxes(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, const CallState* cs,
                                uint2* boxes);
 __global__ void k_bin_count(const uint2* boxes, const CallState* cs, BinGeom bg, uint32_t* counts);
@@ -83,8 +82,9 @@ struct CompositeGeom {
     uint32_t P;           // coarse-binning partitions (columns of the bin-major offset matrix)
 };
 // per-tile lists (tile, depth, id) from the coarse bin lists: tlist + trng[tile] = (start, count)
-void launch_tile_split(const uint4* rec, const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg, const CallState* cs,
-                       uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng, cudaStream_t st);
+void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
+                       const CallState* cs, uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng,
+                       cudaStream_t st);
 cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
                              const uint32_t* tlist, const uint2* trng, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,

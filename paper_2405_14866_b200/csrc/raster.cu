@@ -4,9 +4,9 @@
 //   k_init          reset the per-call device scalars and look-back status words
 //   k_project       EWA projection of every Gaussian, 32-byte splat record,
 //                   depth key scattered BY ID so the depth sort sees id order (tie-break by id)
-//   k_sort_hist / k_scan / k_sort_scatter   x passes: stable LSD radix sort of the depth keys over
-//                   only the bits that vary among visible Gaussians (8-bit digits, per-warp
-//                   partitions, warp-synchronous stable ranking with ballot multisplit)
+//   k_sort_digits + k_sort_pass x passes: stable LSD radix sort of the depth keys over only the
+//                   bits that vary among visible Gaussians (8-bit digits, one-sweep: global digit
+//                   histograms up front, one kernel per pass with decoupled look-back)
 //   k_bin_count     per-tile (consecutive depth ranks) counts of the coarse (32 x 32-pixel) bins
 //   k_scan          flat exclusive scan of the bin-major [bins x tiles] counts -> run starts, K
 //   k_bin_place     per tile: per-warp cursors, then every (Gaussian, bin) entry appended in rank
@@ -38,6 +38,8 @@ __global__ void k_init(CallState* __restrict__ cs, unsigned long long* __restric
         for (int k = 0; k < 8; k++) cs->scan_counter[k] = 0u;
         for (int k = 0; k < 8; k++) cs->work[k] = 0ull;
     }
+    if (blockIdx.x == 0)
+        for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&cs->digit_hist[0][0])[k] = 0u;
 }
 
 // ----------------------------------------------------------------------------- k_project
@@ -135,62 +137,89 @@ __global__ void __launch_bounds__(256) k_project(const float4* __restrict__ pos_
 }
 
 // ----------------------------------------------------------------------------- depth sort
-// Pass `pass` sorts by 8 bits starting at sort_shift(); keys/vals ping-pong a -> b -> a ...
-// Inactive passes (beyond the varying bits) return immediately.  A block owns kSortKeysPerBlock
-// consecutive keys, each warp kSortKeysPerWarp of them in order; warps rank their keys stably
-// (ballot multisplit per 32-key chunk, per-warp digit counters), the block combines warps in order.
-__global__ void __launch_bounds__(kSortWarps * 32) k_sort_hist(const uint32_t* __restrict__ keys_a,
-                                                               const uint32_t* __restrict__ keys_b, int pass,
-                                                               const CallState* __restrict__ cs,
-                                                               uint32_t* __restrict__ hist) {
-    __shared__ uint32_t s_cnt[kSortWarps][256];
-    if (pass >= sort_passes(cs)) return;
-    const uint32_t parts = cs->sort_parts;
-    if (blockIdx.x >= parts) return;
-    const uint32_t* src = (pass & 1) ? keys_b : keys_a;
-    const int shift = sort_shift(cs, pass);
+// Stable LSD radix sort of the depth keys (id order in, (depth, id) order out) over only the bits
+// that vary among visible keys, 8-bit digits, one-sweep style:
+//   k_sort_digits   one read of the keys: the global digit histogram of every pass (cs->digit_hist)
+//   k_sort_pass     per pass, one kernel: a block takes the next partition of kSortKeysPerBlock keys
+//                   (ticket order), ranks them stably (per-warp ballot multisplit, warps in order),
+//                   publishes its per-digit counts and looks back over the earlier partitions for
+//                   its per-digit global offsets (decoupled look-back, one thread per digit), then
+//                   reorders the keys in shared memory by digit so the global writes are runs.
+// Inactive passes (beyond the varying bits) return immediately.
+__global__ void __launch_bounds__(256) k_sort_digits(const uint32_t* __restrict__ keys, CallState* __restrict__ cs) {
+    __shared__ uint32_t s_h[4][256];
+    const int npass = sort_passes(cs);
     const uint32_t n = cs->n;
-    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    for (int k = threadIdx.x; k < kSortWarps * 256; k += blockDim.x) (&s_cnt[0][0])[k] = 0u;
+    if (npass == 0 || blockIdx.x * blockDim.x * 8u >= n) return;
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&s_h[0][0])[k] = 0u;
     __syncthreads();
-    uint32_t* cnt = s_cnt[warp];
-    constexpr int kChunks = kSortKeysPerWarp / 32;
-    const uint32_t b = blockIdx.x * kSortKeysPerBlock + warp * kSortKeysPerWarp;
-    uint32_t key[kChunks];
+    const int shift0 = sort_shift(cs, 0);
+    const uint32_t lane = lane_id();
+    const uint32_t base = blockIdx.x * blockDim.x * 8u + (threadIdx.x >> 5) * 256u;
+    uint32_t key[8];
 #pragma unroll
-    for (int k = 0; k < kChunks; k++) {          // all loads in flight before any ranking
-        const uint32_t idx = b + k * 32 + lane;
-        key[k] = idx < n ? src[idx] : 0u;
+    for (int k = 0; k < 8; k++) {
+        const uint32_t i = base + 32u * k + lane;
+        key[k] = i < n ? keys[i] : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < kChunks; k++) {
-        const bool ok = b + k * 32 + lane < n;
-        const uint32_t d = ok ? (key[k] >> shift) & 255u : 0u;
-        const uint32_t peers = peers8(d, __ballot_sync(0xffffffffu, ok));
-        if (ok && lane == (uint32_t)(__ffs(peers) - 1)) cnt[d] += __popc(peers);
-        __syncwarp();
+    for (int k = 0; k < 8; k++) {
+        const bool ok = base + 32u * k + lane < n;
+        const uint32_t valid = __ballot_sync(0xffffffffu, ok);
+        if (valid == 0u) break;
+        for (int p = 0; p < npass; p++) {
+            const uint32_t d = (key[k] >> (shift0 + 8 * p)) & 255u;
+            const uint32_t peers = peers8(d, valid);
+            if (ok && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_h[p][d], (uint32_t)__popc(peers));
+        }
     }
     __syncthreads();
-    const uint32_t d = threadIdx.x;
-    uint32_t sum = 0;
-#pragma unroll
-    for (int w = 0; w < kSortWarps; w++) sum += s_cnt[w][d];
-    hist[(size_t)d * parts + blockIdx.x] = sum;
+    for (int k = threadIdx.x; k < npass * 256; k += blockDim.x) {
+        const uint32_t v = (&s_h[0][0])[k];
+        if (v) atomicAdd(&cs->digit_hist[k >> 8][k & 255], v);
+    }
 }
 
+// Exclusive scan of v over the 256 threads of the block (one value per thread); s: 8 words.
+__device__ __forceinline__ uint32_t block256_excl(uint32_t v, uint32_t* s) {
+    const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s[w] = x;
+    __syncthreads();
+    uint32_t pre = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) pre += (uint32_t)k < w ? s[k] : 0u;
+    __syncthreads();
+    return pre + x - v;
+}
+
+// Look-back words: epoch << 32 | flag << 30 | count (flag 1: this partition's count, 2: inclusive
+// prefix over partitions 0..p).  The epoch (per call) makes stale words of earlier calls invisible.
+constexpr uint64_t kLbAgg = 1ull << 30, kLbInc = 2ull << 30;
+constexpr uint32_t kLbMask = (1u << 30) - 1u;
+
 // The last pass also writes the pixel box of every rank (boxes[rank]) for the binning kernels.
-__global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __restrict__ keys_a, uint32_t* __restrict__ keys_b,
-                                                                  uint32_t* __restrict__ vals_a, uint32_t* __restrict__ vals_b,
-                                                                  int pass, const CallState* __restrict__ cs,
-                                                                  const uint32_t* __restrict__ offs,
-                                                                  const uint4* __restrict__ rec, uint2* __restrict__ boxes) {
+__global__ void __launch_bounds__(kSortWarps * 32) k_sort_pass(uint32_t* __restrict__ keys_a, uint32_t* __restrict__ keys_b,
+                                                               uint32_t* __restrict__ vals_a, uint32_t* __restrict__ vals_b,
+                                                               int pass, CallState* __restrict__ cs,
+                                                               unsigned long long* __restrict__ lb, uint32_t epoch,
+                                                               const uint4* __restrict__ rec, uint2* __restrict__ boxes) {
+    static_assert(kSortWarps * 32 == 256, "one thread per digit");
     constexpr int kChunks = kSortKeysPerWarp / 32;
-    __shared__ uint32_t s_off[kSortWarps][256];
+    __shared__ uint32_t s_off[kSortWarps][256];        // per-warp digit counts -> per-warp offsets
+    __shared__ uint32_t s_loc[256], s_gbase[256], s_scan[8], s_part;
+    __shared__ uint32_t s_key[kSortKeysPerBlock], s_val[kSortKeysPerBlock];
     const int npass = sort_passes(cs);
     if (pass >= npass) return;
     const bool last = pass == npass - 1;
     const uint32_t parts = cs->sort_parts;
     if (blockIdx.x >= parts) return;
+    if (threadIdx.x == 0) s_part = atomicAdd(&cs->scan_counter[pass], 1u);
     const uint32_t* sk = (pass & 1) ? keys_b : keys_a;
     const uint32_t* sv = (pass & 1) ? vals_b : vals_a;
     uint32_t* dk = (pass & 1) ? keys_a : keys_b;
@@ -200,9 +229,11 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __re
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     for (int k = threadIdx.x; k < kSortWarps * 256; k += blockDim.x) (&s_off[0][0])[k] = 0u;
     __syncthreads();
+    const uint32_t part = s_part;
     uint32_t* cnt = s_off[warp];
     const uint32_t lt = lanemask_lt();
-    const uint32_t b = blockIdx.x * kSortKeysPerBlock + warp * kSortKeysPerWarp;
+    const uint32_t b0 = part * kSortKeysPerBlock;
+    const uint32_t b = b0 + warp * kSortKeysPerWarp;
     uint32_t key[kChunks], val[kChunks], rank[kChunks];
 #pragma unroll
     for (int k = 0; k < kChunks; k++) {
@@ -223,27 +254,65 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_scatter(uint32_t* __re
         __syncwarp();
     }
     __syncthreads();
-    {   // per digit: warps in order after the block's global offset
-        const uint32_t d = threadIdx.x;
-        uint32_t run = offs[(size_t)d * parts + blockIdx.x];
+    const uint32_t d = threadIdx.x;                    // ---- one thread per digit from here
+    uint32_t tot = 0u;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; w++) {
-            const uint32_t c = s_off[w][d];
-            s_off[w][d] = run;
-            run += c;
+    for (int w = 0; w < kSortWarps; w++) {             // warps in order within the partition
+        const uint32_t c = s_off[w][d];
+        s_off[w][d] = tot;
+        tot += c;
+    }
+    unsigned long long* my = lb + (size_t)part * 256 + d;
+    const unsigned long long ep = (unsigned long long)epoch << 32;
+    if (part == 0) *(volatile unsigned long long*)my = ep | kLbInc | tot;
+    else *(volatile unsigned long long*)my = ep | kLbAgg | tot;
+    const uint32_t loc = block256_excl(tot, s_scan);                              // digit start in the block
+    const uint32_t gex = block256_excl(cs->digit_hist[pass][d], s_scan);          // digit start overall
+    uint32_t excl = 0u;
+    if (part > 0) {                  // decoupled look-back over partitions part-1, part-2, ... 8 at a time
+        constexpr int kWin = 8;
+        uint32_t q = part;                             // partitions q..part-1 are accounted for
+        bool done = false;
+        while (!done) {
+            unsigned long long w[kWin];
+#pragma unroll
+            for (int j = 0; j < kWin; j++)
+                w[j] = (uint32_t)j < q ? *(volatile unsigned long long*)(lb + (size_t)(q - 1 - j) * 256 + d)
+                                       : (ep | kLbInc);
+#pragma unroll
+            for (int j = 0; j < kWin; j++) {
+                if (done) break;
+                if ((w[j] >> 32) != epoch) break;      // not published yet: retry from here
+                excl += (uint32_t)w[j] & kLbMask;
+                q--;
+                if (w[j] & kLbInc) done = true;
+            }
+        }
+        *(volatile unsigned long long*)my = ep | kLbInc | (excl + tot);
+    }
+    s_loc[d] = loc;
+    s_gbase[d] = gex + excl;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kChunks; k++) {                // reorder by digit in shared memory
+        if (b + k * 32 + lane < n) {
+            const uint32_t dd = (key[k] >> shift) & 255u;
+            const uint32_t lp = s_loc[dd] + cnt[dd] + rank[k];
+            s_key[lp] = key[k];
+            s_val[lp] = val[k];
         }
     }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kChunks; k++) {
-        if (b + k * 32 + lane < n) {
-            const uint32_t pos = cnt[(key[k] >> shift) & 255u] + rank[k];
-            dk[pos] = key[k];
-            dv[pos] = val[k];
-            if (last) {
-                const uint4 q = rec[2 * val[k] + 1];
-                boxes[pos] = make_uint2(q.z, q.w);
-            }
+    const uint32_t m = n - b0 < (uint32_t)kSortKeysPerBlock ? n - b0 : (uint32_t)kSortKeysPerBlock;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {    // digit runs -> consecutive addresses
+        const uint32_t k = s_key[i], v = s_val[i];
+        const uint32_t dd = (k >> shift) & 255u;
+        const uint32_t pos = s_gbase[dd] + (i - s_loc[dd]);
+        dk[pos] = k;
+        dv[pos] = v;
+        if (last) {
+            const uint4 q = rec[2 * v + 1];
+            boxes[pos] = make_uint2(q.z, q.w);
         }
     }
 }
@@ -358,8 +427,8 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
             ok = box_bins(pb, bg.shift, &x0, &x1, &y0, &y1);
             idx = sorted[r];
         }
-        // 16 x 16 tiles covered by the pixel box: the list entry carries, above the index, which of the
-        // 2 x 2 tiles of its coarse bin the box covers (read by k_tile_split)
+        // 16 x 16 tiles covered by the pixel box: each list entry carries, above the index, the
+        // rectangle of its coarse bin's tiles the box covers (read by k_tile_split)
         const int tx0 = (int)(pb.x & 0xffff) >> 4, tx1 = (int)(pb.x >> 16) >> 4;
         const int ty0 = (int)(pb.y & 0xffff) >> 4, ty1 = (int)(pb.y >> 16) >> 4;
         const int tw = x1 - x0 + 1;
@@ -379,11 +448,18 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
         for (int i = 0, xi = 0, yi = 0, t = t0; i < maxc; i++) {
             if (i < cnt) {
                 const uint32_t pos = s_cnt[rbase + t] + __popc(s_cnt[mbase + t] & lt);
-                const int cx = 2 * (x0 + xi), cy = 2 * (y0 + yi);
-                const uint32_t mx = (uint32_t)(cx >= tx0 && cx <= tx1) | ((uint32_t)(cx + 1 >= tx0 && cx + 1 <= tx1) << 1);
-                const uint32_t my = (uint32_t)(cy >= ty0 && cy <= ty1) | ((uint32_t)(cy + 1 >= ty0 && cy + 1 <= ty1) << 1);
-                const uint32_t tm = ((my & 1u) ? mx : 0u) | ((my & 2u) ? (mx << 2) : 0u);
-                if (pos < cap32) list[pos] = idx | (tm << kListIdxBits);
+                const int sb = bg.shift - 4, qm = (1 << sb) - 1;
+                const int cx = (x0 + xi) << sb, cy = (y0 + yi) << sb;
+                uint32_t rect;
+                if (sb == 1) {                               // 2 x 2 tiles: the tile mask itself
+                    const uint32_t mx = (uint32_t)(cx >= tx0 && cx <= tx1) | ((uint32_t)(cx + 1 >= tx0 && cx + 1 <= tx1) << 1);
+                    const uint32_t my = (uint32_t)(cy >= ty0 && cy <= ty1) | ((uint32_t)(cy + 1 >= ty0 && cy + 1 <= ty1) << 1);
+                    rect = ((my & 1u) ? mx : 0u) | ((my & 2u) ? (mx << 2) : 0u);
+                } else {                                     // 4 x 4 tiles: the bin-local tile rectangle
+                    rect = (uint32_t)max(tx0 - cx, 0) | ((uint32_t)min(tx1 - cx, qm) << sb) |
+                           ((uint32_t)max(ty0 - cy, 0) << (2 * sb)) | ((uint32_t)min(ty1 - cy, qm) << (3 * sb));
+                }
+                if (pos < cap32) list[pos] = idx | (rect << list_idx_bits(bg.shift));
                 else overflow = 1u;
                 t++;
                 if (++xi == tw) { xi = 0; yi++; t += stride; }

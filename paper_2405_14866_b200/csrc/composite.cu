@@ -12,6 +12,7 @@
 // normative fp32 sequence (DESIGN.md a6) bit for bit; the C accumulators are fp32 FMAs.
 // Warps retire when all their pixels stopped (__all_sync); the CTA leaves the list as soon
 // as every pixel stopped (__syncthreads_count).
+#include <algorithm>
 #include <type_traits>
 #include "common.cuh"
 #include "internal.h"
@@ -622,369 +623,382 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     TcBuf<C>& bf = reinterpret_cast<TcBuf<C>*>(smem_raw)[warp];
 
-    const int tile = (int)order[blockIdx.x];
-    const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
-    const uint2 tr = trng[tile];                       // this tile's (depth, id)-ordered list (k_tile_split)
-    const uint32_t cstart = tr.x;
-    uint32_t cend = tr.x + tr.y;
-    if (cend > list_cap) cend = (uint32_t)list_cap;
-    const uint32_t n = cs->n;
-    const int W = cg.W, H = cg.H;
+    // Persistent warps: each warp takes the next 8 x 8 block (tile quadrant) in the heaviest-first
+    // tile order from a per-call counter until all are done, so a warp that finishes early starts
+    // new work instead of idling until its CTA's slowest warp is done.
+    uint32_t* const wq = &const_cast<CallState*>(cs)->scan_counter[6];
+    const uint32_t nblk = 4u * (uint32_t)(cg.TX * cg.TY);
+    for (;;) {
+        uint32_t blk = 0;
+        if (lane == 0) blk = atomicAdd(wq, 1u);
+        blk = __shfl_sync(0xffffffffu, blk, 0);
+        if (blk >= nblk) break;
+        const int tile = (int)order[blk >> 2];
+        const uint32_t qd = blk & 3u;                      // the 8 x 8 quadrant of the tile
+        const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
+        const uint2 tr = trng[tile];                       // this tile's (depth, id)-ordered list (k_tile_split)
+        const uint32_t cstart = tr.x;
+        uint32_t cend = tr.x + tr.y;
+        if (cend > list_cap) cend = (uint32_t)list_cap;
+        const uint32_t n = cs->n;
+        const int W = cg.W, H = cg.H;
 
-    const int bx0 = txi * kTile + 8 * (int)(warp & 1), by0 = tyi * kTile + 8 * (int)(warp >> 1);
-    const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
-    const float pxf = (float)px;
-    const float2 py2 = make_float2((float)pyA, (float)pyB);
-    const float qmax = rc.q_max, amax = rc.alpha_max, amin = rc.alpha_min, teps = rc.t_eps;
-    const float qlim = qmax * 1.015625f + 0.01f;
-    const uint32_t lt = lanemask_lt();
+        const int bx0 = txi * kTile + 8 * (int)(qd & 1), by0 = tyi * kTile + 8 * (int)(qd >> 1);
+        const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
+        const float pxf = (float)px;
+        const float2 py2 = make_float2((float)pyA, (float)pyB);
+        const float qmax = rc.q_max, amax = rc.alpha_max, amin = rc.alpha_min, teps = rc.t_eps;
+        const float qlim = qmax * 1.015625f + 0.01f;
+        const uint32_t lt = lanemask_lt();
 
-    // ldmatrix row addresses.  A (weights, stored [k][pixel p' = 2 lane + (0: A, 1: B)]): lane i
-    // addresses row k = (i & 7) + 8 (i >> 4) of matrix i >> 3, pixel chunk 2 mt + ((i >> 3) & 1).
-    const int li = (int)lane;
-    const uint32_t a_base = smem_u32(&bf.w[0][(li & 7) + 8 * (li >> 4)][0]) + (uint32_t)(((li >> 3) & 1) * 16);
-    constexpr uint32_t kLoOff = 16 * WP * 4;
-    // B (features, stored [k][channel]): lane i addresses row (i & 7) + 8 ((i >> 3) & 1), channel chunk 2 np + (i >> 4)
-    const int bk = (li & 7) + 8 * ((li >> 3) & 1);
-    const uint32_t b_base = smem_u32(&bf.f[0][0]) + (uint32_t)((li >> 4) * 16);
-    uint32_t* const wst = &bf.w[0][0][li];    // this lane's word in weight row 0 (hi)
+        // ldmatrix row addresses.  A (weights, stored [k][pixel p' = 2 lane + (0: A, 1: B)]): lane i
+        // addresses row k = (i & 7) + 8 (i >> 4) of matrix i >> 3, pixel chunk 2 mt + ((i >> 3) & 1).
+        const int li = (int)lane;
+        const uint32_t a_base = smem_u32(&bf.w[0][(li & 7) + 8 * (li >> 4)][0]) + (uint32_t)(((li >> 3) & 1) * 16);
+        constexpr uint32_t kLoOff = 16 * WP * 4;
+        // B (features, stored [k][channel]): lane i addresses row (i & 7) + 8 ((i >> 3) & 1), channel chunk 2 np + (i >> 4)
+        const int bk = (li & 7) + 8 * ((li >> 3) & 1);
+        const uint32_t b_base = smem_u32(&bf.f[0][0]) + (uint32_t)((li >> 4) * 16);
+        uint32_t* const wst = &bf.w[0][0][li];    // this lane's word in weight row 0 (hi)
 
-    float acc[4][NT][4];
-#pragma unroll
-    for (int mt = 0; mt < 4; mt++)
-#pragma unroll
-        for (int nt = 0; nt < NT; nt++)
-#pragma unroll
-            for (int e = 0; e < 4; e++) acc[mt][nt][e] = 0.0f;
-    float2 T = make_float2(1.0f, 1.0f);
-    int ncA = 0, ncB = 0;
-    // active-pixel lane bits: the lane's bit while its pixel still composites, else 0
-    uint32_t actA = (px < W && pyA < H) ? (1u << lane) : 0u;
-    uint32_t actB = (px < W && pyB < H) ? (1u << lane) : 0u;
+        float acc[4][NT][4];
+    #pragma unroll
+        for (int mt = 0; mt < 4; mt++)
+    #pragma unroll
+            for (int nt = 0; nt < NT; nt++)
+    #pragma unroll
+                for (int e = 0; e < 4; e++) acc[mt][nt][e] = 0.0f;
+        float2 T = make_float2(1.0f, 1.0f);
+        int ncA = 0, ncB = 0;
+        // active-pixel lane bits: the lane's bit while its pixel still composites, else 0
+        uint32_t actA = (px < W && pyA < H) ? (1u << lane) : 0u;
+        uint32_t actB = (px < W && pyB < H) ? (1u << lane) : 0u;
 
-    // Compacted mode (entered once, when at most 32 of the 64 pixels still composite): each such pixel
-    // moves to its own lane (original lane ol, half hs -> weight column p' = 2 ol + hs) and the packed
-    // fp32x2 arithmetic runs over pairs of entries instead of pairs of pixels, so the warp walks the
-    // rest of the list at twice the rate.  T and the decisions keep the same fp32 sequence.
-    bool modeB = false, movedA = false, movedB = false, chas = false;
-    int ol = 0, hs = 0, cpx = 0, cpy = 0, nc1 = 0;
-    float T1 = 1.0f;
-    uint32_t act1 = 0u;
+        // Compacted mode (entered once, when at most 32 of the 64 pixels still composite): each such pixel
+        // moves to its own lane (original lane ol, half hs -> weight column p' = 2 ol + hs) and the packed
+        // fp32x2 arithmetic runs over pairs of entries instead of pairs of pixels, so the warp walks the
+        // rest of the list at twice the rate.  T and the decisions keep the same fp32 sequence.
+        bool modeB = false, movedA = false, movedB = false, chas = false;
+        int ol = 0, hs = 0, cpx = 0, cpy = 0, nc1 = 0;
+        float T1 = 1.0f;
+        uint32_t act1 = 0u;
 
-    unsigned long long wk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t pos = cstart;
-    uint32_t pf_pos = 0xffffffffu, pf[2] = {0u, 0u};     // prefetched list indices of entries pf_pos + [0, 64)
-    while (pos < cend && __any_sync(0xffffffffu, (actA | actB | act1) != 0u)) {
-        // culling rectangle = bounding box of the pixels still compositing
-        int lx0, lx1, ly0, ly1;
-        if (!modeB) {
-            lx0 = (actA | actB) ? px : 0x7fffffff;
-            lx1 = (actA | actB) ? px : -1;
-            ly0 = actA ? pyA : (actB ? pyB : 0x7fffffff);
-            ly1 = actB ? pyB : (actA ? pyA : -1);
-        } else {
-            lx0 = act1 ? cpx : 0x7fffffff;
-            lx1 = act1 ? cpx : -1;
-            ly0 = act1 ? cpy : 0x7fffffff;
-            ly1 = act1 ? cpy : -1;
-        }
-        const int ax0 = __reduce_min_sync(0xffffffffu, lx0);
-        const int ax1 = __reduce_max_sync(0xffffffffu, lx1);
-        const int ay0 = __reduce_min_sync(0xffffffffu, ly0);
-        const int ay1 = __reduce_max_sync(0xffffffffu, ly1);
-        const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
-        // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip.
-        //      The list indices of the next 64 entries are loaded one round ahead (pf_pos / pf).
-        int cnt = 0;
-        while (cnt < kBuf && pos < cend) {
-            uint32_t idx[2];
-            if (pf_pos == pos) {
-                idx[0] = pf[0];
-                idx[1] = pf[1];
+        unsigned long long wk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t pos = cstart;
+        uint32_t pf_pos = 0xffffffffu, pf[2] = {0u, 0u};     // prefetched list indices of entries pf_pos + [0, 64)
+        while (pos < cend && __any_sync(0xffffffffu, (actA | actB | act1) != 0u)) {
+            // culling rectangle = bounding box of the pixels still compositing
+            int lx0, lx1, ly0, ly1;
+            if (!modeB) {
+                lx0 = (actA | actB) ? px : 0x7fffffff;
+                lx1 = (actA | actB) ? px : -1;
+                ly0 = actA ? pyA : (actB ? pyB : 0x7fffffff);
+                ly1 = actB ? pyB : (actA ? pyA : -1);
             } else {
-#pragma unroll
+                lx0 = act1 ? cpx : 0x7fffffff;
+                lx1 = act1 ? cpx : -1;
+                ly0 = act1 ? cpy : 0x7fffffff;
+                ly1 = act1 ? cpy : -1;
+            }
+            const int ax0 = __reduce_min_sync(0xffffffffu, lx0);
+            const int ax1 = __reduce_max_sync(0xffffffffu, lx1);
+            const int ay0 = __reduce_min_sync(0xffffffffu, ly0);
+            const int ay1 = __reduce_max_sync(0xffffffffu, ly1);
+            const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
+            // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip.
+            //      The list indices of the next 64 entries are loaded one round ahead (pf_pos / pf).
+            int cnt = 0;
+            while (cnt < kBuf && pos < cend) {
+                uint32_t idx[2];
+                if (pf_pos == pos) {
+                    idx[0] = pf[0];
+                    idx[1] = pf[1];
+                } else {
+    #pragma unroll
+                    for (int hh = 0; hh < 2; hh++) {
+                        const uint32_t e = pos + 32 * hh + lane;
+                        idx[hh] = e < cend ? clist[e] : 0xffffffffu;
+                    }
+                }
+                uint4 r0[2], r1[2];
+                bool keep[2];
+    #pragma unroll
                 for (int hh = 0; hh < 2; hh++) {
-                    const uint32_t e = pos + 32 * hh + lane;
-                    idx[hh] = e < cend ? clist[e] : 0xffffffffu;
+                    const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
+                    r1[hh] = rec[2 * i + 1];
+                    r0[hh] = rec[2 * i];
                 }
-            }
-            uint4 r0[2], r1[2];
-            bool keep[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
-                r1[hh] = rec[2 * i + 1];
-                r0[hh] = rec[2 * i];
-            }
-            pf_pos = pos + 64;
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                const uint32_t e = pf_pos + 32 * hh + lane;
-                pf[hh] = e < cend ? clist[e] : 0xffffffffu;
-            }
-            // The warp's block lies inside the tile, so "box overlaps the active rectangle" implies
-            // "box covers the tile": the per-tile list filter is implied (lists hold visible Gaussians only).
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
-                const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                keep[hh] = idx[hh] < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
-                           ellipse_may_touch2(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
-                                              __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
-                                              __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
-            }
-            uint32_t adv = 0;
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                if (cnt >= kBuf) break;
-                const uint32_t base = pos + 32 * hh;
-                if (base >= cend) break;
-                bool kp = keep[hh];
-                uint32_t bal = __ballot_sync(0xffffffffu, kp);
-                const int room = kBuf - cnt;
-                const uint32_t rank = __popc(bal & lt);
-                uint32_t step = min(32u, cend - base);
-                if (__popc(bal) > room) {
-                    const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
-                    const int cl = __ffs(cut) - 1;
-                    bal &= (1u << cl) - 1u;
-                    step = (uint32_t)cl;
-                    kp = kp && (int)lane < cl;
+                pf_pos = pos + 64;
+    #pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const uint32_t e = pf_pos + 32 * hh + lane;
+                    pf[hh] = e < cend ? clist[e] : 0xffffffffu;
                 }
-                if (kp) {
-                    const int d = cnt + (int)rank;
+                // The warp's block lies inside the tile, so "box overlaps the active rectangle" implies
+                // "box covers the tile": the per-tile list filter is implied (lists hold visible Gaussians only).
+    #pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
                     const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
                     const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                    bf.g[d] = make_float4(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
-                                          __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w));
-                    bf.h[d] = make_float4(__uint_as_float(r1[hh].x), __uint_as_float(r1[hh].y),
-                                          __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
-                                          __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
-                    const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
-                    const uint32_t dst = smem_u32(&bf.f[d][0]);
-#pragma unroll
-                    for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                    keep[hh] = idx[hh] < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
+                               ellipse_may_touch2(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
+                                                  __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
+                                                  __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
                 }
-                cnt += __popc(bal);
-                adv += step;
-                if (step < 32u) break;
-            }
-            pos += adv;
-            if (kCounts) { wk[0] += adv; wk[7] += 1; }
-        }
-        if (kCounts) wk[1] += cnt;
-        cp_async_wait_all();
-        __syncwarp();
-        // ---- composite the staged entries, 16 at a time: SIMT weights -> smem -> tensor cores
-        for (int j0 = 0; j0 < cnt; j0 += 16) {
-            const int nk = min(16, cnt - j0);
-            if (!modeB) {
-                const uint32_t mA = __ballot_sync(0xffffffffu, actA != 0u), mB = __ballot_sync(0xffffffffu, actB != 0u);
-                const int nA = __popc(mA), na = nA + __popc(mB);
-                if (na <= 32) {                           // enter the compacted mode (warp-uniform)
-                    modeB = true;
-                    movedA = actA != 0u;
-                    movedB = actB != 0u;
-                    const bool has = li < na;
-                    int src = 0;
-                    hs = 0;
-                    if (has) {
-                        if (li < nA) src = (int)__fns(mA, 0, li + 1);
-                        else { src = (int)__fns(mB, 0, li - nA + 1); hs = 1; }
+                uint32_t adv = 0;
+    #pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    if (cnt >= kBuf) break;
+                    const uint32_t base = pos + 32 * hh;
+                    if (base >= cend) break;
+                    bool kp = keep[hh];
+                    uint32_t bal = __ballot_sync(0xffffffffu, kp);
+                    const int room = kBuf - cnt;
+                    const uint32_t rank = __popc(bal & lt);
+                    uint32_t step = min(32u, cend - base);
+                    if (__popc(bal) > room) {
+                        const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
+                        const int cl = __ffs(cut) - 1;
+                        bal &= (1u << cl) - 1u;
+                        step = (uint32_t)cl;
+                        kp = kp && (int)lane < cl;
                     }
-                    const float tA = __shfl_sync(0xffffffffu, T.x, src), tB = __shfl_sync(0xffffffffu, T.y, src);
-                    const int cA = __shfl_sync(0xffffffffu, ncA, src), cB = __shfl_sync(0xffffffffu, ncB, src);
-                    ol = src;
-                    T1 = hs ? tB : tA;
-                    nc1 = hs ? cB : cA;
-                    act1 = has ? 1u : 0u;
-                    chas = has;
-                    cpx = bx0 + (ol & 7);
-                    cpy = by0 + (ol >> 3) + 4 * hs;
-                    actA = actB = 0u;
-                    // weight columns of pixels that stopped earlier are never written again: zero them all
-                    uint4* wz = reinterpret_cast<uint4*>(&bf.w[0][0][0]);
-                    for (int k = li; k < 2 * 16 * WP / 4; k += 32) wz[k] = make_uint4(0u, 0u, 0u, 0u);
-                    __syncwarp();
+                    if (kp) {
+                        const int d = cnt + (int)rank;
+                        const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
+                        const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
+                        bf.g[d] = make_float4(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
+                                              __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w));
+                        bf.h[d] = make_float4(__uint_as_float(r1[hh].x), __uint_as_float(r1[hh].y),
+                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
+                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
+                        const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
+                        const uint32_t dst = smem_u32(&bf.f[d][0]);
+    #pragma unroll
+                        for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                    }
+                    cnt += __popc(bal);
+                    adv += step;
+                    if (step < 32u) break;
                 }
+                pos += adv;
+                if (kCounts) { wk[0] += adv; wk[7] += 1; }
             }
-            if (modeB) {
-                const float cpxf = (float)cpx, cpyf = (float)cpy;
-                __half* const wh = reinterpret_cast<__half*>(&bf.w[0][0][0]) + 2 * ol + hs;   // column p', row 0 (hi)
-#pragma unroll 2
-                for (int jj = 0; jj < 16; jj += 2) {
-                    float w0 = 0.0f, w1 = 0.0f;
-                    if (jj < nk) {
-                        const bool has1 = jj + 1 < nk;
-                        const int j1 = j0 + jj + (has1 ? 1 : 0);
-                        const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
-                        const float4 G1 = bf.g[j1], H1 = bf.h[j1];
-                        // q of entries j, j+1 for this lane's pixel (normative a6 sequence per component)
-                        const float2 dx = sub2(bc2(cpxf), make_float2(G0.x, G1.x));
-                        const float2 dy = sub2(bc2(cpyf), make_float2(G0.y, G1.y));
-                        const float2 t1 = mul2(make_float2(G0.w, G1.w), dy);
-                        const float2 t2 = fma2(make_float2(G0.z, G1.z), dx, t1);
-                        const float2 t4 = mul2(mul2(make_float2(H0.x, H1.x), dy), dy);
-                        const float2 q = fma2(t2, dx, t4);
-                        const uint32_t b0 = __float_as_uint(hs ? H0.w : H0.z), b1 = __float_as_uint(hs ? H1.w : H1.z);
-                        const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : kInf;
-                        const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : kInf;
-                        if (kCounts) wk[2] += has1 ? 2 : 1;
-                        if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(qm0, qm1) <= qmax)) {
-                            const float2 e = exp_det2(mul2(bc2(-0.5f), q));
-                            const float2 ae = mul2(make_float2(H0.y, H1.y), e);
-                            const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
-                            const float2 om = sub2(bc2(1.0f), a);
-                            const float2 sc = mul2(a, bc2(2048.0f));
-                            {
-                                const float Tn = fmul(T1, om.x);
-                                const bool ok = qm0 <= qmax && a.x >= amin;
-                                const bool in = ok && Tn >= teps;
-                                if (ok && !in) act1 = 0u;
-                                w0 = in ? fmul(sc.x, T1) : 0.0f;
-                                T1 = in ? Tn : T1;
-                                if (kCounts) nc1 += in ? 1 : 0;
-                            }
-                            {
-                                const float Tn = fmul(T1, om.y);
-                                const bool ok = act1 && qm1 <= qmax && a.y >= amin;
-                                const bool in = ok && Tn >= teps;
-                                if (ok && !in) act1 = 0u;
-                                w1 = in ? fmul(sc.y, T1) : 0.0f;
-                                T1 = in ? Tn : T1;
-                                if (kCounts) nc1 += in ? 1 : 0;
-                            }
+            if (kCounts) wk[1] += cnt;
+            cp_async_wait_all();
+            __syncwarp();
+            // ---- composite the staged entries, 16 at a time: SIMT weights -> smem -> tensor cores
+            for (int j0 = 0; j0 < cnt; j0 += 16) {
+                const int nk = min(16, cnt - j0);
+                if (!modeB) {
+                    const uint32_t mA = __ballot_sync(0xffffffffu, actA != 0u), mB = __ballot_sync(0xffffffffu, actB != 0u);
+                    const int nA = __popc(mA), na = nA + __popc(mB);
+                    if (na <= 32) {                           // enter the compacted mode (warp-uniform)
+                        modeB = true;
+                        movedA = actA != 0u;
+                        movedB = actB != 0u;
+                        const bool has = li < na;
+                        int src = 0;
+                        hs = 0;
+                        if (has) {
+                            if (li < nA) src = (int)__fns(mA, 0, li + 1);
+                            else { src = (int)__fns(mB, 0, li - nA + 1); hs = 1; }
                         }
-                    }
-                    const __half2 hi = __floats2half2_rn(w0, w1);
-                    const float2 hf = __half22float2(hi);
-                    const __half2 lo = __floats2half2_rn(fsub(w0, hf.x), fsub(w1, hf.y));
-                    if (chas) {
-                        wh[jj * 2 * WP] = __low2half(hi);
-                        wh[(jj + 1) * 2 * WP] = __high2half(hi);
-                        wh[(16 + jj) * 2 * WP] = __low2half(lo);
-                        wh[(16 + jj + 1) * 2 * WP] = __high2half(lo);
+                        const float tA = __shfl_sync(0xffffffffu, T.x, src), tB = __shfl_sync(0xffffffffu, T.y, src);
+                        const int cA = __shfl_sync(0xffffffffu, ncA, src), cB = __shfl_sync(0xffffffffu, ncB, src);
+                        ol = src;
+                        T1 = hs ? tB : tA;
+                        nc1 = hs ? cB : cA;
+                        act1 = has ? 1u : 0u;
+                        chas = has;
+                        cpx = bx0 + (ol & 7);
+                        cpy = by0 + (ol >> 3) + 4 * hs;
+                        actA = actB = 0u;
+                        // weight columns of pixels that stopped earlier are never written again: zero them all
+                        uint4* wz = reinterpret_cast<uint4*>(&bf.w[0][0][0]);
+                        for (int k = li; k < 2 * 16 * WP / 4; k += 32) wz[k] = make_uint4(0u, 0u, 0u, 0u);
+                        __syncwarp();
                     }
                 }
-            } else {
-                // full chunks (16 staged entries) take a branch-free copy of the pair loop, so the
-                // scheduler can overlap consecutive pairs; the last, partial chunk keeps the guards
-                auto pairs = [&](auto full) {
-                    constexpr bool kFull = decltype(full)::value;
-#pragma unroll
+                if (modeB) {
+                    const float cpxf = (float)cpx, cpyf = (float)cpy;
+                    __half* const wh = reinterpret_cast<__half*>(&bf.w[0][0][0]) + 2 * ol + hs;   // column p', row 0 (hi)
+    #pragma unroll 2
                     for (int jj = 0; jj < 16; jj += 2) {
-                        float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
-                        if (kFull || jj < nk) {                          // warp-uniform
-                            const int j1 = j0 + jj + ((kFull || jj + 1 < nk) ? 1 : 0);
+                        float w0 = 0.0f, w1 = 0.0f;
+                        if (jj < nk) {
+                            const bool has1 = jj + 1 < nk;
+                            const int j1 = j0 + jj + (has1 ? 1 : 0);
                             const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
                             const float4 G1 = bf.g[j1], H1 = bf.h[j1];
-                            // q of both entries for both pixels; qm = q where the pixel is in the entry's box and
-                            // still compositing, else +inf (so "qm <= q_max" is the whole per-pixel geometric test)
-                            const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
-                            const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : kInf,
-                                                           (__float_as_uint(H0.w) & actB) ? q0.y : kInf);
-                            float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : kInf,
-                                                     (__float_as_uint(H1.w) & actB) ? q1.y : kInf);
-                            if (!kFull && jj + 1 >= nk) qm1 = make_float2(kInf, kInf);
-                            if (kCounts) wk[2] += (kFull || jj + 1 < nk) ? 2 : 1;
-                            if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(fminf(qm0.x, qm0.y), fminf(qm1.x, qm1.y)) <= qmax)) {
-                                // exp / alpha' of both entries are independent of T: computed side by side
-                                const float2 x0 = exp_det2(mul2(bc2(-0.5f), q0));
-                                const float2 x1 = exp_det2(mul2(bc2(-0.5f), q1));
-                                const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);
-                                const float2 a0 = make_float2(fminf(amax, ae0.x), fminf(amax, ae0.y));
-                                const float2 a1 = make_float2(fminf(amax, ae1.x), fminf(amax, ae1.y));
-                                if (kCounts) {
-                                    wk[3] += __any_sync(0xffffffffu, fminf(qm0.x, qm0.y) <= qmax) ? 1 : 0;
-                                    wk[3] += __any_sync(0xffffffffu, fminf(qm1.x, qm1.y) <= qmax) ? 1 : 0;
+                            // q of entries j, j+1 for this lane's pixel (normative a6 sequence per component)
+                            const float2 dx = sub2(bc2(cpxf), make_float2(G0.x, G1.x));
+                            const float2 dy = sub2(bc2(cpyf), make_float2(G0.y, G1.y));
+                            const float2 t1 = mul2(make_float2(G0.w, G1.w), dy);
+                            const float2 t2 = fma2(make_float2(G0.z, G1.z), dx, t1);
+                            const float2 t4 = mul2(mul2(make_float2(H0.x, H1.x), dy), dy);
+                            const float2 q = fma2(t2, dx, t4);
+                            const uint32_t b0 = __float_as_uint(hs ? H0.w : H0.z), b1 = __float_as_uint(hs ? H1.w : H1.z);
+                            const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : kInf;
+                            const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : kInf;
+                            if (kCounts) wk[2] += has1 ? 2 : 1;
+                            if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(qm0, qm1) <= qmax)) {
+                                const float2 e = exp_det2(mul2(bc2(-0.5f), q));
+                                const float2 ae = mul2(make_float2(H0.y, H1.y), e);
+                                const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
+                                const float2 om = sub2(bc2(1.0f), a);
+                                const float2 sc = mul2(a, bc2(2048.0f));
+                                {
+                                    const float Tn = fmul(T1, om.x);
+                                    const bool ok = qm0 <= qmax && a.x >= amin;
+                                    const bool in = ok && Tn >= teps;
+                                    if (ok && !in) act1 = 0u;
+                                    w0 = in ? fmul(sc.x, T1) : 0.0f;
+                                    T1 = in ? Tn : T1;
+                                    if (kCounts) nc1 += in ? 1 : 0;
                                 }
-                                w0 = tstep<kCounts>(qm0, a0, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
-                                // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
-                                qm1 = make_float2(actA ? qm1.x : kInf, actB ? qm1.y : kInf);
-                                w1 = tstep<kCounts>(qm1, a1, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                                {
+                                    const float Tn = fmul(T1, om.y);
+                                    const bool ok = act1 && qm1 <= qmax && a.y >= amin;
+                                    const bool in = ok && Tn >= teps;
+                                    if (ok && !in) act1 = 0u;
+                                    w1 = in ? fmul(sc.y, T1) : 0.0f;
+                                    T1 = in ? Tn : T1;
+                                    if (kCounts) nc1 += in ? 1 : 0;
+                                }
                             }
                         }
-                        // split into fp16 hi / lo and store rows jj, jj+1
-                        const __half2 h0 = __floats2half2_rn(w0.x, w0.y), h1 = __floats2half2_rn(w1.x, w1.y);
-                        const float2 r0 = sub2(w0, __half22float2(h0)), r1 = sub2(w1, __half22float2(h1));
-                        const __half2 l0 = __floats2half2_rn(r0.x, r0.y), l1 = __floats2half2_rn(r1.x, r1.y);
-                        wst[jj * WP] = *reinterpret_cast<const uint32_t*>(&h0);
-                        wst[(jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&h1);
-                        wst[16 * WP + jj * WP] = *reinterpret_cast<const uint32_t*>(&l0);
-                        wst[16 * WP + (jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&l1);
+                        const __half2 hi = __floats2half2_rn(w0, w1);
+                        const float2 hf = __half22float2(hi);
+                        const __half2 lo = __floats2half2_rn(fsub(w0, hf.x), fsub(w1, hf.y));
+                        if (chas) {
+                            wh[jj * 2 * WP] = __low2half(hi);
+                            wh[(jj + 1) * 2 * WP] = __high2half(hi);
+                            wh[(16 + jj) * 2 * WP] = __low2half(lo);
+                            wh[(16 + jj + 1) * 2 * WP] = __high2half(lo);
+                        }
                     }
-                };
-                if (nk == 16) pairs(std::integral_constant<bool, true>());
-                else pairs(std::integral_constant<bool, false>());
-            }
-            __syncwarp();
-            // B fragments: feature rows j0 .. j0+15 (rows past cnt carry weight 0: clamp to a staged row)
-            uint32_t bfr[NT][2];
-            {
-                const int row = min(j0 + bk, cnt - 1);
-                const uint32_t rb = b_base + (uint32_t)(row * PH * 2);
-                if constexpr (NT == 1) {
-                    ldsm_x2_t(rb, bfr[0][0], bfr[0][1]);
                 } else {
-#pragma unroll
-                    for (int np = 0; np < NT / 2; np++)
-                        ldsm_x4_t(rb + np * 32, bfr[2 * np][0], bfr[2 * np][1], bfr[2 * np + 1][0], bfr[2 * np + 1][1]);
+                    // full chunks (16 staged entries) take a branch-free copy of the pair loop, so the
+                    // scheduler can overlap consecutive pairs; the last, partial chunk keeps the guards
+                    auto pairs = [&](auto full) {
+                        constexpr bool kFull = decltype(full)::value;
+    #pragma unroll
+                        for (int jj = 0; jj < 16; jj += 2) {
+                            float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
+                            if (kFull || jj < nk) {                          // warp-uniform
+                                const int j1 = j0 + jj + ((kFull || jj + 1 < nk) ? 1 : 0);
+                                const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
+                                const float4 G1 = bf.g[j1], H1 = bf.h[j1];
+                                // q of both entries for both pixels; qm = q where the pixel is in the entry's box and
+                                // still compositing, else +inf (so "qm <= q_max" is the whole per-pixel geometric test)
+                                const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
+                                const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : kInf,
+                                                               (__float_as_uint(H0.w) & actB) ? q0.y : kInf);
+                                float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : kInf,
+                                                         (__float_as_uint(H1.w) & actB) ? q1.y : kInf);
+                                if (!kFull && jj + 1 >= nk) qm1 = make_float2(kInf, kInf);
+                                if (kCounts) wk[2] += (kFull || jj + 1 < nk) ? 2 : 1;
+                                if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(fminf(qm0.x, qm0.y), fminf(qm1.x, qm1.y)) <= qmax)) {
+                                    // exp / alpha' of both entries are independent of T: computed side by side
+                                    const float2 x0 = exp_det2(mul2(bc2(-0.5f), q0));
+                                    const float2 x1 = exp_det2(mul2(bc2(-0.5f), q1));
+                                    const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);
+                                    const float2 a0 = make_float2(fminf(amax, ae0.x), fminf(amax, ae0.y));
+                                    const float2 a1 = make_float2(fminf(amax, ae1.x), fminf(amax, ae1.y));
+                                    if (kCounts) {
+                                        wk[3] += __any_sync(0xffffffffu, fminf(qm0.x, qm0.y) <= qmax) ? 1 : 0;
+                                        wk[3] += __any_sync(0xffffffffu, fminf(qm1.x, qm1.y) <= qmax) ? 1 : 0;
+                                    }
+                                    w0 = tstep<kCounts>(qm0, a0, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                                    // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
+                                    qm1 = make_float2(actA ? qm1.x : kInf, actB ? qm1.y : kInf);
+                                    w1 = tstep<kCounts>(qm1, a1, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                                }
+                            }
+                            // split into fp16 hi / lo and store rows jj, jj+1
+                            const __half2 h0 = __floats2half2_rn(w0.x, w0.y), h1 = __floats2half2_rn(w1.x, w1.y);
+                            const float2 r0 = sub2(w0, __half22float2(h0)), r1 = sub2(w1, __half22float2(h1));
+                            const __half2 l0 = __floats2half2_rn(r0.x, r0.y), l1 = __floats2half2_rn(r1.x, r1.y);
+                            wst[jj * WP] = *reinterpret_cast<const uint32_t*>(&h0);
+                            wst[(jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&h1);
+                            wst[16 * WP + jj * WP] = *reinterpret_cast<const uint32_t*>(&l0);
+                            wst[16 * WP + (jj + 1) * WP] = *reinterpret_cast<const uint32_t*>(&l1);
+                        }
+                    };
+                    if (nk == 16) pairs(std::integral_constant<bool, true>());
+                    else pairs(std::integral_constant<bool, false>());
                 }
-            }
-#pragma unroll
-            for (int mt = 0; mt < 4; mt++) {
-                uint32_t ah[4], al[4];
-                ldsm_x4_t(a_base + mt * 32, ah[0], ah[1], ah[2], ah[3]);
-                ldsm_x4_t(a_base + mt * 32 + kLoOff, al[0], al[1], al[2], al[3]);
-#pragma unroll
-                for (int nt = 0; nt < NT; nt++) {
-                    hmma16816(acc[mt][nt], ah, bfr[nt][0], bfr[nt][1]);
-                    hmma16816(acc[mt][nt], al, bfr[nt][0], bfr[nt][1]);
+                __syncwarp();
+                // B fragments: feature rows j0 .. j0+15 (rows past cnt carry weight 0: clamp to a staged row)
+                uint32_t bfr[NT][2];
+                {
+                    const int row = min(j0 + bk, cnt - 1);
+                    const uint32_t rb = b_base + (uint32_t)(row * PH * 2);
+                    if constexpr (NT == 1) {
+                        ldsm_x2_t(rb, bfr[0][0], bfr[0][1]);
+                    } else {
+    #pragma unroll
+                        for (int np = 0; np < NT / 2; np++)
+                            ldsm_x4_t(rb + np * 32, bfr[2 * np][0], bfr[2 * np][1], bfr[2 * np + 1][0], bfr[2 * np + 1][1]);
+                    }
                 }
+    #pragma unroll
+                for (int mt = 0; mt < 4; mt++) {
+                    uint32_t ah[4], al[4];
+                    ldsm_x4_t(a_base + mt * 32, ah[0], ah[1], ah[2], ah[3]);
+                    ldsm_x4_t(a_base + mt * 32 + kLoOff, al[0], al[1], al[2], al[3]);
+    #pragma unroll
+                    for (int nt = 0; nt < NT; nt++) {
+                        hmma16816(acc[mt][nt], ah, bfr[nt][0], bfr[nt][1]);
+                        hmma16816(acc[mt][nt], al, bfr[nt][0], bfr[nt][1]);
+                    }
+                }
+                __syncwarp();
+                if (!__any_sync(0xffffffffu, (actA | actB | act1) != 0u)) break;
             }
             __syncwarp();
-            if (!__any_sync(0xffffffffu, (actA | actB | act1) != 0u)) break;
         }
-        __syncwarp();
-    }
 
-    if (kCounts && lane == 0) {
-        unsigned long long* work = const_cast<CallState*>(cs)->work;
-        wk[6] = 1;
-#pragma unroll
-        for (int k = 0; k < 8; k++) atomicAdd(&work[k], wk[k]);
-    }
-    // accumulator (mt, row r in 0..15) <-> pixel p' = 16 mt + r = 2 l' + h: lane l' = 8 mt + (r >> 1), pixel A/B = r & 1
-    const int g = li >> 2, t = li & 3;
-#pragma unroll
-    for (int mt = 0; mt < 4; mt++) {
-#pragma unroll
-        for (int half = 0; half < 2; half++) {
-            const int r = g + 8 * half;
-            const int l2 = 8 * mt + (r >> 1);
-            const int ox = bx0 + (l2 & 7), oy = by0 + (l2 >> 3) + 4 * (r & 1);
-            if (ox < W && oy < H) {
-                float* out = Fout + ((size_t)oy * W + ox) * C + 2 * t;
-#pragma unroll
-                for (int nt = 0; nt < NT; nt++)
-                    *reinterpret_cast<float2*>(out + 8 * nt) =
-                        make_float2(acc[mt][nt][2 * half] * (1.0f / 2048.0f), acc[mt][nt][2 * half + 1] * (1.0f / 2048.0f));
+        if (kCounts && lane == 0) {
+            unsigned long long* work = const_cast<CallState*>(cs)->work;
+            wk[6] = 1;
+    #pragma unroll
+            for (int k = 0; k < 8; k++) atomicAdd(&work[k], wk[k]);
+        }
+        // accumulator (mt, row r in 0..15) <-> pixel p' = 16 mt + r = 2 l' + h: lane l' = 8 mt + (r >> 1), pixel A/B = r & 1
+        const int g = li >> 2, t = li & 3;
+    #pragma unroll
+        for (int mt = 0; mt < 4; mt++) {
+    #pragma unroll
+            for (int half = 0; half < 2; half++) {
+                const int r = g + 8 * half;
+                const int l2 = 8 * mt + (r >> 1);
+                const int ox = bx0 + (l2 & 7), oy = by0 + (l2 >> 3) + 4 * (r & 1);
+                if (ox < W && oy < H) {
+                    float* out = Fout + ((size_t)oy * W + ox) * C + 2 * t;
+    #pragma unroll
+                    for (int nt = 0; nt < NT; nt++)
+                        *reinterpret_cast<float2*>(out + 8 * nt) =
+                            make_float2(acc[mt][nt][2 * half] * (1.0f / 2048.0f), acc[mt][nt][2 * half + 1] * (1.0f / 2048.0f));
+                }
             }
         }
-    }
-#pragma unroll
-    for (int hh = 0; hh < 2; hh++) {
-        const int py = hh ? pyB : pyA;
-        if (px < W && py < H && !(hh ? movedB : movedA)) {        // moved pixels are written by their new lane
-            const size_t pix = (size_t)py * W + px;
-            Aout[pix] = fsub(1.0f, hh ? T.y : T.x);
-            if (kCounts) ncontrib[pix] = hh ? ncB : ncA;
+    #pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+            const int py = hh ? pyB : pyA;
+            if (px < W && py < H && !(hh ? movedB : movedA)) {        // moved pixels are written by their new lane
+                const size_t pix = (size_t)py * W + px;
+                Aout[pix] = fsub(1.0f, hh ? T.y : T.x);
+                if (kCounts) ncontrib[pix] = hh ? ncB : ncA;
+            }
         }
-    }
-    if (modeB && chas) {
-        const size_t pix = (size_t)cpy * W + cpx;
-        Aout[pix] = fsub(1.0f, T1);
-        if (kCounts) ncontrib[pix] = nc1;
+        if (modeB && chas) {
+            const size_t pix = (size_t)cpy * W + cpx;
+            Aout[pix] = fsub(1.0f, T1);
+            if (kCounts) ncontrib[pix] = nc1;
+        }
+
     }
 }
 
@@ -1002,12 +1016,22 @@ static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, cons
         attr_set = true;
     }
     if (tiles == 0) return cudaSuccess;
+    // persistent warps: as many CTAs as are co-resident (more would only find the block counter spent)
+    static int resident = 0;
+    if (resident == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false>, kThreads, smem);
+        resident = std::max(1, sms * std::max(1, per_sm));
+    }
+    const int grid = std::min(tiles, resident);
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     const __half* fh = static_cast<const __half*>(feat);
     if (ncontrib)
-        k_composite_tc<C, true><<<tiles, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
+        k_composite_tc<C, true><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
     else
-        k_composite_tc<C, false><<<tiles, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
+        k_composite_tc<C, false><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
     return cudaGetLastError();
 }
 

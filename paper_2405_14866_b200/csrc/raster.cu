@@ -462,9 +462,10 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
                 const int cx = (x0 + xi) << sb, cy = (y0 + yi) << sb;
                 uint32_t rect;
                 if (sb == 1) {                               // 2 x 2 tiles: the tile mask itself
-                    const uint32_t mx = (uint32_t)(cx >= tx0 && cx <= tx1) | ((uint32_t)(cx + 1 >= tx0 && cx + 1 <= tx1) << 1);
-                    const uint32_t my = (uint32_t)(cy >= ty0 && cy <= ty1) | ((uint32_t)(cy + 1 >= ty0 && cy + 1 <= ty1) << 1);
-                    rect = ((my & 1u) ? mx : 0u) | ((my & 2u) ? (mx << 2) : 0u);
+                    // inside the box's bin range only the first / last bin column (row) can miss a tile
+                    const uint32_t mx = 3u & ~((cx < tx0) ? 1u : 0u) & ~((cx + 1 > tx1) ? 2u : 0u);
+                    const uint32_t my = 3u & ~((cy < ty0) ? 1u : 0u) & ~((cy + 1 > ty1) ? 2u : 0u);
+                    rect = (mx * (my & 1u)) | ((mx << 2) * (my >> 1));
                 } else {                                     // 4 x 4 tiles: the bin-local tile rectangle
                     rect = (uint32_t)max(tx0 - cx, 0) | ((uint32_t)min(tx1 - cx, qm) << sb) |
                            ((uint32_t)max(ty0 - cy, 0) << (2 * sb)) | ((uint32_t)min(ty1 - cy, qm) << (3 * sb));

@@ -95,6 +95,35 @@ def test_c3_full_size_sampled_tiles(ctx, oracle_lib):
     assert out["n"] == 1666464
 
 
+def test_wide_target_64px_coarse_bins(ctx, oracle_lib):
+    """A target wider than 1024 px bins in 64 x 64-pixel coarse bins (4 x 4 tiles, the tile rectangle
+    in the entry bits; include/ta.h ta_rasterize): every stage and every tile list bit-exact, ragged
+    in both directions (88 x 1100)."""
+    out, _ = full_parity(ctx, oracle_lib, sg.make_config("c3", res=256, target_hw=(88, 1100)))
+    assert out["K"] > 0
+
+
+def test_coarse_bins_fall_back_for_large_capacity(ctx, oracle_lib):
+    """With more than 2^24 Gaussian slots (n = -1: the capacity bounds the indices) a > 1024 px target
+    keeps 32 x 32-pixel bins (28 index bits): different coarse binning, identical output bits."""
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("c3", res=128, target_hw=(72, 1040))
+    gp = P.gpu_params(s)
+    cam = s.targets[0]
+    small = P.gpu_unproject(ctx, s, gp)
+    ref = P.gpu_rasterize(ctx, small, cam, gp)
+    big = tb.GaussianBuffers((1 << 24) + 1, s.C, s.feat_dtype)
+    views, keep = tb.views_to_device(s.views)
+    ctx.unproject(views, gp, big)
+    torch.cuda.synchronize()
+    out = P.gpu_rasterize(ctx, big, cam, gp)
+    assert out["n"] == ref["n"] and out["Kc"] != ref["Kc"]
+    for k in ("F", "A", "order", "ranges", "list"):
+        assert np.array_equal(out[k].view(np.uint8), ref[k].view(np.uint8)), k
+    del big
+
+
 @pytest.mark.parametrize("eye", [0, 1])
 def test_paper_variant_reduced(ctx, oracle_lib, eye):
     """SURVEY 8(f) NEXT #3, the paper-exact variant: cam0 + cam2 + cam3 lifted

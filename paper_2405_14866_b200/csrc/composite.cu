@@ -424,6 +424,17 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
                         if ((uint32_t)qy >= y0 && (uint32_t)qy <= y1) tm |= mx << (qy * TPB);
                     if (pos + 32 * u + lane >= s1) tm = 0u;
                 }
+                if (NQ == 16 && __all_sync(0xffffffffu, tm == (1u << NQ) - 1u)) {   // 32 entries covering the whole bin
+#pragma unroll
+                    for (int q = 0; q < NQ; q++) {
+                        if (write) {
+                            const uint64_t p = tbase + (uint64_t)q * len + run[q] + lane;
+                            if (p < tlist_cap) tlist[p] = idx;
+                        }
+                        run[q] += 32u;
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int q = 0; q < NQ; q++) {
                     const bool ok = (tm >> q) & 1u;

@@ -702,8 +702,9 @@ ta_status ta_rasterize_backward(ta_context* c, const ta_gaussians* g, int64_t n,
     (void)cap;   // the outputs hold the call's n Gaussians: zeroed on the device from its count
     const CompositeGeom& cg = c->last_cg;
     cudaError_t e = launch_composite_bwd(g->C, g->feat_dtype == TA_F16 ? 2 : 4, cg.TX * cg.TY, (const uint4*)c->rec.p,
-                                         g->feat, (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p, cg, rc,
-                                         (const CallState*)c->cs.p, (uint64_t)(c->tlist.bytes / 4), grad_F, grad_A,
+                                         g->feat, (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p,
+                                         (const uint32_t*)c->tile_order.p, cg, rc,
+                                         (CallState*)c->cs.p, (uint64_t)(c->tlist.bytes / 4), grad_F, grad_A,
                                          d_mean2, d_conic, d_alpha, d_feat, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "backward launch");
     c->launches += 2;   // k_bwd_zero + k_composite_bwd

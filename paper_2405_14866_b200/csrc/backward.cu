@@ -13,8 +13,11 @@
 // + G_A T_end/(1 - alpha'_j), chained to alpha, q, conic and mean2, and w_j G_F for the features.
 // Per entry the 32 pixels of a warp are summed with shuffles and one lane adds them to the global
 // gradient arrays (fp32 atomics: the summation order over warps is not fixed).
+#include <algorithm>
+#include <cuda_bf16.h>
 #include "common.cuh"
 #include "internal.h"
+#include "tc_dev.cuh"
 
 namespace ta {
 
@@ -230,12 +233,402 @@ __global__ void k_bwd_zero(const CallState* __restrict__ cs, int C, float* __res
     }
 }
 
-cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const uint4* rec, const void* feat, const uint32_t* tlist,
-                                 const uint2* trng, CompositeGeom cg, RasterConsts rc, const CallState* cs,
+// ============================================================================ tensor-core variant
+// k_composite_bwd_tc<C> (fp16-stored features, C in {16, 32, 64}): the forward compositor's layout --
+// persistent warps over 8x8 blocks, lane l owning the pixels (l&7, l>>3) and (l&7, (l>>3)+4), entries
+// culled against the block's still-active pixels and staged 16 at a time -- walked twice per block.
+// The three per-entry contractions run on the tensor cores (mma.sync m16n8k16, fp32 accumulate):
+//   g[p][j]      = G_F(p) . f_j          G[64 px x 16] = GF[64 x C] . f^T       (fp16 hi/lo GF, scaled)
+//   dL/df_j      = sum_p w_pj G_F(p)     D[16 x C]     = W^T[16 x 64] . GF      (fp16 hi/lo both)
+//   moments_j    = sum_p da_pj u(p)      M[16 x 8]     = DA^T[16 x 64] . U      (bf16 hi/lo, U exact)
+// with da = dL/dalpha (per pixel) and u(p) = (1, x, y, x^2, xy, y^2) in block-local pixel
+// coordinates.  dL/dq = -alpha_j / 2 * da (the same factor e links both), so the centre and conic
+// gradients sum_p dq (dx, dy, dx^2, dx dy, dy^2) follow from the moments by expanding dx = x - mx'.
+// Pass 1 replays the decisions (the forward's fp32 sequence) for S = sum_j w_j g_j and T_end; pass 2
+// forms dL/dalpha'_j (R25) per pixel and entry, stages w, dq, dalpha in shared memory and reduces them
+// over the 64 pixels with the MMAs above; one lane per entry adds the sums to the gradient arrays
+// (fp32 atomics).  GF is scaled per block by a power of two (max |GF| -> 2^14) so its fp16 hi/lo
+// split keeps ~22 bits; every result is unscaled exactly.
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void bmma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<const uint32_t*>(&h); }
+__device__ __forceinline__ uint32_t b2u(__nv_bfloat162 h) { return *reinterpret_cast<const uint32_t*>(&h); }
+
+constexpr int kBwdBuf = 16;          // entries staged per round (one MMA k- or n-extent)
+
+template <int C>
+struct BwdBuf {
+    static constexpr int PH = (((C + 8) / 8) & 1) ? C + 8 : C + 16;   // fp16 row pitch: odd number of 16-B chunks
+    static constexpr int WP = 36;                                     // words per [entry][pixel'] row (144 B)
+    float4 g[kBwdBuf];                 // mx, my, ca, cb2
+    float4 h[kBwdBuf];                 // cc, alpha, box lane mask (pixel A), (pixel B)
+    uint32_t id[kBwdBuf];              // array index
+    __half f[kBwdBuf][PH];             // staged fp16 feature rows
+    __half gf[2][64][PH];              // scaled GF, fp16 hi / lo, row p' = 2 lane + (0: pixel A, 1: pixel B)
+    float2 G[kBwdBuf][32];             // scaled g of (entry, lane): (pixel A, pixel B)
+    uint32_t w[2][kBwdBuf][WP];        // fp16 hi / lo of 2^11 w, word = lane: (pixel A, pixel B)
+    uint32_t da[2][kBwdBuf][WP];       // bf16 hi / lo of dL/dalpha, word = lane: (pixel A, pixel B)
+    float mom[kBwdBuf][8];             // per entry: sum da (1, x, y, xx, xy, yy)
+};
+
+template <int C>
+__global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat,
+                                                         const uint32_t* __restrict__ tlist, const uint2* __restrict__ trng,
+                                                         const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
+                                                         CallState* __restrict__ cs, uint64_t list_cap,
+                                                         const float* __restrict__ GF, const float* __restrict__ GA,
+                                                         float* __restrict__ d_mean2, float* __restrict__ d_conic,
+                                                         float* __restrict__ d_alpha, float* __restrict__ d_feat) {
+    constexpr int PH = BwdBuf<C>::PH, WP = BwdBuf<C>::WP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdBuf<C>& bf = *reinterpret_cast<BwdBuf<C>*>(smem_raw);
+    const uint32_t lane = lane_id();
+    const int li = (int)lane, gq = li >> 2, tq = li & 3;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t n = cs->n;
+    const int W = cg.W, H = cg.H;
+    const float qmax = rc.q_max, amax = rc.alpha_max, amin = rc.alpha_min, teps = rc.t_eps;
+    const float qlim = qmax * 1.015625f + 0.01f;
+
+    // U fragments (B operand of the moment MMA, constant): element k of k-step ks is pixel p' = 16 ks + k
+    uint32_t ub[4][2];
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++)
+#pragma unroll
+        for (int hf = 0; hf < 2; hf++) {
+            const int l2 = 8 * ks + tq + 4 * hf;             // lane of pixels p' = 2 l2 (A), 2 l2 + 1 (B)
+            const float x = (float)(l2 & 7), yA = (float)(l2 >> 3), yB = yA + 4.0f;
+            auto u = [&](float y) {
+                switch (gq) {
+                    case 0: return 1.0f;
+                    case 1: return x;
+                    case 2: return y;
+                    case 3: return x * x;
+                    case 4: return x * y;
+                    case 5: return y * y;
+                    default: return 0.0f;
+                }
+            };
+            ub[ks][hf] = b2u(__floats2bfloat162_rn(u(yA), u(yB)));
+        }
+    // ldmatrix lane addresses
+    const uint32_t gf_a = smem_u32(&bf.gf[0][(li & 7) + 8 * ((li >> 3) & 1)][8 * (li >> 4)]);     // A: GF rows, + 16 mt rows, + 16 ks cols
+    const uint32_t f_b = smem_u32(&bf.f[(li & 7) + 8 * (li >> 4)][8 * ((li >> 3) & 1)]);          // B: f rows (entries), + 16 ks cols
+    const uint32_t gf_bt = smem_u32(&bf.gf[0][(li & 7) + 8 * ((li >> 3) & 1)][8 * (li >> 4)]);    // B (trans): GF rows p', + 16 ks rows, + 16 np cols
+    const uint32_t w_a = smem_u32(&bf.w[0][(li & 7) + 8 * ((li >> 3) & 1)][4 * (li >> 4)]);        // A: W rows (entries), + 8 ks words
+    const uint32_t da_a = smem_u32(&bf.da[0][(li & 7) + 8 * ((li >> 3) & 1)][4 * (li >> 4)]);
+    constexpr uint32_t kGfLo = 64 * PH * 2, kWLo = kBwdBuf * WP * 4;
+
+    uint32_t* const wq = &cs->scan_counter[7];
+    const uint32_t nblk = 4u * (uint32_t)(cg.TX * cg.TY);
+    for (;;) {
+        uint32_t blk = 0;
+        if (lane == 0) blk = atomicAdd(wq, 1u);
+        blk = __shfl_sync(0xffffffffu, blk, 0);
+        if (blk >= nblk) break;
+        const int tile = (int)order[blk >> 2];
+        const uint32_t qd = blk & 3u;
+        const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
+        const uint2 tr = trng[tile];
+        const uint32_t cstart = tr.x;
+        uint32_t cend = tr.x + tr.y;
+        if (cend > list_cap) cend = (uint32_t)list_cap;
+        const int bx0 = txi * kTile + 8 * (int)(qd & 1), by0 = tyi * kTile + 8 * (int)(qd >> 1);
+        const int px = bx0 + (li & 7), pyA = by0 + (li >> 3), pyB = pyA + 4;
+        const float pxf = (float)px;
+        const float2 py2 = make_float2((float)pyA, (float)pyB);
+        const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
+
+        // ---- GF of the block, scaled by gsc = 2^(14 - e) (max |GF| = 2^e ... 2^(e+1)), fp16 hi / lo
+        float mx_abs = 0.0f;
+        {
+            const float* rA = GF + ((size_t)pyA * W + px) * C;
+            const float* rB = GF + ((size_t)pyB * W + px) * C;
+#pragma unroll 4
+            for (int c = 0; c < C; c += 4) {
+                if (inA) {
+                    const float4 v = *reinterpret_cast<const float4*>(rA + c);
+                    mx_abs = fmaxf(mx_abs, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+                }
+                if (inB) {
+                    const float4 v = *reinterpret_cast<const float4*>(rB + c);
+                    mx_abs = fmaxf(mx_abs, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+                }
+            }
+        }
+        mx_abs = __reduce_max_sync(0xffffffffu, __float_as_uint(mx_abs)) == 0u ? 0.0f
+                 : __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mx_abs)));
+        const int ex = mx_abs > 0.0f ? (int)((__float_as_uint(mx_abs) >> 23) & 255u) - 127 : 0;
+        const int sh = min(max(14 - ex, -100), 100);
+        const float gsc = ldexpf(1.0f, sh), igsc = ldexpf(1.0f, -sh);
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+            const bool ok = hh ? inB : inA;
+            const float* r = GF + ((size_t)(hh ? pyB : pyA) * W + px) * C;
+            __half* hi = &bf.gf[0][2 * li + hh][0];
+            __half* lo = &bf.gf[1][2 * li + hh][0];
+#pragma unroll 4
+            for (int c = 0; c < C; c += 2) {
+                const float2 v = ok ? *reinterpret_cast<const float2*>(r + c) : make_float2(0.0f, 0.0f);
+                const float2 sv = make_float2(v.x * gsc, v.y * gsc);
+                const __half2 h2 = __floats2half2_rn(sv.x, sv.y);
+                const float2 hf = __half22float2(h2);
+                *reinterpret_cast<__half2*>(hi + c) = h2;
+                *reinterpret_cast<__half2*>(lo + c) = __floats2half2_rn(sv.x - hf.x, sv.y - hf.y);
+            }
+        }
+        const float2 ga2 = make_float2(inA ? GA[(size_t)pyA * W + px] * gsc : 0.0f,
+                                       inB ? GA[(size_t)pyB * W + px] * gsc : 0.0f);
+        __syncwarp();
+
+        float2 S = make_float2(0.0f, 0.0f), Tend = make_float2(1.0f, 1.0f);
+        for (int pass = 0; pass < 2; pass++) {
+            float2 T = make_float2(1.0f, 1.0f), Sup = make_float2(0.0f, 0.0f);
+            uint32_t actA = inA ? (1u << lane) : 0u, actB = inB ? (1u << lane) : 0u;
+            uint32_t pos = cstart;
+            while (pos < cend && __any_sync(0xffffffffu, (actA | actB) != 0u)) {
+                // culling rectangle = bounding box of the pixels still compositing
+                const int lx0 = (actA | actB) ? px : 0x7fffffff, lx1 = (actA | actB) ? px : -1;
+                const int ly0 = actA ? pyA : (actB ? pyB : 0x7fffffff), ly1 = actB ? pyB : (actA ? pyA : -1);
+                const int ax0 = __reduce_min_sync(0xffffffffu, lx0), ax1 = __reduce_max_sync(0xffffffffu, lx1);
+                const int ay0 = __reduce_min_sync(0xffffffffu, ly0), ay1 = __reduce_max_sync(0xffffffffu, ly1);
+                const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
+                // ---- fill: up to 16 entries in list order (32 list entries per round trip)
+                int cnt = 0;
+                while (cnt < kBwdBuf && pos < cend) {
+                    const uint32_t e = pos + lane;
+                    const uint32_t idx = e < cend ? tlist[e] : 0xffffffffu;
+                    const uint32_t i = idx < n ? idx : 0u;
+                    const uint4 r1 = rec[2 * i + 1], r0 = rec[2 * i];
+                    const int gx0 = (int)(r1.z & 0xffff), gx1 = (int)(r1.z >> 16);
+                    const int gy0 = (int)(r1.w & 0xffff), gy1 = (int)(r1.w >> 16);
+                    bool kp = idx < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
+                              ellipse_may_touch2(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
+                                                 __uint_as_float(r0.w), __uint_as_float(r1.x), X0, X1, Y0, Y1, qlim);
+                    uint32_t bal = __ballot_sync(0xffffffffu, kp);
+                    const int room = kBwdBuf - cnt;
+                    const uint32_t rank = __popc(bal & lt);
+                    uint32_t step = min(32u, cend - pos);
+                    if (__popc(bal) > room) {
+                        const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
+                        const int cl = __ffs(cut) - 1;
+                        bal &= (1u << cl) - 1u;
+                        step = (uint32_t)cl;
+                        kp = kp && li < cl;
+                    }
+                    if (kp) {
+                        const int d = cnt + (int)rank;
+                        bf.g[d] = make_float4(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
+                                              __uint_as_float(r0.w));
+                        bf.h[d] = make_float4(__uint_as_float(r1.x), __uint_as_float(r1.y),
+                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
+                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
+                        bf.id[d] = idx;
+                        const char* src = reinterpret_cast<const char*>(feat + (size_t)idx * C);
+                        const uint32_t dst = smem_u32(&bf.f[d][0]);
+#pragma unroll
+                        for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                    }
+                    cnt += __popc(bal);
+                    pos += step;
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                if (cnt == 0) continue;
+                // ---- g = GF . f^T on the tensor cores -> bf.G[entry][lane] (pixel A, pixel B)
+#pragma unroll
+                for (int mt = 0; mt < 4; mt++) {
+                    float acc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+#pragma unroll
+                    for (int ks = 0; ks < C / 16; ks++) {
+                        uint32_t ah[4], al[4], b[4];
+                        const uint32_t aa = gf_a + (uint32_t)((16 * mt * PH + 16 * ks) * 2);
+                        ldsm_x4(aa, ah[0], ah[1], ah[2], ah[3]);
+                        ldsm_x4(aa + kGfLo, al[0], al[1], al[2], al[3]);
+                        ldsm_x4(f_b + (uint32_t)(16 * ks * 2), b[0], b[1], b[2], b[3]);
+                        hmma16816(acc[0], ah, b[0], b[1]);
+                        hmma16816(acc[0], al, b[0], b[1]);
+                        hmma16816(acc[1], ah, b[2], b[3]);
+                        hmma16816(acc[1], al, b[2], b[3]);
+                    }
+                    // row r = 16 mt + gq (+8) is pixel p' = r: lane r >> 1, component r & 1
+#pragma unroll
+                    for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+                        for (int e2 = 0; e2 < 4; e2++) {
+                            const int r = 16 * mt + gq + 8 * (e2 >> 1), col = 8 * nt + 2 * tq + (e2 & 1);
+                            reinterpret_cast<float*>(&bf.G[col][r >> 1])[r & 1] = acc[nt][e2];
+                        }
+                }
+                __syncwarp();
+                // ---- the recurrence (decisions = the forward's fp32 sequence)
+                for (int j = 0; j < kBwdBuf; j++) {
+                    float2 w = make_float2(0.0f, 0.0f), dal = make_float2(0.0f, 0.0f);
+                    if (j < cnt) {
+                        const float4 G0 = bf.g[j], H0 = bf.h[j];
+                        const float2 q = quad_q(G0, H0.x, pxf, py2);
+                        const float2 qm = make_float2((__float_as_uint(H0.z) & actA) ? q.x : kInf,
+                                                      (__float_as_uint(H0.w) & actB) ? q.y : kInf);
+                        const float2 ee = exp_det2(mul2(bc2(-0.5f), q));
+                        const float2 ae = mul2(bc2(H0.y), ee);
+                        const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
+                        const float2 om = sub2(bc2(1.0f), a);
+                        const float2 Tn = mul2(T, om);
+                        const bool okA = qm.x <= qmax && a.x >= amin, okB = qm.y <= qmax && a.y >= amin;
+                        const bool tA = okA && Tn.x >= teps, tB = okB && Tn.y >= teps;
+                        if (okA && !tA) actA = 0u;
+                        if (okB && !tB) actB = 0u;
+                        const float2 gg = bf.G[j][lane];
+                        w = make_float2(tA ? fmul(a.x, T.x) : 0.0f, tB ? fmul(a.y, T.y) : 0.0f);
+                        if (pass == 0) {
+                            S = make_float2(ffma(w.x, gg.x, S.x), ffma(w.y, gg.y, S.y));
+                        } else {
+                            Sup = make_float2(ffma(w.x, gg.x, Sup.x), ffma(w.y, gg.y, Sup.y));
+                            // dL/dalpha' (R25) = T g - (S - Sup) / (1 - alpha') + G_A T_end / (1 - alpha'),
+                            // per pixel, scaled by gsc like g and S; dL/dalpha = dL/dalpha' e unless clamped
+                            auto dpix = [&](bool t, float Tp, float g1, float Sp, float Su, float o, float e1, float ae1,
+                                            float ga1, float Te) {
+                                if (!t || ae1 > amax) return 0.0f;
+                                const float dad = ffma(Tp, g1, fmul(fsub(fmul(ga1, Te), fsub(Sp, Su)), rcp_approx(o)));
+                                return fmul(dad, e1);
+                            };
+                            dal = make_float2(dpix(tA, T.x, gg.x, S.x, Sup.x, om.x, ee.x, ae.x, ga2.x, Tend.x),
+                                              dpix(tB, T.y, gg.y, S.y, Sup.y, om.y, ee.y, ae.y, ga2.y, Tend.y));
+                        }
+                        T = make_float2(tA ? Tn.x : T.x, tB ? Tn.y : T.y);
+                    }
+                    if (pass == 1) {                       // rows j >= cnt are written as zeros
+                        const float2 ws = make_float2(w.x * 2048.0f, w.y * 2048.0f);
+                        const __half2 wh = __floats2half2_rn(ws.x, ws.y);
+                        const float2 whf = __half22float2(wh);
+                        bf.w[0][j][li] = h2u(wh);
+                        bf.w[1][j][li] = h2u(__floats2half2_rn(ws.x - whf.x, ws.y - whf.y));
+                        const __nv_bfloat162 lh = __floats2bfloat162_rn(dal.x, dal.y);
+                        const float2 lhf = __bfloat1622float2(lh);
+                        bf.da[0][j][li] = b2u(lh);
+                        bf.da[1][j][li] = b2u(__floats2bfloat162_rn(dal.x - lhf.x, dal.y - lhf.y));
+                    }
+                }
+                __syncwarp();
+                if (pass == 0) continue;
+                // ---- dL/df = W^T . GF: rows = entries, cols = channels
+#pragma unroll
+                for (int np = 0; np < C / 16; np++) {
+                    float acc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+#pragma unroll
+                    for (int ks = 0; ks < 4; ks++) {
+                        uint32_t ah[4], al[4], bh[4], bl[4];
+                        ldsm_x4(w_a + (uint32_t)(32 * ks), ah[0], ah[1], ah[2], ah[3]);
+                        ldsm_x4(w_a + (uint32_t)(32 * ks) + kWLo, al[0], al[1], al[2], al[3]);
+                        const uint32_t bb = gf_bt + (uint32_t)((16 * ks * PH + 16 * np) * 2);
+                        ldsm_x4_t(bb, bh[0], bh[1], bh[2], bh[3]);
+                        ldsm_x4_t(bb + kGfLo, bl[0], bl[1], bl[2], bl[3]);
+#pragma unroll
+                        for (int nt = 0; nt < 2; nt++) {
+                            hmma16816(acc[nt], ah, bh[2 * nt], bh[2 * nt + 1]);
+                            hmma16816(acc[nt], ah, bl[2 * nt], bl[2 * nt + 1]);
+                            hmma16816(acc[nt], al, bh[2 * nt], bh[2 * nt + 1]);
+                        }
+                    }
+                    const float sc = igsc * (1.0f / 2048.0f);
+#pragma unroll
+                    for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+                        for (int e2 = 0; e2 < 4; e2++) {
+                            const int row = gq + 8 * (e2 >> 1), c = 16 * np + 8 * nt + 2 * tq + (e2 & 1);
+                            if (row < cnt) atomicAdd(d_feat + (size_t)bf.id[row] * C + c, acc[nt][e2] * sc);
+                        }
+                }
+                // ---- moments: DA^T . U
+                {
+                    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                    for (int ks = 0; ks < 4; ks++) {
+                        uint32_t ah[4], al[4];
+                        ldsm_x4(da_a + (uint32_t)(32 * ks), ah[0], ah[1], ah[2], ah[3]);
+                        ldsm_x4(da_a + (uint32_t)(32 * ks) + kWLo, al[0], al[1], al[2], al[3]);
+                        bmma16816(acc, ah, ub[ks][0], ub[ks][1]);
+                        bmma16816(acc, al, ub[ks][0], ub[ks][1]);
+                    }
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; e2++) bf.mom[gq + 8 * (e2 >> 1)][2 * tq + (e2 & 1)] = acc[e2];
+                }
+                __syncwarp();
+                if (li < cnt) {                            // one lane per entry: the scalar gradients
+                    const float4 G0 = bf.g[li];
+                    const float cc = bf.h[li].x;
+                    const float* m = bf.mom[li];
+                    const float mxl = G0.x - (float)bx0, myl = G0.y - (float)by0;
+                    const float M0 = m[0], Mx = m[1], My = m[2], Mxx = m[3], Mxy = m[4], Myy = m[5];
+                    const float k = -0.5f * bf.h[li].y * igsc;   // dL/dq = -alpha / 2 * dL/dalpha
+                    const float Sdx = k * (Mx - mxl * M0), Sdy = k * (My - myl * M0);
+                    const float Sdxx = k * (Mxx - 2.0f * mxl * Mx + mxl * mxl * M0);
+                    const float Sdxy = k * (Mxy - mxl * My - myl * Mx + mxl * myl * M0);
+                    const float Sdyy = k * (Myy - 2.0f * myl * My + myl * myl * M0);
+                    const uint32_t gi = bf.id[li];
+                    atomicAdd(d_alpha + gi, M0 * igsc);
+                    atomicAdd(d_conic + 3 * (size_t)gi + 0, Sdxx);
+                    atomicAdd(d_conic + 3 * (size_t)gi + 1, Sdxy);
+                    atomicAdd(d_conic + 3 * (size_t)gi + 2, Sdyy);
+                    atomicAdd(d_mean2 + 2 * (size_t)gi + 0, -(2.0f * G0.z * Sdx + G0.w * Sdy));
+                    atomicAdd(d_mean2 + 2 * (size_t)gi + 1, -(G0.w * Sdx + 2.0f * cc * Sdy));
+                }
+                __syncwarp();
+            }
+            if (pass == 0) Tend = T;
+        }
+    }
+}
+
+template <int C>
+static cudaError_t launch_bwd_tc(int tiles, const uint4* rec, const void* feat, const uint32_t* tlist, const uint2* trng,
+                                 const uint32_t* order, CompositeGeom cg, RasterConsts rc, CallState* cs,
                                  uint64_t list_cap, const float* GF, const float* GA, float* d_mean2, float* d_conic,
                                  float* d_alpha, float* d_feat, cudaStream_t st) {
+    const size_t smem = sizeof(BwdBuf<C>);
+    static int resident = 0;
+    if (resident == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_composite_bwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_bwd_tc<C>, 32, smem);
+        resident = std::max(1, sms * std::max(1, per_sm));
+    }
+    cudaError_t e = cudaMemsetAsync(&cs->scan_counter[7], 0, 4, st);
+    if (e != cudaSuccess) return e;
+    k_composite_bwd_tc<C><<<std::min(4 * tiles, resident), 32, smem, st>>>(
+        rec, static_cast<const __half*>(feat), tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2, d_conic,
+        d_alpha, d_feat);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const uint4* rec, const void* feat, const uint32_t* tlist,
+                                 const uint2* trng, const uint32_t* order, CompositeGeom cg, RasterConsts rc,
+                                 CallState* cs, uint64_t list_cap, const float* GF, const float* GA, float* d_mean2,
+                                 float* d_conic, float* d_alpha, float* d_feat, cudaStream_t st) {
     const size_t smem = (size_t)kBwdBatch * (16 + 16 + 4 + 4 * (size_t)C);
     k_bwd_zero<<<1184, 256, 0, st>>>(cs, C, d_mean2, d_conic, d_alpha, d_feat);
+    if (fbytes == 2 && tiles > 0 && !getenv("TA_BWD_SIMT")) {
+        switch (C) {
+            case 16: return launch_bwd_tc<16>(tiles, rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
+                                              d_conic, d_alpha, d_feat, st);
+            case 32: return launch_bwd_tc<32>(tiles, rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
+                                              d_conic, d_alpha, d_feat, st);
+            case 64: return launch_bwd_tc<64>(tiles, rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
+                                              d_conic, d_alpha, d_feat, st);
+            default: break;
+        }
+    }
 #define TA_BWD(CC)                                                                                                      \
     case CC: {                                                                                                          \
         if (fbytes == 2) {                                                                                              \

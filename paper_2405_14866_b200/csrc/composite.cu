@@ -16,6 +16,7 @@
 #include <type_traits>
 #include "common.cuh"
 #include "internal.h"
+#include "tc_dev.cuh"
 
 namespace ta {
 
@@ -89,58 +90,6 @@ __device__ __forceinline__ bool ellipse_may_touch(float mx, float my, float ca, 
     return best <= qlim;
 }
 
-// Packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): each component is one IEEE fp32
-// operation rounded to nearest -- the same result as the scalar __f*_rn sequence, two pixels per
-// instruction.
-typedef unsigned long long u64x;
-__device__ __forceinline__ u64x pk2(float2 a) { return *reinterpret_cast<const u64x*>(&a); }
-__device__ __forceinline__ float2 up2(u64x a) { return *reinterpret_cast<const float2*>(&a); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-    u64x r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
-    return up2(r);
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    u64x r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
-    return up2(r);
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-    u64x r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
-    return up2(r);
-}
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-    u64x r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
-    return up2(r);
-}
-__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
-
-// exp_det (R13) of two arguments at once; identical per component to exp_det() for
-// x >= -80 (the only arguments whose results are used: x = -q/2 with q <= q_max).
-__device__ __forceinline__ float2 exp_det2(float2 x) {
-    // k = the integer nearest (ties to even) to the exact product x*log2e, with one rounding:
-    // fma(x, log2e, 1.5*2^23) lands on that integer (|x*log2e| < 2^22), the difference recovers it as
-    // a float and the low mantissa bits hold it as an integer.  (Written as one fma on purpose: ptxas
-    // contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2, so a separate product is not expressible.)
-    constexpr float kMagic = 12582912.0f;                  // 1.5 * 2^23
-    const float2 t = fma2(x, bc2(1.44269502162933349609375f), bc2(kMagic));
-    const float2 k = sub2(t, bc2(kMagic));
-    const float2 nk = make_float2(-k.x, -k.y);
-    const float2 r = fma2(nk, bc2(0.693147182464599609375f), x);
-    float2 p = bc2(1.3814548728987575e-3f);
-    p = fma2(p, r, bc2(8.36869515478611e-3f));
-    p = fma2(p, r, bc2(4.166838899254799e-2f));
-    p = fma2(p, r, bc2(1.666652113199234e-1f));
-    p = fma2(p, r, bc2(4.999999403953552e-1f));
-    p = fma2(p, r, bc2(1.0f));
-    p = fma2(p, r, bc2(1.0f));
-    const int kx = __float_as_int(t.x) - 0x4b400000, ky = __float_as_int(t.y) - 0x4b400000;
-    const float2 s = make_float2(__int_as_float((kx + 127) << 23), __int_as_float((ky + 127) << 23));
-    return mul2(p, s);
-}
-
 constexpr int kWarps = 4;                        // warps per CTA = 8x8-pixel blocks of the 16x16 tile
 constexpr int kThreads = 32 * kWarps;
 constexpr int kBuf = 64;                         // entries staged per warp at a time
@@ -153,18 +102,6 @@ struct WarpBuf {
     uint2 bm[kBuf];                    // lanes whose pixel A / pixel B lies inside the pixel box
     float f[kBuf][CP];
 };
-
-// Lanes of an 8x8 block (lane l: column l&7, row l>>3 (+4 for pixel B)) whose pixel lies inside the
-// box [gx0,gx1]x[gy0,gy1]; computed once per staged entry instead of once per pixel.
-__device__ __forceinline__ uint32_t box_lane_mask(int gx0, int gx1, int gy0, int gy1, int bx0, int ry) {
-    const int cx0 = max(gx0 - bx0, 0), cx1 = min(gx1 - bx0, 7);
-    const int ry0 = max(gy0 - ry, 0), ry1 = min(gy1 - ry, 3);
-    if (cx0 > cx1 || ry0 > ry1) return 0u;
-    const uint32_t col = (0xffu >> (7 - cx1)) & (0xffu << cx0);
-    const int span = 8 * (ry1 - ry0 + 1);
-    const uint32_t rows = (span >= 32 ? 0xffffffffu : ((1u << span) - 1u)) << (8 * ry0);
-    return rows & (col * 0x01010101u);
-}
 
 // One CTA per 16x16 tile; warp w owns the 8x8 block (8*(w&1), 8*(w>>1)); lane l owns the two pixels
 // (l&7, l>>3) and (l&7, (l>>3)+4) of its block (same column: dx is shared, the rest is computed
@@ -525,70 +462,6 @@ struct TcBuf {
     __half f[kBuf][PH];                // staged fp16 feature rows
     uint32_t w[2][16][WP];             // [hi|lo][k][lane]: half2 (w(pixel A), w(pixel B)) of staged entry j0+k
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr) : "memory");
-}
-__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr) : "memory");
-}
-__device__ __forceinline__ void hmma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// Conservative "may the ellipse q <= qlim reach the pixel rectangle [X0,X1] x [Y0,Y1]" test.  For a
-// centre outside the rectangle the minimum of the convex q over it lies on an edge facing the centre
-// (at a minimiser on x = X0 the gradient 2 C d has no y part, so d_x = (g_x / 2) Sigma_xx >= 0, i.e.
-// mx <= X0; likewise for the other edges), so only those (at most one vertical and one horizontal)
-// are evaluated, each at the clamped minimiser along it.  The approximate reciprocal only moves the
-// evaluation point by ~1e-7 relative (q error second order); qlim carries a 1.6 % + 0.01 margin.
-// Nearly degenerate conics (condition > 4096) are never culled (the per-pixel test decides).
-__device__ __forceinline__ bool ellipse_may_touch2(float mx, float my, float ca, float cb2, float cc, float X0,
-                                                   float X1, float Y0, float Y1, float qlim) {
-    const float lx = X0 - mx, hx = X1 - mx, ly = Y0 - my, hy = Y1 - my;
-    const bool vx = lx > 0.0f || hx < 0.0f, vy = ly > 0.0f || hy < 0.0f;
-    if (!vx && !vy) return true;                       // centre inside
-    const float cb = 0.5f * cb2;
-    if (!(fmaf(-cb, cb, ca * cc) * 4096.0f > ca * cc)) return true;
-    float best = 3.0e38f;
-    if (vx) {
-        const float dx = lx > 0.0f ? lx : hx;
-        const float dy = fminf(fmaxf(-cb * dx * rcp_approx(cc), ly), hy);
-        best = dx * (ca * dx + cb2 * dy) + cc * dy * dy;
-    }
-    if (vy) {
-        const float ey = ly > 0.0f ? ly : hy;
-        const float ex = fminf(fmaxf(-cb * ey * rcp_approx(ca), lx), hx);
-        best = fminf(best, ex * (ca * ex + cb2 * ey) + cc * ey * ey);
-    }
-    return best <= qlim;
-}
-
-constexpr float kInf = __builtin_huge_valf();
-
-// q = fma(fma(ca, dx, cb2*dy), dx, (cc*dy)*dy) for the lane's two pixels (normative a6 sequence)
-__device__ __forceinline__ float2 quad_q(const float4 G, float cc, float pxf, float2 py2) {
-    const float dx = fsub(pxf, G.x);
-    const float2 dy = sub2(py2, bc2(G.y));
-    const float2 t1 = mul2(bc2(G.w), dy);
-    const float2 t2 = fma2(bc2(G.z), bc2(dx), t1);
-    const float2 t4 = mul2(mul2(bc2(cc), dy), dy);
-    return fma2(t2, bc2(dx), t4);
-}
 
 // One compositing step of the normative a6 recurrence for the lane's two pixels.  qm = q (or +inf if
 // the pixel is outside the box / already stopped), a = alpha'.  Returns the weight 2^11 alpha' T of

@@ -91,9 +91,9 @@ cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, con
                              int32_t* ncontrib, cudaStream_t st);
 // backward.cu
 cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const uint4* rec, const void* feat, const uint32_t* tlist,
-                                 const uint2* trng, CompositeGeom cg, RasterConsts rc, const CallState* cs,
-                                 uint64_t list_cap, const float* GF, const float* GA, float* d_mean2, float* d_conic,
-                                 float* d_alpha, float* d_feat, cudaStream_t st);
+                                 const uint2* trng, const uint32_t* order, CompositeGeom cg, RasterConsts rc,
+                                 CallState* cs, uint64_t list_cap, const float* GF, const float* GA, float* d_mean2,
+                                 float* d_conic, float* d_alpha, float* d_feat, cudaStream_t st);
 // debug: compact the per-tile (tile, depth, id) lists the compositor walks into one array (a3/a5 check)
 void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, CompositeGeom cg, uint32_t* tile_offs,
                              unsigned long long* status, uint32_t* counter, unsigned long long* total, uint32_t* out_list,

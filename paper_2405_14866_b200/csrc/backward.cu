@@ -273,9 +273,11 @@ struct BwdBuf {
     uint32_t id[kBwdBuf];              // array index
     __half f[kBwdBuf][PH];             // staged fp16 feature rows
     __half gf[2][64][PH];              // scaled GF, fp16 hi / lo, row p' = 2 lane + (0: pixel A, 1: pixel B)
-    float2 G[kBwdBuf][32];             // scaled g of (entry, lane): (pixel A, pixel B)
     uint32_t w[2][kBwdBuf][WP];        // fp16 hi / lo of 2^11 w, word = lane: (pixel A, pixel B)
-    uint32_t da[2][kBwdBuf][WP];       // bf16 hi / lo of dL/dalpha, word = lane: (pixel A, pixel B)
+    union {
+        float2 G[kBwdBuf][32];         // scaled g of (entry, lane): (pixel A, pixel B), read into registers
+        uint32_t da[2][kBwdBuf][WP];   // then: bf16 hi / lo of dL/dalpha, word = lane: (pixel A, pixel B)
+    };
     float mom[kBwdBuf][8];             // per entry: sum da (1, x, y, xx, xy, yy)
 };
 
@@ -469,7 +471,12 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
                         }
                 }
                 __syncwarp();
+                float2 gv[kBwdBuf];                        // this lane's g of the staged entries
+#pragma unroll
+                for (int j = 0; j < kBwdBuf; j++) gv[j] = bf.G[j][lane];
+                __syncwarp();                              // bf.G is overwritten by bf.da below
                 // ---- the recurrence (decisions = the forward's fp32 sequence)
+#pragma unroll
                 for (int j = 0; j < kBwdBuf; j++) {
                     float2 w = make_float2(0.0f, 0.0f), dal = make_float2(0.0f, 0.0f);
                     if (j < cnt) {
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
                         const bool tA = okA && Tn.x >= teps, tB = okB && Tn.y >= teps;
                         if (okA && !tA) actA = 0u;
                         if (okB && !tB) actB = 0u;
-                        const float2 gg = bf.G[j][lane];
+                        const float2 gg = gv[j];
                         w = make_float2(tA ? fmul(a.x, T.x) : 0.0f, tB ? fmul(a.y, T.y) : 0.0f);
                         if (pass == 0) {
                             S = make_float2(ffma(w.x, gg.x, S.x), ffma(w.y, gg.y, S.y));

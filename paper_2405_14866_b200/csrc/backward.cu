@@ -14,6 +14,7 @@
 // Per entry the 32 pixels of a warp are summed with shuffles and one lane adds them to the global
 // gradient arrays (fp32 atomics: the summation order over warps is not fixed).
 #include <algorithm>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include "common.cuh"
 #include "internal.h"
@@ -475,54 +476,64 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
 #pragma unroll
                 for (int j = 0; j < kBwdBuf; j++) gv[j] = bf.G[j][lane];
                 __syncwarp();                              // bf.G is overwritten by bf.da below
-                // ---- the recurrence (decisions = the forward's fp32 sequence)
+                // ---- the recurrence (decisions = the forward's fp32 sequence).  Full chunks of 16 take a
+                //      branch-free copy so the scheduler can overlap consecutive entries.
+                auto recur = [&](auto full, auto second) {
+                    constexpr bool kFull = decltype(full)::value, kP2 = decltype(second)::value;
 #pragma unroll
-                for (int j = 0; j < kBwdBuf; j++) {
-                    float2 w = make_float2(0.0f, 0.0f), dal = make_float2(0.0f, 0.0f);
-                    if (j < cnt) {
-                        const float4 G0 = bf.g[j], H0 = bf.h[j];
-                        const float2 q = quad_q(G0, H0.x, pxf, py2);
-                        const float2 qm = make_float2((__float_as_uint(H0.z) & actA) ? q.x : kInf,
-                                                      (__float_as_uint(H0.w) & actB) ? q.y : kInf);
-                        const float2 ee = exp_det2(mul2(bc2(-0.5f), q));
-                        const float2 ae = mul2(bc2(H0.y), ee);
-                        const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
-                        const float2 om = sub2(bc2(1.0f), a);
-                        const float2 Tn = mul2(T, om);
-                        const bool okA = qm.x <= qmax && a.x >= amin, okB = qm.y <= qmax && a.y >= amin;
-                        const bool tA = okA && Tn.x >= teps, tB = okB && Tn.y >= teps;
-                        if (okA && !tA) actA = 0u;
-                        if (okB && !tB) actB = 0u;
-                        const float2 gg = gv[j];
-                        w = make_float2(tA ? fmul(a.x, T.x) : 0.0f, tB ? fmul(a.y, T.y) : 0.0f);
-                        if (pass == 0) {
-                            S = make_float2(ffma(w.x, gg.x, S.x), ffma(w.y, gg.y, S.y));
-                        } else {
-                            Sup = make_float2(ffma(w.x, gg.x, Sup.x), ffma(w.y, gg.y, Sup.y));
-                            // dL/dalpha' (R25) = T g - (S - Sup) / (1 - alpha') + G_A T_end / (1 - alpha'),
-                            // per pixel, scaled by gsc like g and S; dL/dalpha = dL/dalpha' e unless clamped
-                            auto dpix = [&](bool t, float Tp, float g1, float Sp, float Su, float o, float e1, float ae1,
-                                            float ga1, float Te) {
-                                if (!t || ae1 > amax) return 0.0f;
-                                const float dad = ffma(Tp, g1, fmul(fsub(fmul(ga1, Te), fsub(Sp, Su)), rcp_approx(o)));
-                                return fmul(dad, e1);
-                            };
-                            dal = make_float2(dpix(tA, T.x, gg.x, S.x, Sup.x, om.x, ee.x, ae.x, ga2.x, Tend.x),
-                                              dpix(tB, T.y, gg.y, S.y, Sup.y, om.y, ee.y, ae.y, ga2.y, Tend.y));
+                    for (int j = 0; j < kBwdBuf; j++) {
+                        float2 w = make_float2(0.0f, 0.0f), dal = make_float2(0.0f, 0.0f);
+                        if (kFull || j < cnt) {
+                            const float4 G0 = bf.g[j], H0 = bf.h[j];
+                            const float2 q = quad_q(G0, H0.x, pxf, py2);
+                            const float2 qm = make_float2((__float_as_uint(H0.z) & actA) ? q.x : kInf,
+                                                          (__float_as_uint(H0.w) & actB) ? q.y : kInf);
+                            const float2 ee = exp_det2(mul2(bc2(-0.5f), q));
+                            const float2 ae = mul2(bc2(H0.y), ee);
+                            const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
+                            const float2 om = sub2(bc2(1.0f), a);
+                            const float2 Tn = mul2(T, om);
+                            const bool okA = qm.x <= qmax && a.x >= amin, okB = qm.y <= qmax && a.y >= amin;
+                            const bool tA = okA && Tn.x >= teps, tB = okB && Tn.y >= teps;
+                            if (okA && !tA) actA = 0u;
+                            if (okB && !tB) actB = 0u;
+                            const float2 gg = gv[j];
+                            w = make_float2(tA ? fmul(a.x, T.x) : 0.0f, tB ? fmul(a.y, T.y) : 0.0f);
+                            if (!kP2) {
+                                S = make_float2(ffma(w.x, gg.x, S.x), ffma(w.y, gg.y, S.y));
+                            } else {
+                                Sup = make_float2(ffma(w.x, gg.x, Sup.x), ffma(w.y, gg.y, Sup.y));
+                                // dL/dalpha' (R25) = T g - (S - Sup) / (1 - alpha') + G_A T_end / (1 - alpha'), per
+                                // pixel, scaled by gsc like g and S; dL/dalpha = dL/dalpha' e unless clamped
+                                const float2 num = sub2(mul2(ga2, Tend), sub2(S, Sup));
+                                const float2 r = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                                const float2 dad = fma2(T, gg, mul2(num, r));
+                                const float2 d = mul2(dad, ee);
+                                dal = make_float2((tA && !(ae.x > amax)) ? d.x : 0.0f, (tB && !(ae.y > amax)) ? d.y : 0.0f);
+                            }
+                            T = make_float2(tA ? Tn.x : T.x, tB ? Tn.y : T.y);
                         }
-                        T = make_float2(tA ? Tn.x : T.x, tB ? Tn.y : T.y);
+                        if (kP2) {                         // rows j >= cnt are written as zeros
+                            const float2 ws = mul2(w, bc2(2048.0f));
+                            const __half2 wh = __floats2half2_rn(ws.x, ws.y);
+                            const float2 whf = __half22float2(wh);
+                            bf.w[0][j][li] = h2u(wh);
+                            bf.w[1][j][li] = h2u(__floats2half2_rn(ws.x - whf.x, ws.y - whf.y));
+                            const __nv_bfloat162 lh = __floats2bfloat162_rn(dal.x, dal.y);
+                            const float2 lhf = __bfloat1622float2(lh);
+                            bf.da[0][j][li] = b2u(lh);
+                            bf.da[1][j][li] = b2u(__floats2bfloat162_rn(dal.x - lhf.x, dal.y - lhf.y));
+                        }
                     }
-                    if (pass == 1) {                       // rows j >= cnt are written as zeros
-                        const float2 ws = make_float2(w.x * 2048.0f, w.y * 2048.0f);
-                        const __half2 wh = __floats2half2_rn(ws.x, ws.y);
-                        const float2 whf = __half22float2(wh);
-                        bf.w[0][j][li] = h2u(wh);
-                        bf.w[1][j][li] = h2u(__floats2half2_rn(ws.x - whf.x, ws.y - whf.y));
-                        const __nv_bfloat162 lh = __floats2bfloat162_rn(dal.x, dal.y);
-                        const float2 lhf = __bfloat1622float2(lh);
-                        bf.da[0][j][li] = b2u(lh);
-                        bf.da[1][j][li] = b2u(__floats2bfloat162_rn(dal.x - lhf.x, dal.y - lhf.y));
-                    }
+                };
+                using T_ = std::true_type;
+                using F_ = std::false_type;
+                if (pass == 0) {
+                    if (cnt == kBwdBuf) recur(T_(), F_());
+                    else recur(F_(), F_());
+                } else {
+                    if (cnt == kBwdBuf) recur(T_(), T_());
+                    else recur(F_(), T_());
                 }
                 __syncwarp();
                 if (pass == 0) continue;

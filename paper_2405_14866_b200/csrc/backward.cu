@@ -5,7 +5,9 @@
 // l.386-387 (the differentiable rasterizer of [kerbl20233d]); reading R25 (decisions held
 // fixed, no gradient through a binding alpha clamp).  It reuses the splat records and the per-tile
 // lists of the preceding ta_rasterize on the same context.
-// One CTA per 16 x 16 tile, one pixel per thread; the tile list is staged 256 entries at a time in
+// Two kernels: k_composite_bwd_tc<C> (fp16-stored features, C in {16, 32, 64}; tensor cores, see the
+// section comment below) and the plain k_composite_bwd (fp32-stored features and C = 8):
+// one CTA per 16 x 16 tile, one pixel per thread; the tile list is staged 256 entries at a time in
 // shared memory (record + fp32 feature row).  Pass 1 replays the forward per pixel (the same fp32
 // decision sequence as the forward kernels, so the composited set is identical) and accumulates
 // S = sum w_j g_j (g_j = G_F . f_j) and T_end; pass 2 replays it again and forms every composited

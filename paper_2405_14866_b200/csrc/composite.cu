@@ -1,17 +1,18 @@
-// composite.cu -- a6 front-to-back compositing of the C-channel latent feature (sm_100a).
+// composite.cu -- a6 front-to-back compositing of the C-channel latent feature (sm_100a), and the
+// tile split that feeds it.
 //
-// One CTA per 16x16 tile, one pixel per thread; warp w owns the 8x4 pixel block
-// (8*(w&1), 4*(w>>1)) of the tile.
-// The tile's (depth, id)-ordered list is consumed in batches of kBatch Gaussians staged in
-// shared memory (splat record + feature row converted once to fp32, padded rows so the
-// 128-bit staging stores are conflict-free).  While staging, every entry gets two 8-bit warp
-// masks: "may touch" (pixel box overlaps the warp's block AND a conservative minimum of q over
-// the block is <= 9) and "block inside the pixel box" (per-pixel box test skipped); each warp
-// then walks only its entries (ballot + ffs).  Accumulation uses packed FFMA2 (fma.rn.f32x2).  Transmittance T,
-// the decisions (box, q <= 9, alpha' >= 1/255, T*(1-alpha') < 1e-4) and A = 1 - T follow the
-// normative fp32 sequence (DESIGN.md a6) bit for bit; the C accumulators are fp32 FMAs.
-// Warps retire when all their pixels stopped (__all_sync); the CTA leaves the list as soon
-// as every pixel stopped (__syncthreads_count).
+//   k_tile_split<NQ>   coarse (bin, depth, id) lists -> per-tile lists (tile q of bin b at
+//                      NQ * start_b + q * len_b), trng[tile] = (start, count)
+//   k_tile_order       heaviest-first order of the tiles (by list length)
+//   k_composite_tc<C>  fp16-stored features: persistent warps, each pulling 8x8 pixel blocks (tile
+//                      quadrants) from a per-call counter; lane l owns pixels (l&7, l>>3) and
+//                      (l&7, (l>>3)+4).  The warp walks its tile's list, stages the entries whose
+//                      ellipse can reach its still-active pixels (splat record + fp16 feature row by
+//                      cp.async), runs the normative fp32 recurrence with packed fp32x2 instructions
+//                      (T, alpha', the decisions and A bit-exact) and accumulates F on the tensor
+//                      cores (mma.sync m16n8k16, fp16 hi/lo weights x fp16 features, fp32 accumulate).
+//   k_composite<C, float>  fp32-stored features: the same recurrence, all-SIMT packed FFMA2
+//                      accumulation, one CTA per tile.
 #include <algorithm>
 #include <type_traits>
 #include "common.cuh"
@@ -106,10 +107,10 @@ struct WarpBuf {
 // One CTA per 16x16 tile; warp w owns the 8x8 block (8*(w&1), 8*(w>>1)); lane l owns the two pixels
 // (l&7, l>>3) and (l&7, (l>>3)+4) of its block (same column: dx is shared, the rest is computed
 // for both pixels with packed fp32x2 instructions).  Warps are fully independent (no barrier):
-// each walks the tile's coarse (32x32-bin) list in depth order, keeps the entries whose tile box
-// covers this tile (= the tile's (tile, depth, id) list) and whose ellipse can reach its block
-// (conservative), stages up to 32 of them in a warp-private shared buffer (splat record + fp32
-// feature row) and composites them; the 4 warps of a tile share the list reads through L1.
+// each walks the tile's (tile, depth, id) list (k_tile_split), keeps the entries whose ellipse can
+// reach its still-active pixels (conservative), stages them in a warp-private shared buffer (splat
+// record + fp32 feature row) and composites them; the 4 warps of a tile share the list reads
+// through L1.
 template <int C, typename FT, bool kCounts>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const uint32_t* __restrict__ clist,

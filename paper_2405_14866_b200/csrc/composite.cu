@@ -14,6 +14,7 @@
 //   k_composite<C, float>  fp32-stored features: the same recurrence, all-SIMT packed FFMA2
 //                      accumulation, one CTA per tile.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include "common.cuh"
 #include "internal.h"
@@ -908,6 +909,7 @@ static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, cons
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false>, kThreads, smem);
+        if (const char* e = getenv("TA_TC_CTAS_PER_SM")) per_sm = std::min(per_sm, atoi(e));   // tuning knob
         resident = std::max(1, sms * std::max(1, per_sm));
     }
     const int grid = std::min(tiles, resident);

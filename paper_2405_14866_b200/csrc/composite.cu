@@ -453,16 +453,31 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ t
 // fp16 subnormals and is removed exactly at the end.  Products are exact and the MMA accumulates
 // in fp32, so F matches the oracle's sequential fp32 sum to ~1e-6 (tolerance 1e-4, R22).
 
+#ifndef TA_TC_NB
+#define TA_TC_NB 64
+#endif
+template <int N>
+struct SAcc {
+    float4 v[N][32];
+};
+template <>
+struct SAcc<0> {};
+
 template <int C>
 struct TcBuf {
     // fp16 feature row pitch (halves): an odd number of 16-B chunks, so the 8 rows one ldmatrix
     // phase reads fall into 8 different 16-B bank groups
     static constexpr int PH = (((C + 8) / 8) & 1) ? C + 8 : C + 16;
     static constexpr int WP = 36;      // weight row pitch (32-bit words): 144 B, odd number of 16-B chunks
-    float4 g[kBuf];                    // mx, my, ca, cb2
-    float4 h[kBuf];                    // cc, alpha, box lane mask (pixel A), box lane mask (pixel B)
-    __half f[kBuf][PH];                // staged fp16 feature rows
+    // C = 64: the accumulators of channels 32..63 live in shared memory (lane-private float4 slots)
+    // and 32 entries are staged at a time, so 3 CTAs fit per SM instead of 2 (registers / smem)
+    static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : NT, NTS = NT - NTR;
+    static constexpr int NB = C >= 64 ? 32 : TA_TC_NB;   // entries staged per warp at a time
+    float4 g[NB];                      // mx, my, ca, cb2
+    float4 h[NB];                      // cc, alpha, box lane mask (pixel A), box lane mask (pixel B)
+    __half f[NB][PH];                  // staged fp16 feature rows
     uint32_t w[2][16][WP];             // [hi|lo][k][lane]: half2 (w(pixel A), w(pixel B)) of staged entry j0+k
+    SAcc<4 * NTS> sacc;                // [mt * NTS + nt - NTR][lane] (C = 64 only)
 };
 
 // One compositing step of the normative a6 recurrence for the lane's two pixels.  qm = q (or +inf if
@@ -497,7 +512,7 @@ constexpr bool kSkipEmptyPairs = false;
 constexpr int kTcMinBlocks = TA_TC_MIN_BLOCKS;   // CTAs per SM the register budget targets
 
 template <int C, bool kCounts>
-__global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : kTcMinBlocks))
+__global__ void __launch_bounds__(kThreads, (C >= 64 ? 3 : kTcMinBlocks))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
                const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
                const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
@@ -505,6 +520,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     constexpr int NT = C / 8;                 // n-tiles of 8 channels
     constexpr int PH = TcBuf<C>::PH;
     constexpr int WP = TcBuf<C>::WP;
+    constexpr int NB = TcBuf<C>::NB, NTR = TcBuf<C>::NTR, NTS = TcBuf<C>::NTS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     TcBuf<C>& bf = reinterpret_cast<TcBuf<C>*>(smem_raw)[warp];
@@ -547,13 +563,17 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         const uint32_t b_base = smem_u32(&bf.f[0][0]) + (uint32_t)((li >> 4) * 16);
         uint32_t* const wst = &bf.w[0][0][li];    // this lane's word in weight row 0 (hi)
 
-        float acc[4][NT][4];
-    #pragma unroll
+        float acc[4][NTR][4];
+#pragma unroll
         for (int mt = 0; mt < 4; mt++)
-    #pragma unroll
-            for (int nt = 0; nt < NT; nt++)
-    #pragma unroll
+#pragma unroll
+            for (int nt = 0; nt < NTR; nt++)
+#pragma unroll
                 for (int e = 0; e < 4; e++) acc[mt][nt][e] = 0.0f;
+        if constexpr (NTS > 0) {
+#pragma unroll
+            for (int k = 0; k < 4 * NTS; k++) bf.sacc.v[k][li] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
         float2 T = make_float2(1.0f, 1.0f);
         int ncA = 0, ncB = 0;
         // active-pixel lane bits: the lane's bit while its pixel still composites, else 0
@@ -591,16 +611,16 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
             const int ay0 = __reduce_min_sync(0xffffffffu, ly0);
             const int ay1 = __reduce_max_sync(0xffffffffu, ly1);
             const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
-            // ---- fill: up to kBuf entries of this warp, in list order; 64 list entries per round trip.
+            // ---- fill: up to NB entries of this warp, in list order; 64 list entries per round trip.
             //      The list indices of the next 64 entries are loaded one round ahead (pf_pos / pf).
             int cnt = 0;
-            while (cnt < kBuf && pos < cend) {
+            while (cnt < NB && pos < cend) {
                 uint32_t idx[2];
                 if (pf_pos == pos) {
                     idx[0] = pf[0];
                     idx[1] = pf[1];
                 } else {
-    #pragma unroll
+#pragma unroll
                     for (int hh = 0; hh < 2; hh++) {
                         const uint32_t e = pos + 32 * hh + lane;
                         idx[hh] = e < cend ? clist[e] : 0xffffffffu;
@@ -608,21 +628,21 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 }
                 uint4 r0[2], r1[2];
                 bool keep[2];
-    #pragma unroll
+#pragma unroll
                 for (int hh = 0; hh < 2; hh++) {
                     const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
                     r1[hh] = rec[2 * i + 1];
                     r0[hh] = rec[2 * i];
                 }
                 pf_pos = pos + 64;
-    #pragma unroll
+#pragma unroll
                 for (int hh = 0; hh < 2; hh++) {
                     const uint32_t e = pf_pos + 32 * hh + lane;
                     pf[hh] = e < cend ? clist[e] : 0xffffffffu;
                 }
                 // The warp's block lies inside the tile, so "box overlaps the active rectangle" implies
                 // "box covers the tile": the per-tile list filter is implied (lists hold visible Gaussians only).
-    #pragma unroll
+#pragma unroll
                 for (int hh = 0; hh < 2; hh++) {
                     const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
                     const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
@@ -632,14 +652,14 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                                                   __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
                 }
                 uint32_t adv = 0;
-    #pragma unroll
+#pragma unroll
                 for (int hh = 0; hh < 2; hh++) {
-                    if (cnt >= kBuf) break;
+                    if (cnt >= NB) break;
                     const uint32_t base = pos + 32 * hh;
                     if (base >= cend) break;
                     bool kp = keep[hh];
                     uint32_t bal = __ballot_sync(0xffffffffu, kp);
-                    const int room = kBuf - cnt;
+                    const int room = NB - cnt;
                     const uint32_t rank = __popc(bal & lt);
                     uint32_t step = min(32u, cend - base);
                     if (__popc(bal) > room) {
@@ -660,7 +680,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                                               __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
                         const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
                         const uint32_t dst = smem_u32(&bf.f[d][0]);
-    #pragma unroll
+#pragma unroll
                         for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
                     }
                     cnt += __popc(bal);
@@ -709,7 +729,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 if (modeB) {
                     const float cpxf = (float)cpx, cpyf = (float)cpy;
                     __half* const wh = reinterpret_cast<__half*>(&bf.w[0][0][0]) + 2 * ol + hs;   // column p', row 0 (hi)
-    #pragma unroll 2
+#pragma unroll 2
                     for (int jj = 0; jj < 16; jj += 2) {
                         float w0 = 0.0f, w1 = 0.0f;
                         if (jj < nk) {
@@ -769,7 +789,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                     // scheduler can overlap consecutive pairs; the last, partial chunk keeps the guards
                     auto pairs = [&](auto full) {
                         constexpr bool kFull = decltype(full)::value;
-    #pragma unroll
+#pragma unroll
                         for (int jj = 0; jj < 16; jj += 2) {
                             float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
                             if (kFull || jj < nk) {                          // warp-uniform
@@ -824,20 +844,31 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                     if constexpr (NT == 1) {
                         ldsm_x2_t(rb, bfr[0][0], bfr[0][1]);
                     } else {
-    #pragma unroll
+#pragma unroll
                         for (int np = 0; np < NT / 2; np++)
                             ldsm_x4_t(rb + np * 32, bfr[2 * np][0], bfr[2 * np][1], bfr[2 * np + 1][0], bfr[2 * np + 1][1]);
                     }
                 }
-    #pragma unroll
+#pragma unroll
                 for (int mt = 0; mt < 4; mt++) {
                     uint32_t ah[4], al[4];
                     ldsm_x4_t(a_base + mt * 32, ah[0], ah[1], ah[2], ah[3]);
                     ldsm_x4_t(a_base + mt * 32 + kLoOff, al[0], al[1], al[2], al[3]);
-    #pragma unroll
-                    for (int nt = 0; nt < NT; nt++) {
+#pragma unroll
+                    for (int nt = 0; nt < NTR; nt++) {
                         hmma16816(acc[mt][nt], ah, bfr[nt][0], bfr[nt][1]);
                         hmma16816(acc[mt][nt], al, bfr[nt][0], bfr[nt][1]);
+                    }
+                    if constexpr (NTS > 0) {
+#pragma unroll
+                        for (int nt = NTR; nt < NT; nt++) {        // C = 64: accumulators in shared memory
+                            float4& slot = bf.sacc.v[mt * NTS + nt - NTR][li];
+                            const float4 v = slot;
+                            float d[4] = {v.x, v.y, v.z, v.w};
+                            hmma16816(d, ah, bfr[nt][0], bfr[nt][1]);
+                            hmma16816(d, al, bfr[nt][0], bfr[nt][1]);
+                            slot = make_float4(d[0], d[1], d[2], d[3]);
+                        }
                     }
                 }
                 __syncwarp();
@@ -849,28 +880,36 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         if (kCounts && lane == 0) {
             unsigned long long* work = const_cast<CallState*>(cs)->work;
             wk[6] = 1;
-    #pragma unroll
+#pragma unroll
             for (int k = 0; k < 8; k++) atomicAdd(&work[k], wk[k]);
         }
         // accumulator (mt, row r in 0..15) <-> pixel p' = 16 mt + r = 2 l' + h: lane l' = 8 mt + (r >> 1), pixel A/B = r & 1
         const int g = li >> 2, t = li & 3;
-    #pragma unroll
+#pragma unroll
         for (int mt = 0; mt < 4; mt++) {
-    #pragma unroll
+#pragma unroll
             for (int half = 0; half < 2; half++) {
                 const int r = g + 8 * half;
                 const int l2 = 8 * mt + (r >> 1);
                 const int ox = bx0 + (l2 & 7), oy = by0 + (l2 >> 3) + 4 * (r & 1);
                 if (ox < W && oy < H) {
                     float* out = Fout + ((size_t)oy * W + ox) * C + 2 * t;
-    #pragma unroll
-                    for (int nt = 0; nt < NT; nt++)
+#pragma unroll
+                    for (int nt = 0; nt < NTR; nt++)
                         *reinterpret_cast<float2*>(out + 8 * nt) =
                             make_float2(acc[mt][nt][2 * half] * (1.0f / 2048.0f), acc[mt][nt][2 * half + 1] * (1.0f / 2048.0f));
+                    if constexpr (NTS > 0) {
+#pragma unroll
+                        for (int nt = NTR; nt < NT; nt++) {
+                            const float4 v = bf.sacc.v[mt * NTS + nt - NTR][li];
+                            *reinterpret_cast<float2*>(out + 8 * nt) =
+                                make_float2((half ? v.z : v.x) * (1.0f / 2048.0f), (half ? v.w : v.y) * (1.0f / 2048.0f));
+                        }
+                    }
                 }
             }
         }
-    #pragma unroll
+#pragma unroll
         for (int hh = 0; hh < 2; hh++) {
             const int py = hh ? pyB : pyA;
             if (px < W && py < H && !(hh ? movedB : movedA)) {        // moved pixels are written by their new lane

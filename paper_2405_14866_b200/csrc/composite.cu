@@ -473,25 +473,28 @@ struct TcBuf {
     // and 32 entries are staged at a time, so 3 CTAs fit per SM instead of 2 (registers / smem)
     static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : NT, NTS = NT - NTR;
     static constexpr int NB = C >= 64 ? 32 : TA_TC_NB;   // entries staged per warp at a time
-    float4 g[NB];                      // mx, my, ca, cb2
-    float4 h[NB];                      // cc, alpha, box lane mask (pixel A), box lane mask (pixel B)
+    float4 g[NB];                      // mx, my, -ca/2, -cb2/2   (pre-scaled by exact powers of two:
+    float4 h[NB];                      // -cc/2, 2^11 alpha, box lane mask (A), (B)   q' = -q/2, a' = 2^11 alpha')
     __half f[NB][PH];                  // staged fp16 feature rows
     uint32_t w[2][16][WP];             // [hi|lo][k][lane]: half2 (w(pixel A), w(pixel B)) of staged entry j0+k
     SAcc<4 * NTS> sacc;                // [mt * NTS + nt - NTR][lane] (C = 64 only)
 };
 
-// One compositing step of the normative a6 recurrence for the lane's two pixels.  qm = q (or +inf if
-// the pixel is outside the box / already stopped), a = alpha'.  Returns the weight 2^11 alpha' T of
-// each pixel (0 if it does not composite this entry) and advances T / the active bits.
+// One compositing step of the normative a6 recurrence for the lane's two pixels, in the staged
+// scaling: qm = q' = -q/2 (or -inf if the pixel is outside the box / already stopped), a = 2^11
+// alpha'; qlo = -q_max/2, alo = 2^11 alpha_min.  Both scalings are exact (powers of two, no
+// subnormals on the used range), so every decision and T are those of the normative sequence:
+// fma(a, -2^-11, 1) = fl(1 - alpha').  Returns the weight 2^11 alpha' T of each pixel (0 if it does
+// not composite this entry) and advances T / the active bits.
 template <bool kCounts>
-__device__ __forceinline__ float2 tstep(float2 qm, float2 a, float qmax, float amin, float teps, float2& T,
+__device__ __forceinline__ float2 tstep(float2 qm, float2 a, float qlo, float alo, float teps, float2& T,
                                         uint32_t& actA, uint32_t& actB, int& ncA, int& ncB, unsigned long long* wk) {
-    const float2 Tn = mul2(T, sub2(bc2(1.0f), a));
-    const bool okA = qm.x <= qmax && a.x >= amin, okB = qm.y <= qmax && a.y >= amin;
+    const float2 Tn = mul2(T, fma2(a, bc2(-1.0f / 2048.0f), bc2(1.0f)));
+    const bool okA = qm.x >= qlo && a.x >= alo, okB = qm.y >= qlo && a.y >= alo;
     const bool inA = okA && Tn.x >= teps, inB = okB && Tn.y >= teps;
     if (okA && !inA) actA = 0u;           // T would drop below t_eps: stop before this Gaussian (R10)
     if (okB && !inB) actB = 0u;
-    const float2 ws = mul2(mul2(a, bc2(2048.0f)), T);
+    const float2 ws = mul2(a, T);
     const float2 w = make_float2(inA ? ws.x : 0.0f, inB ? ws.y : 0.0f);
     T = make_float2(inA ? Tn.x : T.x, inB ? Tn.y : T.y);
     if (kCounts) {
@@ -549,7 +552,8 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
         const float pxf = (float)px;
         const float2 py2 = make_float2((float)pyA, (float)pyB);
-        const float qmax = rc.q_max, amax = rc.alpha_max, amin = rc.alpha_min, teps = rc.t_eps;
+        const float qmax = rc.q_max, teps = rc.t_eps;
+        const float qlo = -0.5f * qmax, amx = 2048.0f * rc.alpha_max, alo = 2048.0f * rc.alpha_min;
         const float qlim = qmax * 1.015625f + 0.01f;
         const uint32_t lt = lanemask_lt();
 
@@ -674,8 +678,8 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
                         const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
                         bf.g[d] = make_float4(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
-                                              __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w));
-                        bf.h[d] = make_float4(__uint_as_float(r1[hh].x), __uint_as_float(r1[hh].y),
+                                              -0.5f * __uint_as_float(r0[hh].z), -0.5f * __uint_as_float(r0[hh].w));
+                        bf.h[d] = make_float4(-0.5f * __uint_as_float(r1[hh].x), 2048.0f * __uint_as_float(r1[hh].y),
                                               __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
                                               __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
                         const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
@@ -743,32 +747,31 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                             const float2 t1 = mul2(make_float2(G0.w, G1.w), dy);
                             const float2 t2 = fma2(make_float2(G0.z, G1.z), dx, t1);
                             const float2 t4 = mul2(mul2(make_float2(H0.x, H1.x), dy), dy);
-                            const float2 q = fma2(t2, dx, t4);
+                            const float2 q = fma2(t2, dx, t4);     // q' = -q/2 (staged conic is -conic/2)
                             const uint32_t b0 = __float_as_uint(hs ? H0.w : H0.z), b1 = __float_as_uint(hs ? H1.w : H1.z);
-                            const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : kInf;
-                            const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : kInf;
+                            const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : -kInf;
+                            const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : -kInf;
                             if (kCounts) wk[2] += has1 ? 2 : 1;
-                            if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(qm0, qm1) <= qmax)) {
-                                const float2 e = exp_det2(mul2(bc2(-0.5f), q));
-                                const float2 ae = mul2(make_float2(H0.y, H1.y), e);
-                                const float2 a = make_float2(fminf(amax, ae.x), fminf(amax, ae.y));
-                                const float2 om = sub2(bc2(1.0f), a);
-                                const float2 sc = mul2(a, bc2(2048.0f));
+                            if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fmaxf(qm0, qm1) >= qlo)) {
+                                const float2 e = exp_det2(q);
+                                const float2 ae = mul2(make_float2(H0.y, H1.y), e);             // 2^11 alpha e
+                                const float2 a = make_float2(fminf(amx, ae.x), fminf(amx, ae.y)); // 2^11 alpha'
+                                const float2 om = fma2(a, bc2(-1.0f / 2048.0f), bc2(1.0f));      // fl(1 - alpha')
                                 {
                                     const float Tn = fmul(T1, om.x);
-                                    const bool ok = qm0 <= qmax && a.x >= amin;
+                                    const bool ok = qm0 >= qlo && a.x >= alo;
                                     const bool in = ok && Tn >= teps;
                                     if (ok && !in) act1 = 0u;
-                                    w0 = in ? fmul(sc.x, T1) : 0.0f;
+                                    w0 = in ? fmul(a.x, T1) : 0.0f;
                                     T1 = in ? Tn : T1;
                                     if (kCounts) nc1 += in ? 1 : 0;
                                 }
                                 {
                                     const float Tn = fmul(T1, om.y);
-                                    const bool ok = act1 && qm1 <= qmax && a.y >= amin;
+                                    const bool ok = act1 && qm1 >= qlo && a.y >= alo;
                                     const bool in = ok && Tn >= teps;
                                     if (ok && !in) act1 = 0u;
-                                    w1 = in ? fmul(sc.y, T1) : 0.0f;
+                                    w1 = in ? fmul(a.y, T1) : 0.0f;
                                     T1 = in ? Tn : T1;
                                     if (kCounts) nc1 += in ? 1 : 0;
                                 }
@@ -796,30 +799,31 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                                 const int j1 = j0 + jj + ((kFull || jj + 1 < nk) ? 1 : 0);
                                 const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
                                 const float4 G1 = bf.g[j1], H1 = bf.h[j1];
-                                // q of both entries for both pixels; qm = q where the pixel is in the entry's box and
-                                // still compositing, else +inf (so "qm <= q_max" is the whole per-pixel geometric test)
+                                // q' = -q/2 of both entries for both pixels; qm = q' where the pixel is in the entry's
+                                // box and still compositing, else -inf (so "qm >= -q_max/2" is the whole per-pixel
+                                // geometric test)
                                 const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
-                                const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : kInf,
-                                                               (__float_as_uint(H0.w) & actB) ? q0.y : kInf);
-                                float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : kInf,
-                                                         (__float_as_uint(H1.w) & actB) ? q1.y : kInf);
-                                if (!kFull && jj + 1 >= nk) qm1 = make_float2(kInf, kInf);
+                                const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : -kInf,
+                                                               (__float_as_uint(H0.w) & actB) ? q0.y : -kInf);
+                                float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : -kInf,
+                                                         (__float_as_uint(H1.w) & actB) ? q1.y : -kInf);
+                                if (!kFull && jj + 1 >= nk) qm1 = make_float2(-kInf, -kInf);
                                 if (kCounts) wk[2] += (kFull || jj + 1 < nk) ? 2 : 1;
-                                if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fminf(fminf(qm0.x, qm0.y), fminf(qm1.x, qm1.y)) <= qmax)) {
+                                if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fmaxf(fmaxf(qm0.x, qm0.y), fmaxf(qm1.x, qm1.y)) >= qlo)) {
                                     // exp / alpha' of both entries are independent of T: computed side by side
-                                    const float2 x0 = exp_det2(mul2(bc2(-0.5f), q0));
-                                    const float2 x1 = exp_det2(mul2(bc2(-0.5f), q1));
-                                    const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);
-                                    const float2 a0 = make_float2(fminf(amax, ae0.x), fminf(amax, ae0.y));
-                                    const float2 a1 = make_float2(fminf(amax, ae1.x), fminf(amax, ae1.y));
+                                    const float2 x0 = exp_det2(q0);
+                                    const float2 x1 = exp_det2(q1);
+                                    const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);   // 2^11 alpha e
+                                    const float2 a0 = make_float2(fminf(amx, ae0.x), fminf(amx, ae0.y));
+                                    const float2 a1 = make_float2(fminf(amx, ae1.x), fminf(amx, ae1.y));
                                     if (kCounts) {
-                                        wk[3] += __any_sync(0xffffffffu, fminf(qm0.x, qm0.y) <= qmax) ? 1 : 0;
-                                        wk[3] += __any_sync(0xffffffffu, fminf(qm1.x, qm1.y) <= qmax) ? 1 : 0;
+                                        wk[3] += __any_sync(0xffffffffu, fmaxf(qm0.x, qm0.y) >= qlo) ? 1 : 0;
+                                        wk[3] += __any_sync(0xffffffffu, fmaxf(qm1.x, qm1.y) >= qlo) ? 1 : 0;
                                     }
-                                    w0 = tstep<kCounts>(qm0, a0, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                                    w0 = tstep<kCounts>(qm0, a0, qlo, alo, teps, T, actA, actB, ncA, ncB, wk);
                                     // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
-                                    qm1 = make_float2(actA ? qm1.x : kInf, actB ? qm1.y : kInf);
-                                    w1 = tstep<kCounts>(qm1, a1, qmax, amin, teps, T, actA, actB, ncA, ncB, wk);
+                                    qm1 = make_float2(actA ? qm1.x : -kInf, actB ? qm1.y : -kInf);
+                                    w1 = tstep<kCounts>(qm1, a1, qlo, alo, teps, T, actA, actB, ncA, ncB, wk);
                                 }
                             }
                             // split into fp16 hi / lo and store rows jj, jj+1

@@ -481,16 +481,17 @@ struct TcBuf {
 };
 
 // One compositing step of the normative a6 recurrence for the lane's two pixels, in the staged
-// scaling: qm = q' = -q/2 (or -inf if the pixel is outside the box / already stopped), a = 2^11
-// alpha'; qlo = -q_max/2, alo = 2^11 alpha_min.  Both scalings are exact (powers of two, no
+// scaling: q = q' = -q/2, a = 2^11 alpha', mA / mB = the entry's box lane masks (a pixel takes part
+// only while its bit is also set in actA / actB); qlo = -q_max/2, alo = 2^11 alpha_min.  Both scalings are exact (powers of two, no
 // subnormals on the used range), so every decision and T are those of the normative sequence:
 // fma(a, -2^-11, 1) = fl(1 - alpha').  Returns the weight 2^11 alpha' T of each pixel (0 if it does
 // not composite this entry) and advances T / the active bits.
 template <bool kCounts>
-__device__ __forceinline__ float2 tstep(float2 qm, float2 a, float qlo, float alo, float teps, float2& T,
-                                        uint32_t& actA, uint32_t& actB, int& ncA, int& ncB, unsigned long long* wk) {
+__device__ __forceinline__ float2 tstep(float2 q, float2 a, uint32_t mA, uint32_t mB, float qlo, float alo, float teps,
+                                        float2& T, uint32_t& actA, uint32_t& actB, int& ncA, int& ncB,
+                                        unsigned long long* wk) {
     const float2 Tn = mul2(T, fma2(a, bc2(-1.0f / 2048.0f), bc2(1.0f)));
-    const bool okA = qm.x >= qlo && a.x >= alo, okB = qm.y >= qlo && a.y >= alo;
+    const bool okA = (mA & actA) && q.x >= qlo && a.x >= alo, okB = (mB & actB) && q.y >= qlo && a.y >= alo;
     const bool inA = okA && Tn.x >= teps, inB = okB && Tn.y >= teps;
     if (okA && !inA) actA = 0u;           // T would drop below t_eps: stop before this Gaussian (R10)
     if (okB && !inB) actB = 0u;
@@ -799,17 +800,14 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                                 const int j1 = j0 + jj + ((kFull || jj + 1 < nk) ? 1 : 0);
                                 const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
                                 const float4 G1 = bf.g[j1], H1 = bf.h[j1];
-                                // q' = -q/2 of both entries for both pixels; qm = q' where the pixel is in the entry's
-                                // box and still compositing, else -inf (so "qm >= -q_max/2" is the whole per-pixel
-                                // geometric test)
+                                // q' = -q/2 of both entries for both pixels; a pixel takes part while it is inside
+                                // the entry's box (lane masks) and still compositing (actA / actB), and q' >= -q_max/2
                                 const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);
-                                const float2 qm0 = make_float2((__float_as_uint(H0.z) & actA) ? q0.x : -kInf,
-                                                               (__float_as_uint(H0.w) & actB) ? q0.y : -kInf);
-                                float2 qm1 = make_float2((__float_as_uint(H1.z) & actA) ? q1.x : -kInf,
-                                                         (__float_as_uint(H1.w) & actB) ? q1.y : -kInf);
-                                if (!kFull && jj + 1 >= nk) qm1 = make_float2(-kInf, -kInf);
-                                if (kCounts) wk[2] += (kFull || jj + 1 < nk) ? 2 : 1;
-                                if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fmaxf(fmaxf(qm0.x, qm0.y), fmaxf(qm1.x, qm1.y)) >= qlo)) {
+                                const uint32_t mA0 = __float_as_uint(H0.z), mB0 = __float_as_uint(H0.w);
+                                const bool has1 = kFull || jj + 1 < nk;
+                                const uint32_t mA1 = has1 ? __float_as_uint(H1.z) : 0u, mB1 = has1 ? __float_as_uint(H1.w) : 0u;
+                                if (kCounts) wk[2] += has1 ? 2 : 1;
+                                if (!kSkipEmptyPairs || __any_sync(0xffffffffu, ((mA0 | mA1) & actA) | ((mB0 | mB1) & actB))) {
                                     // exp / alpha' of both entries are independent of T: computed side by side
                                     const float2 x0 = exp_det2(q0);
                                     const float2 x1 = exp_det2(q1);
@@ -817,13 +815,12 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                                     const float2 a0 = make_float2(fminf(amx, ae0.x), fminf(amx, ae0.y));
                                     const float2 a1 = make_float2(fminf(amx, ae1.x), fminf(amx, ae1.y));
                                     if (kCounts) {
-                                        wk[3] += __any_sync(0xffffffffu, fmaxf(qm0.x, qm0.y) >= qlo) ? 1 : 0;
-                                        wk[3] += __any_sync(0xffffffffu, fmaxf(qm1.x, qm1.y) >= qlo) ? 1 : 0;
+                                        wk[3] += __any_sync(0xffffffffu, ((mA0 & actA) && q0.x >= qlo) || ((mB0 & actB) && q0.y >= qlo)) ? 1 : 0;
+                                        wk[3] += __any_sync(0xffffffffu, ((mA1 & actA) && q1.x >= qlo) || ((mB1 & actB) && q1.y >= qlo)) ? 1 : 0;
                                     }
-                                    w0 = tstep<kCounts>(qm0, a0, qlo, alo, teps, T, actA, actB, ncA, ncB, wk);
-                                    // entry 1's mask was taken before entry 0's stop: drop pixels that just stopped
-                                    qm1 = make_float2(actA ? qm1.x : -kInf, actB ? qm1.y : -kInf);
-                                    w1 = tstep<kCounts>(qm1, a1, qlo, alo, teps, T, actA, actB, ncA, ncB, wk);
+                                    w0 = tstep<kCounts>(q0, a0, mA0, mB0, qlo, alo, teps, T, actA, actB, ncA, ncB, wk);
+                                    // entry 1 sees the active bits after entry 0 (pixels that just stopped drop out)
+                                    w1 = tstep<kCounts>(q1, a1, mA1, mB1, qlo, alo, teps, T, actA, actB, ncA, ncB, wk);
                                 }
                             }
                             // split into fp16 hi / lo and store rows jj, jj+1

@@ -253,7 +253,8 @@ namespace {
 // ~1024 for 2048^2), warps per binning block (per-warp [NB] cursors + lane masks must fit in shared
 // memory), P = rank tiles of nw * 256 ranks.
 ta_status bin_geometry(ta_context* c, int H, int W, int64_t cap, BinGeom* bg) {
-    bg->shift = (std::max(H, W) > 1024 && cap <= ((int64_t)1 << list_idx_bits(kMaxCoarseShift))) ? kMaxCoarseShift : 5;
+    static const int min_side6 = getenv("TA_COARSE64_ABOVE") ? atoi(getenv("TA_COARSE64_ABOVE")) : 1024;   // tuning knob
+    bg->shift = (std::max(H, W) > min_side6 && cap <= ((int64_t)1 << list_idx_bits(kMaxCoarseShift))) ? kMaxCoarseShift : 5;
     if (cap > ((int64_t)1 << list_idx_bits(5)))
         return fail(c, TA_ERR_CAPACITY, "more than 2^%d Gaussians", list_idx_bits(5));
     const int bs = 1 << bg->shift;

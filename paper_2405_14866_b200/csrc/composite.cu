@@ -473,8 +473,11 @@ struct TcBuf {
     // and 32 entries are staged at a time, so 3 CTAs fit per SM instead of 2 (registers / smem)
     static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : NT, NTS = NT - NTR;
     static constexpr int NB = C >= 64 ? 32 : TA_TC_NB;   // entries staged per warp at a time
-    float4 g[NB];                      // mx, my, -ca/2, -cb2/2   (pre-scaled by exact powers of two:
-    float4 h[NB];                      // -cc/2, 2^11 alpha, box lane mask (A), (B)   q' = -q/2, a' = 2^11 alpha')
+    // staged records, entry pairs (2k, 2k+1) interleaved so that the compacted mode loads its packed
+    // (entry, entry) operands directly: p[k][0] = (mx, mx', my, my'), [1] = (-ca/2, .., -cb2/2, ..),
+    // [2] = (-cc/2, .., 2^11 alpha, ..), [3] = (box lane mask A, .., mask B, ..)  (pre-scaled by exact
+    // powers of two: q' = -q/2, a' = 2^11 alpha')
+    float4 p[NB / 2][4];
     __half f[NB][PH];                  // staged fp16 feature rows
     uint32_t w[2][16][WP];             // [hi|lo][k][lane]: half2 (w(pixel A), w(pixel B)) of staged entry j0+k
     SAcc<4 * NTS> sacc;                // [mt * NTS + nt - NTR][lane] (C = 64 only)
@@ -678,11 +681,15 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         const int d = cnt + (int)rank;
                         const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
                         const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                        bf.g[d] = make_float4(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
-                                              -0.5f * __uint_as_float(r0[hh].z), -0.5f * __uint_as_float(r0[hh].w));
-                        bf.h[d] = make_float4(-0.5f * __uint_as_float(r1[hh].x), 2048.0f * __uint_as_float(r1[hh].y),
-                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
-                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
+                        float* const pp = reinterpret_cast<float*>(&bf.p[d >> 1][0]) + (d & 1);
+                        pp[0] = __uint_as_float(r0[hh].x);
+                        pp[2] = __uint_as_float(r0[hh].y);
+                        pp[4] = -0.5f * __uint_as_float(r0[hh].z);
+                        pp[6] = -0.5f * __uint_as_float(r0[hh].w);
+                        pp[8] = -0.5f * __uint_as_float(r1[hh].x);
+                        pp[10] = 2048.0f * __uint_as_float(r1[hh].y);
+                        pp[12] = __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0));
+                        pp[14] = __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4));
                         const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
                         const uint32_t dst = smem_u32(&bf.f[d][0]);
 #pragma unroll
@@ -739,23 +746,22 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         float w0 = 0.0f, w1 = 0.0f;
                         if (jj < nk) {
                             const bool has1 = jj + 1 < nk;
-                            const int j1 = j0 + jj + (has1 ? 1 : 0);
-                            const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
-                            const float4 G1 = bf.g[j1], H1 = bf.h[j1];
+                            const float4* const pr = bf.p[(j0 + jj) >> 1];   // entries j, j+1 side by side
+                            const float4 P0 = pr[0], P1 = pr[1], P2 = pr[2], P3 = pr[3];
                             // q of entries j, j+1 for this lane's pixel (normative a6 sequence per component)
-                            const float2 dx = sub2(bc2(cpxf), make_float2(G0.x, G1.x));
-                            const float2 dy = sub2(bc2(cpyf), make_float2(G0.y, G1.y));
-                            const float2 t1 = mul2(make_float2(G0.w, G1.w), dy);
-                            const float2 t2 = fma2(make_float2(G0.z, G1.z), dx, t1);
-                            const float2 t4 = mul2(mul2(make_float2(H0.x, H1.x), dy), dy);
+                            const float2 dx = sub2(bc2(cpxf), make_float2(P0.x, P0.y));
+                            const float2 dy = sub2(bc2(cpyf), make_float2(P0.z, P0.w));
+                            const float2 t1 = mul2(make_float2(P1.z, P1.w), dy);
+                            const float2 t2 = fma2(make_float2(P1.x, P1.y), dx, t1);
+                            const float2 t4 = mul2(mul2(make_float2(P2.x, P2.y), dy), dy);
                             const float2 q = fma2(t2, dx, t4);     // q' = -q/2 (staged conic is -conic/2)
-                            const uint32_t b0 = __float_as_uint(hs ? H0.w : H0.z), b1 = __float_as_uint(hs ? H1.w : H1.z);
+                            const uint32_t b0 = __float_as_uint(hs ? P3.z : P3.x), b1 = __float_as_uint(hs ? P3.w : P3.y);
                             const float qm0 = (act1 && ((b0 >> ol) & 1u)) ? q.x : -kInf;
                             const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : -kInf;
                             if (kCounts) wk[2] += has1 ? 2 : 1;
                             if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fmaxf(qm0, qm1) >= qlo)) {
                                 const float2 e = exp_det2(q);
-                                const float2 ae = mul2(make_float2(H0.y, H1.y), e);             // 2^11 alpha e
+                                const float2 ae = mul2(make_float2(P2.z, P2.w), e);             // 2^11 alpha e
                                 const float2 a = make_float2(fminf(amx, ae.x), fminf(amx, ae.y)); // 2^11 alpha'
                                 const float2 om = fma2(a, bc2(-1.0f / 2048.0f), bc2(1.0f));      // fl(1 - alpha')
                                 {
@@ -797,9 +803,10 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         for (int jj = 0; jj < 16; jj += 2) {
                             float2 w0 = make_float2(0.0f, 0.0f), w1 = make_float2(0.0f, 0.0f);
                             if (kFull || jj < nk) {                          // warp-uniform
-                                const int j1 = j0 + jj + ((kFull || jj + 1 < nk) ? 1 : 0);
-                                const float4 G0 = bf.g[j0 + jj], H0 = bf.h[j0 + jj];
-                                const float4 G1 = bf.g[j1], H1 = bf.h[j1];
+                                const float4* const pr = bf.p[(j0 + jj) >> 1];   // entries j, j+1 side by side
+                                const float4 P0 = pr[0], P1 = pr[1], P2 = pr[2], P3 = pr[3];
+                                const float4 G0 = make_float4(P0.x, P0.z, P1.x, P1.z), G1 = make_float4(P0.y, P0.w, P1.y, P1.w);
+                                const float4 H0 = make_float4(P2.x, P2.z, P3.x, P3.z), H1 = make_float4(P2.y, P2.w, P3.y, P3.w);
                                 // q' = -q/2 of both entries for both pixels; a pixel takes part while it is inside
                                 // the entry's box (lane masks) and still compositing (actA / actB), and q' >= -q_max/2
                                 const float2 q0 = quad_q(G0, H0.x, pxf, py2), q1 = quad_q(G1, H1.x, pxf, py2);

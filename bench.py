@@ -305,12 +305,16 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
+    marks = []                                        # step boundaries on the main stream (per-step spread)
     for _ in range(args.steps):
         timed_step(params)
+        marks.append(torch.cuda.Event(enable_timing=True))
+        marks[-1].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     ms_local = ev0.elapsed_time(ev1)
+    step_ms = sorted([ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])])
     clk = clocks.stop()
     launches = int(sum_over_ranks(sum(cx.launches for cx in ctxs) + ctx_prep.launches - launches0))
     ms = max_over_ranks(ms_local)
@@ -345,7 +349,11 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded synthgen rig: ellipsoid upper body, log-normal scales, random rotations)",
             "config": dict(workload_config(n_g, kmax), streams=nstr), "gpu_launches": launches, "clocks": clk,
-            "overflow": overflow}
+            "overflow": overflow,
+            "step_ms_rank0": {"median": step_ms[len(step_ms) // 2], "min": step_ms[0],
+                              "p90": step_ms[min(len(step_ms) - 1, int(0.9 * len(step_ms)))],
+                              "note": "device time between consecutive step boundaries on rank 0's main stream "
+                                      "(frames are pipelined, so a step boundary is where its renders end)"}}
 
     # ---------------- roofline of the dominant kernel (rank 0's live stage events)
     if prof is not None and rank == 0:

@@ -124,7 +124,7 @@ void ta_default_params(ta_raster_params* p);
 ta_status ta_context_create(int32_t device, ta_context** out);
 ta_status ta_context_destroy(ta_context* ctx);
 
-/* Grow scratch for up to `max_gaussians` Gaussians, `max_entries` (32x32-pixel bin, Gaussian) pairs
+/* Grow scratch for up to `max_gaussians` Gaussians, `max_entries` (coarse bin, Gaussian) pairs
    (ta_debug_view.Kc of a representative call) and an H x W target (synchronous: allocation).
    Needed before TA_FLAG_ASYNC calls / graph capture. */
 ta_status ta_reserve(ta_context* ctx, int64_t max_gaussians, int64_t max_entries, int32_t H, int32_t W);
@@ -208,8 +208,10 @@ ta_status ta_blend(ta_context* ctx, const ta_source_view* views, int32_t V, cons
  *   d_mean2 [n][2]   d/d(pixel centre x, y)
  *   d_conic [n][3]   d/d(ca, cb2, cc) of q = ca dx^2 + cb2 dx dy + cc dy^2 (the record's conic)
  *   d_alpha [n]      d/d(opacity)      d_feat [n][C]  d/d(feature row)       (device float, overwritten)
- * Sums over pixels use fp32 atomics (order not fixed).  Errors: TA_ERR_INVALID_ARG for NULL pointers
- * or no matching forward call.
+ * Sums over pixels use fp32 atomics (order not fixed).  fp16-stored features with C in {16, 32, 64}
+ * run the tensor-core kernel (contractions by mma.sync, fp32 accumulation); fp32-stored features and
+ * C = 8 the plain per-pixel kernel.  Errors: TA_ERR_INVALID_ARG for NULL pointers or no matching
+ * forward call.
  */
 ta_status ta_rasterize_backward(ta_context* ctx, const ta_gaussians* g, int64_t n, int32_t H, int32_t W,
                                 const ta_raster_params* params, const float* grad_F, const float* grad_A,
@@ -230,7 +232,9 @@ ta_status ta_rasterize_backward(ta_context* ctx, const ta_gaussians* g, int64_t 
  * The host fields (n, K, P, tiles_x, tiles_y, sort_passes) are filled by a synchronising read.
  */
 typedef struct {
-    int64_t n, K, Kc;            /* Gaussians, (tile, Gaussian) entries, (32x32 bin, Gaussian) entries */
+    int64_t n, K, Kc;            /* Gaussians, (tile, Gaussian) entries, (coarse bin, Gaussian) entries:
+                                    32 x 32-pixel bins up to 1024 px per side, 64 x 64 beyond when the
+                                    Gaussian indices fit 24 bits */
     int32_t P, tiles_x, tiles_y, sort_passes;
     const uint32_t* records;
     const uint32_t* depth_keys;

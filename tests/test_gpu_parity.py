@@ -169,6 +169,42 @@ def test_c4_views_vs_single_view(ctx, oracle_lib):
         P.check_composite(out, F, A, nc)
 
 
+def test_concurrent_contexts_on_streams_match_sequential(ctx):
+    """The bench's launch configuration: views of one frame alternate over 4 (context, stream) pairs
+    with TA_FLAG_ASYNC after ta_reserve, kernels of different views overlapping; every view's F and A
+    are bit-identical to the same view rendered alone on one context (full c3 sources, 8 targets)."""
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("c3")
+    targets = sg.make_targets("c4", n_targets=8)
+    gp = P.gpu_params(s, flags=0)
+    g = P.gpu_unproject(ctx, s, gp)
+    H, W, C = 1024, 1024, s.C
+    ref = []
+    for cam in targets:
+        K, R, t = sg.cam_arrays(cam)
+        F, A = tb.rasterize(ctx, g, K, R, t, H, W, gp, n=-1)
+        torch.cuda.synchronize()
+        ref.append((F.clone(), A.clone(), ctx.debug_last().Kc))
+    kc = max(r[2] for r in ref)
+    ctxs = [tb.Context(0) for _ in range(4)]
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    pa = tb.default_params(default_scale=s.default_scale, default_opacity=s.default_opacity, flags=tb.TA_FLAG_ASYNC)
+    for cx in ctxs:
+        cx.reserve(g.capacity, int(kc * 1.05) + 4096, H, W)
+    outs = [(torch.empty((H, W, C), device="cuda"), torch.empty((H, W), device="cuda")) for _ in targets]
+    torch.cuda.synchronize()
+    for k, cam in enumerate(targets):
+        K, R, t = sg.cam_arrays(cam)
+        ctxs[k % 4].rasterize(g, -1, tb.intrinsics(K), tb.extrinsics(R, t), H, W, pa, outs[k][0], outs[k][1],
+                              streams[k % 4])
+    torch.cuda.synchronize()
+    assert not any(cx.check_overflow() for cx in ctxs)
+    for (F, A), (Fr, Ar, _) in zip(outs, ref):
+        assert torch.equal(A.view(torch.int32), Ar.view(torch.int32))
+        assert torch.equal(F.view(torch.int32), Fr.view(torch.int32))
+
+
 def test_c5_stress_sampled_tiles(ctx, oracle_lib):
     """configs[4] (4 x 2048^2, ~6.7M Gaussians, C = 64, 2048^2 target): a1 + a2 bit-exact in full,
     a4 depth order, a3/a5 on sampled tiles via per-tile enumeration, a6 on the sampled tiles."""

@@ -475,21 +475,28 @@ def e2e(args, ctx, g, views, keep, scene, cams, outs, H, W, C_, rank, world, str
     host_out = [(torch.empty((H, W, C_), dtype=torch.float32).pin_memory(),
                  torch.empty((H, W), dtype=torch.float32).pin_memory()) for _ in range(nbuf)]
     d2h = len(cams) * (H * W * C_ * 4 + H * W * 4)
-    copy = torch.cuda.Stream()
+    copy = torch.cuda.Stream()        # D2H of the rendered views
+    upload = torch.cuda.Stream()      # H2D of the next frame's source maps (PCIe is full duplex)
     rendered = [torch.cuda.Event() for _ in cams]
     copied = [torch.cuda.Event() for _ in cams]
+    lifted = {"ev": None}
 
     def step():
-        # inputs: H2D from pinned memory on the copy stream, consumed by ta_unproject on the compute stream
+        # inputs: H2D from pinned memory on the upload stream (once the previous frame's ta_unproject
+        # has read the device copies), consumed by ta_unproject on the compute stream
         if host_in:
-            with torch.cuda.stream(copy):
+            if lifted["ev"] is not None:
+                upload.wait_event(lifted["ev"])
+            with torch.cuda.stream(upload):
                 for h, d in host_in:
                     d.copy_(h, non_blocking=True)
             ev = torch.cuda.Event()
-            ev.record(copy)
+            ev.record(upload)
             stream.wait_event(ev)
         if rank == 0:
             ctx.unproject(views, params_sync, g, stream)
+            lifted["ev"] = torch.cuda.Event()
+            lifted["ev"].record(stream)
         broadcast()
         for k, ((Ki, Ri), (F, A)) in enumerate(zip(cams, outs)):
             stream.wait_event(copied[k])               # previous step's D2H of this buffer is done
@@ -519,9 +526,9 @@ def e2e(args, ctx, g, views, keep, scene, cams, outs, H, W, C_, rank, world, str
     return {"value": total_views * steps / (ms / 1e3),
             "unit": "views/s", "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
             "d2h_bytes_per_step": int(sum_over_ranks(d2h)), "steps": steps,
-            "note": "per step: source maps H2D from pinned host memory (copy stream) + ta_unproject + "
+            "note": "per step: source maps H2D from pinned host memory (upload stream) + ta_unproject + "
                     "ta_rasterize of every view + each view's F and A D2H into pinned host memory on a copy "
-                    "stream overlapping the next view's rendering"}
+                    "stream overlapping the next view's rendering (H2D and D2H use the two PCIe directions)"}
 
 
 def main():

@@ -341,7 +341,11 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
     const uint32_t s0 = cstart + warp * segl, s1 = min(cend, s0 + segl);
     const uint32_t lt = lanemask_lt();
     const uint64_t tbase = (uint64_t)cstart * NQ;
+    // every write of this bin lies below tbase + NQ len: one capacity check for the whole bin
+    const bool fits = tbase + (uint64_t)NQ * len <= tlist_cap && (uint64_t)NQ * len < (1ull << 32);
+    uint32_t* const tl = tlist + (fits ? tbase : 0);
     constexpr int kU = 4;                                           // chunks of 32 entries in flight
+    // pass 2 keeps in run[q] the offset of tile q's next entry from tl (q len + cursor)
     auto walk = [&](bool write, uint32_t (&run)[NQ]) {
         for (uint32_t pos = s0; pos < s1; pos += 32 * kU) {
             uint32_t ent[kU];
@@ -366,10 +370,7 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
                 if (NQ == 16 && __all_sync(0xffffffffu, tm == (1u << NQ) - 1u)) {   // 32 entries covering the whole bin
 #pragma unroll
                     for (int q = 0; q < NQ; q++) {
-                        if (write) {
-                            const uint64_t p = tbase + (uint64_t)q * len + run[q] + lane;
-                            if (p < tlist_cap) tlist[p] = idx;
-                        }
+                        if (write && fits) tl[run[q] + lane] = idx;
                         run[q] += 32u;
                     }
                     continue;
@@ -378,10 +379,7 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
                 for (int q = 0; q < NQ; q++) {
                     const bool ok = (tm >> q) & 1u;
                     const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-                    if (write && ok) {
-                        const uint64_t p = tbase + (uint64_t)q * len + run[q] + __popc(bal & lt);
-                        if (p < tlist_cap) tlist[p] = idx;
-                    }
+                    if (write && ok && fits) tl[run[q] + __popc(bal & lt)] = idx;
                     run[q] += __popc(bal);
                 }
             }
@@ -415,7 +413,7 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < NQ; q++) run[q] = s_cnt[warp][q];
+    for (int q = 0; q < NQ; q++) run[q] = (uint32_t)q * len + s_cnt[warp][q];
     walk(true, run);
 }
 

@@ -68,6 +68,12 @@ def test_rig_reduced(ctx):
     run_case(ctx, sg.make_config("c3", res=128, target_hw=(72, 104)))
 
 
+def test_rig_larger_target(ctx):
+    """configs[2] distributions at 256^2 sources into a ragged 200 x 232 target (C = 32 fp16): the
+    tensor-core kernel over many 8x8 blocks with long lists and mode changes."""
+    run_case(ctx, sg.make_config("c3", res=256, target_hw=(200, 232)), seed=5)
+
+
 def test_requires_forward_first(ctx):
     import torch
     import paper_2405_14866_b200 as tb

@@ -517,7 +517,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     TA_LAUNCHED(c);
     const int64_t cap_blocks = (cap + 255) / 256;
     if (cap_blocks > 0) {
-        k_project<<<(unsigned)cap_blocks, 256, 0, s>>>((const float4*)g->pos_alpha, (const float4*)g->cov, cam, rc, cs,
+        k_project<<<(unsigned)((cap + 511) / 512), 256, 0, s>>>((const float4*)g->pos_alpha, (const float4*)g->cov, cam, rc, cs,
                                                        rec, k0, v0);
         TA_LAUNCHED(c);
     }

@@ -390,7 +390,17 @@ __global__ void __launch_bounds__(256) k_bin_count(const uint2* __restrict__ box
     const uint32_t n = cs->n;
     const uint32_t R = (uint32_t)bg.nw * kBinRanksPerWarp;
     const uint32_t r1 = min(n, (tile + 1) * R);
-    for (uint32_t r = tile * R + threadIdx.x; r < r1; r += blockDim.x) count_box(s_h, boxes[r], bg);
+    constexpr int kIn = 8;                                  // boxes in flight per thread
+    for (uint32_t r = tile * R + threadIdx.x; r < r1; r += kIn * blockDim.x) {
+        uint2 bx[kIn];
+#pragma unroll
+        for (int u = 0; u < kIn; u++) {
+            const uint32_t rr = r + u * blockDim.x;
+            bx[u] = rr < r1 ? boxes[rr] : make_uint2(kEmptyRect, kEmptyRect);
+        }
+#pragma unroll
+        for (int u = 0; u < kIn; u++) count_box(s_h, bx[u], bg);
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < NB; k += blockDim.x) counts[(size_t)k * P + tile] = s_h[k];
 }
@@ -417,7 +427,16 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
     const uint32_t wr1 = min(n, wr0 + kBinRanksPerWarp);
     uint32_t* run = s_cnt + (size_t)warp * NB;
     // ---- per-warp bin counts of the warp's ranks
-    for (uint32_t r = wr0 + lane; r < wr1; r += 32) count_box(run, boxes[r], bg);
+    {
+        uint2 bx[kBinRanksPerWarp / 32];                  // all of this lane's boxes in flight at once
+#pragma unroll
+        for (int u = 0; u < kBinRanksPerWarp / 32; u++) {
+            const uint32_t r = wr0 + lane + 32u * u;
+            bx[u] = r < wr1 ? boxes[r] : make_uint2(kEmptyRect, kEmptyRect);
+        }
+#pragma unroll
+        for (int u = 0; u < kBinRanksPerWarp / 32; u++) count_box(run, bx[u], bg);
+    }
     __syncthreads();
     // ---- per bin: cursors = start of the (bin, tile) run + entries of the earlier warps
     for (int b = threadIdx.x; b < NB; b += blockDim.x) {
@@ -436,17 +455,19 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
     const uint32_t lt = lanemask_lt(), bit = 1u << lane;
     const uint32_t cap32 = (uint32_t)min(list_cap, (uint64_t)0xffffffffu);
     uint32_t overflow = 0u;
+    // the next step's box and index are loaded while this step places its entries
+    uint2 nb = make_uint2(kEmptyRect, kEmptyRect);
+    uint32_t nidx = 0u;
+    if (wr0 + lane < wr1) { nb = boxes[wr0 + lane]; nidx = sorted[wr0 + lane]; }
     for (uint32_t r0 = wr0; r0 < wr1; r0 += 32) {
         const uint32_t r = r0 + lane;
-        uint32_t idx = 0u;
+        const uint2 pb = nb;
+        const uint32_t idx = nidx;
+        nb = make_uint2(kEmptyRect, kEmptyRect);
+        if (r + 32 < wr1) { nb = boxes[r + 32]; nidx = sorted[r + 32]; }
         int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
         bool ok = false;
-        uint2 pb = make_uint2(kEmptyRect, kEmptyRect);
-        if (r < wr1) {
-            pb = boxes[r];
-            ok = box_bins(pb, bg.shift, &x0, &x1, &y0, &y1);
-            idx = sorted[r];
-        }
+        if (r < wr1) ok = box_bins(pb, bg.shift, &x0, &x1, &y0, &y1);
         // 16 x 16 tiles covered by the pixel box: each list entry carries, above the index, the
         // rectangle of its coarse bin's tiles the box covers (read by k_tile_split)
         const int tx0 = (int)(pb.x & 0xffff) >> 4, tx1 = (int)(pb.x >> 16) >> 4;

@@ -324,15 +324,28 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_pass(uint32_t* __restr
     }
     __syncthreads();
     const uint32_t m = n - b0 < (uint32_t)kSortKeysPerBlock ? n - b0 : (uint32_t)kSortKeysPerBlock;
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {    // digit runs -> consecutive addresses
-        const uint32_t k = s_key[i], v = s_val[i];
-        const uint32_t dd = (k >> shift) & 255u;
-        const uint32_t pos = s_gbase[dd] + (i - s_loc[dd]);
-        dk[pos] = k;
-        dv[pos] = v;
-        if (last) {
-            const uint4 q = rec[2 * v + 1];
-            boxes[pos] = make_uint2(q.z, q.w);
+    constexpr int kIt = kSortKeysPerBlock / (kSortWarps * 32);
+    uint2 bq[kIt];                                     // last pass: every pixel box gathered up front
+    if (last) {
+#pragma unroll
+        for (int u = 0; u < kIt; u++) {
+            const uint32_t i = threadIdx.x + u * (kSortWarps * 32);
+            if (i < m) {
+                const uint4 q = rec[2 * s_val[i] + 1];
+                bq[u] = make_uint2(q.z, q.w);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kIt; u++) {                    // digit runs -> consecutive addresses
+        const uint32_t i = threadIdx.x + u * (kSortWarps * 32);
+        if (i < m) {
+            const uint32_t k = s_key[i], v = s_val[i];
+            const uint32_t dd = (k >> shift) & 255u;
+            const uint32_t pos = s_gbase[dd] + (i - s_loc[dd]);
+            dk[pos] = k;
+            dv[pos] = v;
+            if (last) boxes[pos] = bq[u];
         }
     }
 }

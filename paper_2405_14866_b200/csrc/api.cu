@@ -526,7 +526,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     const uint32_t parts_max = (uint32_t)((cap + kSortKeysPerBlock - 1) / kSortKeysPerBlock);
     const uint32_t sort_blocks = parts_max;
     if (sort_blocks > 0) {
-        k_sort_digits<<<(unsigned)((cap + 2047) / 2048), 256, 0, s>>>(k0, cs);
+        k_sort_digits<<<(unsigned)std::min<int64_t>((cap + 2047) / 2048, 2 * c->num_sms), 256, 0, s>>>(k0, cs);
         TA_LAUNCHED(c);
         for (int pass = 0; pass < 4; pass++) {
             k_sort_pass<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs,

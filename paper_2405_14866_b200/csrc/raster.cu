@@ -164,34 +164,36 @@ __global__ void __launch_bounds__(256) k_sort_digits(const uint32_t* __restrict_
     for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&s_h[0][0])[k] = 0u;
     __syncthreads();
     const int shift0 = sort_shift(cs, 0);
-    // 8 consecutive keys per thread (neighbouring source pixels: similar depths, so the high digits
-    // come in runs and are counted run-length, one shared atomic per run)
-    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8u;
-    uint32_t key[8];
-    if (i0 + 8u <= n) {
-        const uint4 a = *reinterpret_cast<const uint4*>(keys + i0), b = *reinterpret_cast<const uint4*>(keys + i0 + 4);
-        key[0] = a.x; key[1] = a.y; key[2] = a.z; key[3] = a.w; key[4] = b.x; key[5] = b.y; key[6] = b.z; key[7] = b.w;
-    } else {
+    // grid-stride over tiles of 2048 keys, 8 consecutive keys per thread (neighbouring source pixels:
+    // similar depths, so the high digits come in runs and are counted run-length, one shared atomic
+    // per run); the block's histograms go to global memory once
+    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8u; i0 < n; i0 += gridDim.x * blockDim.x * 8u) {
+        uint32_t key[8];
+        if (i0 + 8u <= n) {
+            const uint4 a = *reinterpret_cast<const uint4*>(keys + i0), b = *reinterpret_cast<const uint4*>(keys + i0 + 4);
+            key[0] = a.x; key[1] = a.y; key[2] = a.z; key[3] = a.w; key[4] = b.x; key[5] = b.y; key[6] = b.z; key[7] = b.w;
+        } else {
 #pragma unroll
-        for (int k = 0; k < 8; k++) key[k] = i0 + k < n ? keys[i0 + k] : 0u;
-    }
-    const int m = i0 >= n ? 0 : (int)min(8u, n - i0);
-    for (int p = 0; p < npass; p++) {
-        const int sh = shift0 + 8 * p;
-        uint32_t prev = 0xffffffffu, run = 0u;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            if (k < m) {
-                const uint32_t d = (key[k] >> sh) & 255u;
-                if (d != prev) {
-                    if (run) atomicAdd(&s_h[p][prev], run);
-                    prev = d;
-                    run = 0u;
-                }
-                run++;
-            }
+            for (int k = 0; k < 8; k++) key[k] = i0 + k < n ? keys[i0 + k] : 0u;
         }
-        if (run) atomicAdd(&s_h[p][prev], run);
+        const int m = (int)min(8u, n - i0);
+        for (int p = 0; p < npass; p++) {
+            const int sh = shift0 + 8 * p;
+            uint32_t prev = 0xffffffffu, run = 0u;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (k < m) {
+                    const uint32_t d = (key[k] >> sh) & 255u;
+                    if (d != prev) {
+                        if (run) atomicAdd(&s_h[p][prev], run);
+                        prev = d;
+                        run = 0u;
+                    }
+                    run++;
+                }
+            }
+            if (run) atomicAdd(&s_h[p][prev], run);
+        }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < npass * 256; k += blockDim.x) {

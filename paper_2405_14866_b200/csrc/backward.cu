@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
             float2 T = make_float2(1.0f, 1.0f), Sup = make_float2(0.0f, 0.0f);
             uint32_t actA = inA ? (1u << lane) : 0u, actB = inB ? (1u << lane) : 0u;
             uint32_t pos = cstart;
+            uint32_t pf_pos = 0xffffffffu, pf = 0u;          // list index of entry pf_pos + lane, loaded ahead
             while (pos < cend && __any_sync(0xffffffffu, (actA | actB) != 0u)) {
                 // culling rectangle = bounding box of the pixels still compositing
                 const int lx0 = (actA | actB) ? px : 0x7fffffff, lx1 = (actA | actB) ? px : -1;
@@ -410,9 +411,11 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
                 int cnt = 0;
                 while (cnt < kBwdBuf && pos < cend) {
                     const uint32_t e = pos + lane;
-                    const uint32_t idx = e < cend ? tlist[e] : 0xffffffffu;
+                    const uint32_t idx = pf_pos == pos ? pf : (e < cend ? tlist[e] : 0xffffffffu);
                     const uint32_t i = idx < n ? idx : 0u;
                     const uint4 r1 = rec[2 * i + 1], r0 = rec[2 * i];
+                    pf_pos = pos + 32;
+                    pf = pos + 32 + lane < cend ? tlist[pos + 32 + lane] : 0xffffffffu;
                     const int gx0 = (int)(r1.z & 0xffff), gx1 = (int)(r1.z >> 16);
                     const int gy0 = (int)(r1.w & 0xffff), gy1 = (int)(r1.w >> 16);
                     bool kp = idx < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&

@@ -103,6 +103,14 @@ def test_wide_target_64px_coarse_bins(ctx, oracle_lib):
     assert out["K"] > 0
 
 
+def test_large_ragged_target(ctx, oracle_lib):
+    """A sparse scene in a 2300 x 3100 target: 64-px coarse bins over 49 x 36 bins, most tiles empty,
+    every stage and every pixel against the oracle (C = 16 fp16)."""
+    s = sg.make_random_scene(7, H=2300, W=3100, C=16, n_src=40, feat_dtype="f16")
+    out, _ = full_parity(ctx, oracle_lib, s)
+    assert out["K"] > 0 and out["tiles_x"] == 194 and out["tiles_y"] == 144
+
+
 def test_coarse_bins_fall_back_for_large_capacity(ctx, oracle_lib):
     """With more than 2^24 Gaussian slots (n = -1: the capacity bounds the indices) a > 1024 px target
     keeps 32 x 32-pixel bins (28 index bits): different coarse binning, identical output bits."""

@@ -54,10 +54,11 @@ def run_case(ctx, scene, seed=0):
     return ref
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(9))
 def test_random_scenes(ctx, seed):
-    """fp32 features (SIMT kernel) and fp16 features (tensor-core kernel, C in {16, 32, 64})."""
-    C = (8, 16, 32, 64, 16, 32, 64, 32)[seed]
+    """fp32 features and C = 8 fp16 (plain kernel), fp16 features with C in {16, 32, 64} (tensor-core
+    kernel)."""
+    C = (8, 16, 32, 64, 16, 32, 64, 32, 8)[seed]
     dt = "f16" if seed % 2 or seed >= 4 else "f32"
     s = sg.make_random_scene(20 + seed, H=21 + 9 * seed, W=47 - 6 * seed, C=C, n_src=14 + 2 * seed, feat_dtype=dt)
     run_case(ctx, s, seed)

@@ -95,52 +95,127 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
-def oracle_crop_view(scene_g, cam, crop=256):
-    """One bounded sample of the per-view work on the CPU oracle: the central crop x crop window of a
-    1024^2 target (1/16 of its pixels) -- project all Gaussians, build the window's tile lists,
-    composite every window pixel.  Returns seconds."""
+# The oracle (oracle/taoracle.c, plain single-threaded C) is the reported CPU baseline (SURVEY 8(d)
+# "Oracle timing"): Tiny, c2, one c3 view and one c5 view on ONE thread (bounded samples where a whole
+# view would take minutes, each scaled to ms/view and stated), and the c4 workload across all host
+# cores as independent single-threaded instances on different views.
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _window_seconds(g, cam, crop=256):
+    """The central crop x crop window of `cam` (1/16 of a 1024^2 target) on the oracle: projection of
+    all Gaussians, the window's (tile, depth, id) lists, compositing of its pixels."""
     import oracle
     import synthgen as sg
-    x0 = (cam.W - crop) // 2
-    y0 = (cam.H - crop) // 2
-    cc = sg.crop_camera(cam, x0, y0, crop, crop)
+    x0, y0 = (cam.W - crop) // 2, (cam.H - crop) // 2
     t0 = time.perf_counter()
-    oracle.rasterize(scene_g, cc)
+    oracle.rasterize(g, sg.crop_camera(cam, x0, y0, crop, crop))
     return time.perf_counter() - t0
 
 
-def cpu_baseline_value(g, cam, steps=1, crop=256):
-    ts = [oracle_crop_view(g, cam, crop) for _ in range(steps)]
-    frac = (crop * crop) / float(cam.W * cam.H)
-    t = statistics.mean(ts)
-    return 1.0 / (t / frac), t, frac
+_POOL_G = None
+
+
+def _pool_window(args):
+    j, crop = args
+    import synthgen as sg
+    return _window_seconds(_POOL_G, sg.make_targets("c4")[j % 32], crop)
+
+
+def c4_all_cores(g, cores, rounds=1, crop=256):
+    """c4 on every host core: `cores` independent single-threaded oracle processes per round, each on
+    the central window of a different parallax target.  Returns (views/s, wall seconds, windows)."""
+    import multiprocessing as mp
+    global _POOL_G
+    _POOL_G = g                                   # shared with the forked workers (copy-on-write)
+    ctx = mp.get_context("fork")
+    frac = crop * crop / float(1024 * 1024)
+    with ctx.Pool(cores) as pool:
+        pool.map(_pool_window, [(j, 32) for j in range(cores)])          # warm-up (page in, tiny windows)
+        t0 = time.perf_counter()
+        n = 0
+        for r in range(rounds):
+            pool.map(_pool_window, [(r * cores + j, crop) for j in range(cores)])
+            n += cores
+        wall = time.perf_counter() - t0
+    return n * frac / wall, wall, n
+
+
+def cpu_single_thread_table(g_c3, c3cam):
+    """ms per view on one thread: Tiny and c2 whole views; c3 = projection + full lists + compositing of
+    every 4th tile (x4); c5 = 16-row bands at 1/4, 1/2, 3/4 height (x 2048/16).  ~30-60 s."""
+    import numpy as np
+    import oracle
+    import synthgen as sg
+    out = {}
+    for name in ("tiny", "c2"):
+        s = sg.make_config(name)
+        g = oracle.unproject(s)
+        t0 = time.perf_counter()
+        oracle.rasterize(g, s.targets[0])
+        out[name] = {"ms_per_view": (time.perf_counter() - t0) * 1e3, "sample": "whole view"}
+    K, R, t = sg.cam_arrays(c3cam)
+    t0 = time.perf_counter()
+    pr = oracle.project(g_c3, K, R, t, c3cam.H, c3cam.W)
+    ranges, lst = oracle.tile_lists(pr, g_c3["ids"], c3cam.H, c3cam.W)
+    t1 = time.perf_counter()
+    T = len(ranges)
+    tiles = np.arange(0, T, 4, dtype=np.int32)
+    oracle.composite(g_c3, pr, ranges, lst, c3cam.H, c3cam.W, tiles=tiles)
+    t2 = time.perf_counter()
+    out["c3"] = {"ms_per_view": ((t1 - t0) + (t2 - t1) * T / len(tiles)) * 1e3,
+                 "sample": "projection + all tile lists whole; compositing of every 4th tile, x4"}
+    s5 = sg.make_config("c5", n_targets=1)
+    g5 = oracle.unproject(s5)
+    cam5 = s5.targets[0]
+    del s5
+    bt = []
+    for y0 in (cam5.H // 4, cam5.H // 2, 3 * cam5.H // 4):
+        band = sg.crop_camera(cam5, 0, y0, cam5.W, 16)
+        t0 = time.perf_counter()
+        oracle.rasterize(g5, band)
+        bt.append(time.perf_counter() - t0)
+    out["c5"] = {"ms_per_view": float(np.mean(bt)) * cam5.H / 16 * 1e3,
+                 "sample": "16-row bands at 1/4, 1/2, 3/4 height (projection of all 6.67M Gaussians + band "
+                           "lists + compositing), mean x 128 bands"}
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores, same metric / config / unit as our
+    arm; each step = one round of `cores` independent single-threaded oracle processes, each on the
+    central 256^2 window (1/16 view) of a different c4 target.  Rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import synthgen as sg
     import oracle
-    s = sg.make_config("c3")
-    g = oracle.unproject(s)
-    cam = sg.make_targets("c4")[0]
-    for _ in range(args.warmup):
-        oracle_crop_view(g, cam)
-    ts = [oracle_crop_view(g, cam) for _ in range(args.steps)]
-    frac = 256 * 256 / float(cam.W * cam.H)
-    t = statistics.mean(ts)
-    value = frac / t
-    sample = ("oracle/taoracle.c single-threaded: per step the central 256x256 window (1/16 of the pixels) of a "
-              "c4 1024^2 target -- EWA projection of all 1.67M Gaussians, (tile, depth, id) lists of the window, "
-              "compositing of its 65,536 pixels; value = (1/16) / step seconds; unprojection (per frame, "
-              "<1% of the oracle's per-view time) excluded")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "ms_per_view": t * 1e3 / frac,
+    oracle.build()
+    g = oracle.unproject(sg.make_config("c3"))
+    cores = os.cpu_count() or 1
+    v, wall, nwin = c4_all_cores(g, cores, rounds=max(1, args.steps))
+    sample = (f"oracle/taoracle.c, {cores} independent single-threaded processes (one per host core, "
+              f"{cpu_model()}); per step one round of {cores} windows: the central 256x256 window (1/16 of the "
+              f"pixels) of a different c4 1024^2 target each -- EWA projection of all 1.67M Gaussians, the "
+              f"window's (tile, depth, id) lists, compositing of its 65,536 pixels; value = windows/16 / wall "
+              f"seconds; unprojection (per frame) excluded")
+    ms_step = wall / max(1, args.steps) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "views/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_view": 1e3 / v,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": workload_config(None, None),
-            "cpu_baseline": {"value": value, "unit": "views/s", "cores": 1, "kind": "oracle", "sample": sample},
-            "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": "views/s", "cores": cores, "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -167,6 +242,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world} (launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without WORLD_SIZE to let bench.py relaunch itself)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -186,8 +264,8 @@ def run_ours(args):
     C_, H, W = 32, 1024, 1024
     cap = 4 * 1024 * 1024
     g = tb.GaussianBuffers(cap, C_, "f16", device=dev)
-    params_sync = tb.default_params()
-    params = tb.default_params(flags=tb.TA_FLAG_ASYNC)
+    params_sync = tb.default_params(exact_exp=int(not args.fast_exp))
+    params = tb.default_params(flags=tb.TA_FLAG_ASYNC, exact_exp=int(not args.fast_exp))
 
     scene = None
     views = keep = None
@@ -200,11 +278,12 @@ def run_ours(args):
         cams.append((tb.intrinsics(K), tb.extrinsics(R, t)))
     outs = [(torch.empty((H, W, C_), dtype=torch.float32, device=dev),
              torch.empty((H, W), dtype=torch.float32, device=dev)) for _ in mine]
+    bcast_rows = {"rows": None}          # host bound on n once known: the broadcast then never syncs
 
     def broadcast(gb=None):
         gb = gb if gb is not None else g
         if world > 1:
-            tdist.broadcast_gaussians((gb.pos_alpha, gb.cov, gb.feat), gb.n_dev, src=0)
+            tdist.broadcast_gaussians((gb.pos_alpha, gb.cov, gb.feat), gb.n_dev, src=0, rows=bcast_rows["rows"])
 
     def step(p):
         if rank == 0:
@@ -265,7 +344,8 @@ def run_ours(args):
         pipe["k"] += 1
         pipe["ready"] = prepare(pipe["k"] % 2)          # next frame's set, overlapping these renders
 
-    # sizing pass (synchronous): learn K per view, reserve for async steps
+    # sizing pass (synchronous; the broadcast reads n back once here): learn n and K per view, reserve
+    # for the asynchronous timed steps
     step(params_sync)
     torch.cuda.synchronize()
     kmax = kcmax = 0
@@ -274,6 +354,7 @@ def run_ours(args):
         d = ctx.debug_last()
         kmax, kcmax = max(kmax, d.K), max(kcmax, d.Kc)
     n_g = g.n
+    bcast_rows["rows"] = n_g                        # the frame's Gaussian count (same scene every frame)
     for cx in ctxs:
         cx.reserve(cap, int(kcmax * 1.05) + 4096, H, W)
 
@@ -318,6 +399,40 @@ def run_ours(args):
     clk = clocks.stop()
     launches = int(sum_over_ranks(sum(cx.launches for cx in ctxs) + ctx_prep.launches - launches0))
     ms = max_over_ranks(ms_local)
+    overflow = any(cx.check_overflow() for cx in ctxs)
+    value = n_views * args.steps / (ms / 1e3)
+
+    # per-view checksums of this frame's outputs (identical bits at every N: the view of index j is
+    # rendered by whichever rank owns it), summed over ranks into one table
+    ck = torch.zeros((n_views, 2), dtype=torch.int64, device=dev)
+    wF = torch.arange(H * W * C_, device=dev, dtype=torch.int64) % 1000003 + 1
+    wA = wF[:H * W]
+    for j, (F, A) in zip(mine, outs):
+        ck[j, 0] = (F.reshape(-1).view(torch.int32).to(torch.int64) * wF).sum()
+        ck[j, 1] = (A.reshape(-1).view(torch.int32).to(torch.int64) * wA).sum()
+    del wF, wA
+    if world > 1:
+        dist.all_reduce(ck)
+    checks = ["%016x%016x" % (int(a) & (2**64 - 1), int(b) & (2**64 - 1)) for a, b in ck.tolist()]
+
+    line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "ms_per_view": ms / (args.steps * n_views),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded synthgen rig: ellipsoid upper body, log-normal scales, random rotations)",
+            "config": dict(workload_config(n_g, kmax), streams=nstr,
+                           exp="fast (MUFU ex2.approx, TA exact_exp = 0)" if args.fast_exp else
+                               "exact (exp_det, DESIGN.md R13; TA exact_exp = 1)"),
+            "gpu_launches": launches, "clocks": clk, "overflow": overflow,
+            "step_ms_rank0": {"median": step_ms[len(step_ms) // 2], "min": step_ms[0],
+                              "p90": step_ms[min(len(step_ms) - 1, int(0.9 * len(step_ms)))],
+                              "note": "device time between consecutive step boundaries on rank 0's main stream "
+                                      "(frames are pipelined, so a step boundary is where its renders end)"},
+            "view_checksums": {"what": "per view j: weighted sums of the int32 bit patterns of F and A "
+                                       "(identical at every N iff every view's bits are)",
+                               "first": checks[0], "all_sha16": __import__("hashlib").sha256(
+                                   "".join(checks).encode()).hexdigest()[:16]}}
+
+    # ---------------- per-kernel durations: live stage events (single stream) or a serialized replay
     prof = None
     stage_timing = "stage events of context 0 inside the timed region (single stream)"
     if not args.no_stage_events:
@@ -341,19 +456,6 @@ def run_ours(args):
             stage_timing = ("stage events over a single-stream replay of the K timed steps (the timed multi-stream "
                             "step overlaps kernels of different views, so per-kernel durations are not defined there)")
     ctx.profile(False)
-    overflow = any(cx.check_overflow() for cx in ctxs)
-    value = n_views * args.steps / (ms / 1e3)
-
-    line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "ms_per_view": ms / (args.steps * n_views),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded synthgen rig: ellipsoid upper body, log-normal scales, random rotations)",
-            "config": dict(workload_config(n_g, kmax), streams=nstr), "gpu_launches": launches, "clocks": clk,
-            "overflow": overflow,
-            "step_ms_rank0": {"median": step_ms[len(step_ms) // 2], "min": step_ms[0],
-                              "p90": step_ms[min(len(step_ms) - 1, int(0.9 * len(step_ms)))],
-                              "note": "device time between consecutive step boundaries on rank 0's main stream "
-                                      "(frames are pipelined, so a step boundary is where its renders end)"}}
 
     # ---------------- roofline of the dominant kernel (rank 0's live stage events)
     if prof is not None and rank == 0:
@@ -364,7 +466,16 @@ def run_ours(args):
         tot = sum(share.values())
         line["stages_share"] = {k: round(v / tot, 4) for k, v in share.items()} if tot else {}
         line["roofline"] = roofline(ctx, g, cams[0], outs[0], H, W, C_, stages, n_g, stream,
-                                    ms_per_view=ms / (args.steps * n_views))
+                                    ms_per_view=ms / (args.steps * n_views), exact_exp=int(not args.fast_exp))
+
+    # ---------------- c3 headline (BASELINE.json north_star): one 1024^2 target, one call at a time
+    if rank == 0 and not args.no_c3:
+        line["c3_single_view"] = c3_single_view(args, ctx, g, views, params, params_sync, H, W, C_, n_g, stream)
+
+    # ---------------- render + gather of every view to rank 0
+    if world > 1 and not args.no_gather:
+        line["render_gather"] = render_gather(args, ctxs, side, g, cams, outs, mine, n_views, H, W, C_, params,
+                                              rank, world, stream, broadcast, barrier, max_over_ranks)
 
     # ---------------- end to end through the C ABI with host buffers
     if not args.no_e2e:
@@ -373,13 +484,7 @@ def run_ours(args):
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        import oracle
-        go = oracle.unproject(scene)
-        v, t, frac = cpu_baseline_value(go, targets[0])
-        line["cpu_baseline"] = {"value": v, "unit": "views/s", "cores": 1, "kind": "oracle",
-                                "sample": f"oracle/taoracle.c single-threaded on the central 256x256 window "
-                                          f"({frac:.4f} of the pixels) of c4 target 0: projection of all Gaussians + "
-                                          f"window tile lists + compositing, {t:.2f} s; value = fraction / seconds"}
+        line["cpu_baseline"] = cpu_baseline(scene, targets)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -388,7 +493,139 @@ def run_ours(args):
     return 0
 
 
-def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None):
+def cpu_baseline(scene, targets):
+    import oracle
+    oracle.build()
+    go = oracle.unproject(scene)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    v, wall, nwin = c4_all_cores(go, cores, rounds=1)
+    table = cpu_single_thread_table(go, sg_c3_target())
+    return {"value": v, "unit": "views/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": (f"c4 on all {cores} host cores: {nwin} independent single-threaded oracle processes, each "
+                       f"the central 256x256 window (1/16 view) of a different c4 target (projection of all "
+                       f"Gaussians + window lists + compositing), {wall:.1f} s wall; value = windows/16 / s"),
+            "single_thread_ms_per_view": table, "seconds": time.perf_counter() - t0}
+
+
+def sg_c3_target():
+    import synthgen as sg
+    return sg.make_targets("c3")[0]
+
+
+def l2_flush(buf):
+    """Write a buffer larger than L2 (126 MB) between timed calls."""
+    buf.add_(1)
+
+
+def c3_single_view(args, ctx, g, views, params, params_sync, H, W, C_, n_g, stream):
+    """BASELINE.json north_star headline: the c3 target (1024^2, the 4-view set) rendered one call at a
+    time on one stream, CUDA events around each ta_rasterize (K1-K5), L2 flushed between calls;
+    median / min / p90 over >= 20 calls after 5 warm-ups.  ta_unproject (per frame) is timed the same
+    way and reported separately with its own HBM roofline."""
+    import numpy as np
+    import torch
+    import synthgen as sg
+    import paper_2405_14866_b200 as tb
+    cam = sg.make_targets("c3")[0]
+    K, R, t = sg.cam_arrays(cam)
+    Ki, Ri = tb.intrinsics(K), tb.extrinsics(R, t)
+    F = torch.empty((H, W, C_), dtype=torch.float32, device="cuda")
+    A = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+    n = max(20, args.c3_calls)
+
+    def timed(fn):
+        ts = []
+        for i in range(5 + n):
+            l2_flush(flush)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= 5:
+                ts.append(a.elapsed_time(b))
+        ts.sort()
+        return {"median": ts[len(ts) // 2], "min": ts[0], "p90": ts[min(len(ts) - 1, int(0.9 * len(ts)))],
+                "calls": len(ts)}
+
+    ctx.rasterize(g, -1, Ki, Ri, H, W, params_sync, F, A, stream)     # size this target's lists
+    torch.cuda.synchronize()
+    d = ctx.debug_last()
+    ctx.reserve(g.capacity, int(d.Kc * 1.05) + 4096, H, W)
+    r_ms = timed(lambda: ctx.rasterize(g, -1, Ki, Ri, H, W, params, F, A, stream))
+    u_ms = timed(lambda: ctx.unproject(views, params_sync, g, stream))
+    torch.cuda.synchronize()
+    peaks, src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS))
+    # per-view algorithmic bytes (SURVEY 8(d)): B_alg = N (48 + 2C) + 16 K + 4 HW (C + 1)
+    b_alg = n_g * (48 + 2 * C_) + 16 * int(d.K) + 4 * H * W * (C_ + 1)
+    src_px = sum(int(v.H) * int(v.W) for v in views)
+    # unproject: read disparity 4 + mask 1 + scale 12 + quat 16 + opacity 4 + features 2C per source
+    # pixel, write pos_alpha 16 + cov 32 + features 2C per lifted Gaussian
+    b_unp = src_px * (4 + 1 + 12 + 16 + 4 + 2 * C_) + n_g * (16 + 32 + 2 * C_)
+    t_r, t_u = r_ms["median"] / 1e3, u_ms["median"] / 1e3
+    return {"target": "c3 (BASELINE.json configs[2]): 1024^2 on the arc between the pairs, C = 32",
+            "rasterize_ms": r_ms, "views_per_s": 1e3 / r_ms["median"],
+            "roofline": {"bound": "hbm", "alg_bytes": b_alg, "achieved": b_alg / t_r / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": b_alg / t_r / 1e9 / hbm, "peak_source": src,
+                         "north_star_target_ms": b_alg / (0.5 * hbm * 1e9) * 1e3,
+                         "entries": int(d.K), "coarse_entries": int(d.Kc)},
+            "unproject_ms": u_ms,
+            "unproject_roofline": {"bound": "hbm", "alg_bytes": b_unp, "achieved": b_unp / t_u / 1e9, "peak": hbm,
+                                   "unit": "GB/s", "frac": b_unp / t_u / 1e9 / hbm},
+            "frame_ms_amortised_32_views": u_ms["median"] / 32 + r_ms["median"],
+            "timing": "CUDA events on the launching stream around each call, 256 MB L2 flush between calls, "
+                      "TA_FLAG_ASYNC after ta_reserve (no host sync inside the call)"}
+
+
+def render_gather(args, ctxs, side, g, cams, outs, mine, n_views, H, W, C_, params, rank, world, stream, broadcast,
+                  barrier, max_over_ranks):
+    """Render + gather to rank 0: per step every rank renders its views (as in the
+    timed step) and every view's F and A go to rank 0 by collective gathers (ncclGather over
+    NVLink / NVSwitch).  Rank 0's ingress bound = (N-1)/N x 32 x 4HW(C+1) bytes / link bandwidth."""
+    import torch
+    from paper_2405_14866_b200 import dist as tdist
+    nstr = len(ctxs)
+
+    def step():
+        broadcast()
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        for sd in side:
+            sd.wait_event(ready)
+        for k, ((Ki, Ri), (F, A)) in enumerate(zip(cams, outs)):
+            ctxs[k % nstr].rasterize(g, -1, Ki, Ri, H, W, params, F, A, side[k % nstr])
+        for sd in side:
+            done = torch.cuda.Event()
+            done.record(sd)
+            stream.wait_event(done)
+        tdist.gather_views([F for F, _ in outs], n_views, rank, world)
+        tdist.gather_views([A for _, A in outs], n_views, rank, world)
+
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    steps = max(2, min(args.steps, 5))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(a.elapsed_time(b))
+    view_bytes = 4 * H * W * (C_ + 1)
+    ingress = (world - 1) / world * n_views * view_bytes
+    return {"value": n_views * steps / (ms / 1e3), "unit": "views/s", "ms_per_step": ms / steps, "steps": steps,
+            "gather_bytes_per_step": n_views * view_bytes,
+            "ingress_bound_ms": {"nominal_900GBps": ingress / 900e9 * 1e3, "measured_770GBps": ingress / 770e9 * 1e3},
+            "note": "per step: broadcast + render of each rank's views + torch.distributed.gather (NCCL) of every "
+                    "view's F and A to rank 0 in view order; max over ranks"}
+
+
+def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None, exact_exp=1):
     """Algorithmic bytes / flops per launch over the live
     per-launch time of each stage; the dominant stage is reported."""
     import numpy as np
@@ -397,7 +634,7 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
     from tests import _parity as P   # d2h helper only (no oracle use)
     Ki, Ri = cam0
     F, A = out0
-    pc = tb.default_params(flags=tb.TA_FLAG_DEBUG_COUNTS)
+    pc = tb.default_params(flags=tb.TA_FLAG_DEBUG_COUNTS, exact_exp=exact_exp)
     ctx.rasterize(g, -1, Ki, Ri, H, W, pc, F, A, stream)
     torch.cuda.synchronize()
     d = ctx.debug_last()
@@ -419,7 +656,9 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
         "bin_count": 12 * nvis + 4 * NB * d.P,
         "bin_scan": 8 * NB * d.P,
         "bin_place": 12 * nvis + 4 * Kc + 4 * NB * d.P,
-        "composite": 4 * Kc + nvis * (32 + fb) + 4 * H * W * (C_ + 1),
+        # the compositor walks the per-tile lists (4 B per (tile, Gaussian) entry), reads each visible
+        # Gaussian's 32-B record + feature row once, writes F and A
+        "composite": 4 * K + nvis * (32 + fb) + 4 * H * W * (C_ + 1),
     }
     flops_comp = pairs * (2 * C_ + 12)
     dom = max((k for k in bytes_alg), key=lambda k: stages.get(k, 0.0))
@@ -443,14 +682,21 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
         kname = {"project": "k_project", "bin_count": "k_bin_count", "bin_place": "k_bin_place",
                  "composite": "k_composite_tc", "sort": "k_sort_pass"}.get(dom)
         if kname in tj:
-            traffic = tj[kname]["dram_bytes"]
-            r["traffic_source"] = "profiles/traffic.json <- " + tj[kname]["source"] + " (ncu --set full, one launch)"
+            e = tj[kname]
+            traffic = e["dram_bytes"]
+            r["traffic_source"] = ("profiles/traffic.json <- " + e["source"] + " (ncu --set full, one launch: "
+                                   + e.get("kernel", kname) + ", grid " + str(e.get("grid")) + ", "
+                                   + str(e.get("duration_us")) + " us)")
+            r["traffic_over_algorithmic"] = traffic / bytes_alg[dom]
     except Exception:
         pass
     r.update({"kernel": dom, "traffic": traffic, "ms_per_launch": stages[dom],
               "algorithmic_bytes_per_launch": bytes_alg[dom], "composited_pairs_per_view": pairs,
-              "visible_gaussians": nvis, "entries_per_view": K, "coarse_entries_per_view": Kc})
-    # whole-view roofline: all per-view algorithmic bytes vs the summed per-view stage time
+              "visible_gaussians": nvis, "entries_per_view": K, "coarse_entries_per_view": Kc,
+              "work_counters": {k: int(v) for k, v in zip(
+                  ("list_entries_read", "staged", "evaluated", "evaluated_q_ok", "accumulated", "composited_pairs",
+                   "warps", "fill_rounds"), d.work)}})
+    # whole-view roofline: all per-view algorithmic bytes vs the per-view time of the timed step
     view_ms = ms_per_view if ms_per_view else sum(v for k, v in stages.items() if k != "unproject")
     b_view = n_g * 48 + nvis * fb + 16 * K + 4 * H * W * (C_ + 1)
     r["view"] = {"ms": view_ms, "alg_bytes": b_view, "hbm_frac": b_view / (view_ms / 1e3) / 1e9 / hbm,
@@ -531,6 +777,66 @@ def e2e(args, ctx, g, views, keep, scene, cams, outs, H, W, C_, rank, world, str
                     "stream overlapping the next view's rendering (H2D and D2H use the two PCIe directions)"}
 
 
+def free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    p = so.getsockname()[1]
+    so.close()
+    return p
+
+
+def relaunch_command(args_gpus, argv, env):
+    """--gpus N > 1 without a torchrun environment: the command that relaunches this script with N
+    ranks (one process per GPU, rendezvous on 127.0.0.1).  None when no relaunch is needed."""
+    if args_gpus <= 1 or "WORLD_SIZE" in env:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args_gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__), *argv]
+
+
+def run_dry_dist(args):
+    """--dry-run-dist (CPU, gloo): the multi-rank host logic of the bench without a GPU -- view
+    sharding, the host-bound broadcast of a Gaussian set, per-view rendering (a deterministic stand-in
+    image per view index), the gather to rank 0 in view order, max-over-ranks timing.  Rank 0 checks
+    that every gathered view equals the single-process rendering of that view index and prints one
+    JSON line (tests/test_dist_gloo.py drives it through the relaunch path)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2405_14866_b200 import dist as tdist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE = {world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_views = args.views
+
+    def render(j):
+        gen = torch.Generator().manual_seed(1000 + j)
+        return torch.randn((8, 8, 4), generator=gen)
+
+    g = (torch.arange(40, dtype=torch.float32).reshape(10, 4) if rank == 0 else torch.zeros((10, 4)))
+    n_dev = torch.tensor([7 if rank == 0 else 0], dtype=torch.int64)
+    if world > 1:
+        tdist.broadcast_gaussians((g,), n_dev, rows=8)
+    mine = tdist.shard(n_views, rank, world)
+    t0 = time.perf_counter()
+    local = [render(j) for j in mine]
+    out = tdist.gather_views(local, n_views, rank, world) if world > 1 else local
+    ms = tdist.reduce_scalar((time.perf_counter() - t0) * 1e3, "max")
+    if rank == 0:
+        ok = len(out) == n_views and all(torch.equal(v, render(j)) for j, v in enumerate(out))
+        print(json.dumps({"dry_run_dist": True, "n_gpus": world, "views": n_views, "views_equal": ok,
+                          "n_broadcast": int(n_dev[0]), "gaussians_equal": bool(torch.equal(
+                              g[:8], torch.arange(40, dtype=torch.float32).reshape(10, 4)[:8])),
+                          "ms_max_over_ranks": ms}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -539,10 +845,20 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--views", type=int, default=32)
     ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--fast-exp", action="store_true", help="time the opt-in MUFU ex2 mode (exact_exp = 0)")
+    ap.add_argument("--c3-calls", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stage-events", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--dry-run-dist", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    cmd = relaunch_command(args.gpus, sys.argv[1:], os.environ)
+    if cmd is not None:
+        return subprocess.call(cmd)
+    if args.dry_run_dist:
+        return run_dry_dist(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -109,6 +109,11 @@ typedef struct {
     float default_scale;         /* used when a view has no scale map */
     float default_opacity;       /* used when a view has no opacity map */
     uint32_t flags;              /* TA_FLAG_* */
+    int32_t exact_exp;           /* 1 (default): exp by the fixed fp32 sequence exp_det (R13), identical to the
+                                    oracle, so every decision and A are bit-exact.  0: the opt-in fast mode --
+                                    the compositor evaluates exp(-q/2) with the SFU (ex2.approx of the same
+                                    staged argument times log2 e); alpha' may then differ by a few ulp, which
+                                    can move a stop decision (parity reported separately: test_gpu_fast_exp) */
 } ta_raster_params;
 
 /* ta_rasterize does not synchronise with the host.  Scratch must already be large enough

@@ -635,8 +635,8 @@ void tao_blend(int V, const tao_bview* views, const tao_params* p, const tao_bpa
                     ws = ws + w;
                 }
             }
-            /* Eq. 10 */
-            if (ws >= bp->w_min) {
+            /* Eq. 10; sum w = 0 is a hole even for w_min = 0 (hole colour 0) */
+            if (ws > 0.0f && ws >= bp->w_min) {
                 for (int k = 0; k < 3; k++) rgb[pix * 3 + k] = acc[k] / ws;
             } else {
                 for (int k = 0; k < 3; k++) rgb[pix * 3 + k] = 0.0f;

@@ -46,7 +46,8 @@ class Gaussians(C.Structure):
 class RasterParams(C.Structure):
     _fields_ = [("dilation", C.c_float), ("alpha_max", C.c_float), ("alpha_min", C.c_float),
                 ("t_eps", C.c_float), ("cull_sigma", C.c_float), ("z_near", C.c_float), ("d_min", C.c_float),
-                ("default_scale", C.c_float), ("default_opacity", C.c_float), ("flags", C.c_uint32)]
+                ("default_scale", C.c_float), ("default_opacity", C.c_float), ("flags", C.c_uint32),
+                ("exact_exp", C.c_int32)]
 
 
 class BlendParams(C.Structure):

@@ -31,6 +31,11 @@ struct ta_context {
     int device = 0;
     int num_sms = 148;
     size_t smem_optin = 0;
+    // per-context launch configuration (ta_context_create, on this context's device): persistent grid
+    // sizes of the compositor / backward per C slot, and the tuning knobs read once from the environment
+    int resident_tc[4] = {1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1};
+    int coarse64_above = 1024;    // TA_COARSE64_ABOVE: 64-px coarse bins for targets wider / taller than this
+    bool bwd_simt = false;        // TA_BWD_SIMT: force the plain backward kernel
     std::string err;
     uint64_t launches = 0;
     DevBuf cs, status, rec, boxes, tile_order, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
@@ -45,6 +50,10 @@ struct ta_context {
     uint32_t last_P = 0;
     bool last_counts = false;
     CompositeGeom last_cg{};
+    int last_C = 0, last_fbytes = 0;  // the forward call the backward pass must match
+    int64_t last_n = 0;
+    const void* last_feat = nullptr;
+    RasterConsts last_rc{};
     DevBuf dbg_offs, dbg_list;
     // stage profiling
     bool profiling = false;
@@ -178,6 +187,7 @@ void ta_default_params(ta_raster_params* p) {
     p->default_scale = 0.0f;
     p->default_opacity = 1.0f;
     p->flags = 0u;
+    p->exact_exp = 1;
 }
 
 const char* ta_status_string(ta_status s) {
@@ -221,6 +231,19 @@ ta_status ta_context_create(int32_t device, ta_context** out) {
         cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess ||
         cudaFuncSetAttribute(k_bin_place, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) {
         cudaGetLastError();
+        if (c->pinned) cudaFreeHost(c->pinned);
+        cudaFree(c->cs.p);
+        delete c;
+        return TA_ERR_CUDA;
+    }
+    if (const char* e = getenv("TA_COARSE64_ABOVE")) c->coarse64_above = atoi(e);   // tuning knobs
+    c->bwd_simt = getenv("TA_BWD_SIMT") != nullptr;
+    const int cap = getenv("TA_TC_CTAS_PER_SM") ? atoi(getenv("TA_TC_CTAS_PER_SM")) : 0;
+    if (prepare_composite(c->num_sms, cap, c->resident_tc) != cudaSuccess ||
+        prepare_composite_bwd(c->num_sms, c->resident_bwd) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeHost(c->pinned);
+        cudaFree(c->cs.p);
         delete c;
         return TA_ERR_CUDA;
     }
@@ -253,7 +276,7 @@ namespace {
 // ~1024 for 2048^2), warps per binning block (per-warp [NB] cursors + lane masks must fit in shared
 // memory), P = rank tiles of nw * 256 ranks.
 ta_status bin_geometry(ta_context* c, int H, int W, int64_t cap, BinGeom* bg) {
-    static const int min_side6 = getenv("TA_COARSE64_ABOVE") ? atoi(getenv("TA_COARSE64_ABOVE")) : 1024;   // tuning knob
+    const int min_side6 = c->coarse64_above;
     bg->shift = (std::max(H, W) > min_side6 && cap <= ((int64_t)1 << list_idx_bits(kMaxCoarseShift))) ? kMaxCoarseShift : 5;
     if (cap > ((int64_t)1 << list_idx_bits(5)))
         return fail(c, TA_ERR_CAPACITY, "more than 2^%d Gaussians", list_idx_bits(5));
@@ -284,11 +307,15 @@ CompositeGeom composite_geometry(const BinGeom& bg, int H, int W) {
     return cg;
 }
 
-// Coarse list (entries x 4 B) and the per-tile lists (tiles per bin x 4 B).
+// Coarse list (entries x 4 B) and the per-tile lists (tiles per bin x 4 B).  Per-tile list positions
+// are 32-bit (trng, the compositors' cursors), so the tile-list space nq x entries must stay below 2^32.
 ta_status reserve_lists(ta_context* c, size_t entries, int shift) {
     ta_status st;
     const size_t nq = (size_t)1 << (2 * (shift - 4));
     entries = std::max<size_t>(entries, 1);
+    if ((uint64_t)entries * nq > 0xffffffffull)
+        return fail(c, TA_ERR_CAPACITY, "%zu coarse entries x %zu tiles per bin exceed the 2^32-1 tile-list positions",
+                    entries, nq);
     if ((st = grow(c, c->list, entries * 4)) != TA_OK) return st;
     return grow(c, c->tlist, entries * 4 * nq);
 }
@@ -391,7 +418,8 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     if (!c) return TA_ERR_INVALID_ARG;
     if (max_gaussians < 0 || max_entries < 0 || H <= 0 || W <= 0 || H > 32767 || W > 32767)
         return fail(c, TA_ERR_INVALID_ARG, "ta_reserve: bad sizes");
-    if (max_entries > 0xffffffffll) return fail(c, TA_ERR_CAPACITY, "more than 2^32-1 tile entries");
+    if (max_entries > 0xffffffffll) return fail(c, TA_ERR_CAPACITY, "more than 2^32-1 tile entries");   // (and reserve_lists:
+                                                                                                        //  x tiles per bin)
     cudaSetDevice(c->device);
     ta_status st;
     if ((st = reserve_gaussians(c, max_gaussians)) != TA_OK) return st;
@@ -482,9 +510,13 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     if ((st = reserve_gaussians(c, cap)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, cap, H, W)) != TA_OK) return st;
     if (counts && (st = grow(c, c->ncontrib, (size_t)H * W * 4)) != TA_OK) return st;
-    if ((st = reserve_lists(c, c->list.p ? c->list.bytes / 4 : (size_t)std::max<int64_t>(cap, 1) * 4, bg.shift)) !=
-        TA_OK)
-        return st;
+    {
+        const uint64_t nq = 1ull << (2 * (bg.shift - 4));
+        const uint64_t first = std::min<uint64_t>((uint64_t)std::max<int64_t>(cap, 1) * 4, 0xffffffffull / nq);
+        if ((st = reserve_lists(c, c->list.p ? std::min<uint64_t>(c->list.bytes / 4, 0xffffffffull / nq) : first,
+                                bg.shift)) != TA_OK)
+            return st;
+    }
 
     TargetCam cam;
     cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
@@ -497,6 +529,8 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     rc.dilation = p->dilation; rc.alpha_max = p->alpha_max; rc.alpha_min = p->alpha_min; rc.t_eps = p->t_eps;
     rc.cull_sigma = p->cull_sigma; rc.z_near = p->z_near;
     rc.q_max = p->cull_sigma * p->cull_sigma;
+    if (p->exact_exp != 0 && p->exact_exp != 1) return fail(c, TA_ERR_INVALID_ARG, "exact_exp must be 0 or 1");
+    const bool fast_exp = p->exact_exp == 0;
 
     CallState* cs = (CallState*)c->cs.p;
     unsigned long long* status = (unsigned long long*)c->status.p;
@@ -554,10 +588,16 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
         TA_CUDA(c, cudaMemcpyAsync(c->pinned, &cs->K, 8, cudaMemcpyDeviceToHost, s));
         TA_CUDA(c, cudaStreamSynchronize(s));
         const uint64_t Kh = c->pinned[0];
-        if (Kh > 0xffffffffull) return fail(c, TA_ERR_CAPACITY, "%llu tile entries exceed 2^32-1", (unsigned long long)Kh);
-        if (!lists_reserved(c, (size_t)Kh, bg.shift) &&
-            (st = reserve_lists(c, std::max<size_t>(c->list.bytes / 4, (size_t)(Kh + Kh / 8 + 1024)), bg.shift)) != TA_OK)
-            return st;
+        const uint64_t nq = 1ull << (2 * (bg.shift - 4));
+        if (Kh * nq > 0xffffffffull)
+            return fail(c, TA_ERR_CAPACITY, "%llu coarse entries x %llu tiles per bin exceed 2^32-1 tile-list positions",
+                        (unsigned long long)Kh, (unsigned long long)nq);
+        if (!lists_reserved(c, (size_t)Kh, bg.shift)) {
+            // grow by 1/8 headroom, but never past the 32-bit tile-list position space
+            const uint64_t want = std::min<uint64_t>(std::max<uint64_t>(c->list.bytes / 4, Kh + Kh / 8 + 1024),
+                                                     0xffffffffull / nq);
+            if ((st = reserve_lists(c, (size_t)want, bg.shift)) != TA_OK) return st;
+        }
     }
     tm.end();
     tm.begin(TA_STAGE_BIN_PLACE);
@@ -569,7 +609,7 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);
-    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, rec, g->feat, (const uint32_t*)c->tlist.p,
+    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, c->resident_tc, rec, g->feat, (const uint32_t*)c->tlist.p,
                                      (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
                                      (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
                                      counts ? (int32_t*)c->ncontrib.p : nullptr, s);
@@ -580,6 +620,11 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     c->last_TX = cg.TX; c->last_TY = cg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;
     c->last_cg = cg;
     c->last_counts = counts;
+    c->last_C = g->C;
+    c->last_fbytes = g->feat_dtype == TA_F16 ? 2 : 4;
+    c->last_n = n;
+    c->last_feat = g->feat;
+    c->last_rc = rc;
     return TA_OK;
 }
 
@@ -693,16 +738,24 @@ ta_status ta_rasterize_backward(ta_context* c, const ta_gaussians* g, int64_t n,
         return fail(c, TA_ERR_INVALID_ARG, "ta_rasterize_backward needs the matching ta_rasterize on this context first");
     if (!supported_C(g->C)) return fail(c, TA_ERR_UNSUPPORTED, "C = %d not in {8,16,32,64}", g->C);
     if (n < -1 || (n == -1 && !g->n_dev) || n > g->capacity) return fail(c, TA_ERR_INVALID_ARG, "bad n");
-    cudaSetDevice(c->device);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int64_t cap = n >= 0 ? n : g->capacity;
     RasterConsts rc;
     rc.dilation = p->dilation; rc.alpha_max = p->alpha_max; rc.alpha_min = p->alpha_min; rc.t_eps = p->t_eps;
     rc.cull_sigma = p->cull_sigma; rc.z_near = p->z_near;
     rc.q_max = p->cull_sigma * p->cull_sigma;
-    (void)cap;   // the outputs hold the call's n Gaussians: zeroed on the device from its count
+    // the pass reuses the forward call's records and tile lists: it must be the same Gaussian set,
+    // feature layout, count and constants (a different C would index the feature rows with the wrong
+    // stride); grad_F is read with 16-byte vector loads
+    const int fbytes = g->feat_dtype == TA_F16 ? 2 : 4;
+    if (g->C != c->last_C || fbytes != c->last_fbytes || n != c->last_n || g->feat != c->last_feat ||
+        memcmp(&rc, &c->last_rc, sizeof(rc)) != 0)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_rasterize_backward: C, feature dtype/array, n or params differ from the "
+                                           "preceding ta_rasterize on this context");
+    if ((((uintptr_t)grad_F) | ((uintptr_t)d_feat)) & 15)
+        return fail(c, TA_ERR_INVALID_ARG, "grad_F / d_feat must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
     const CompositeGeom& cg = c->last_cg;
-    cudaError_t e = launch_composite_bwd(g->C, g->feat_dtype == TA_F16 ? 2 : 4, cg.TX * cg.TY, (const uint4*)c->rec.p,
+    cudaError_t e = launch_composite_bwd(g->C, fbytes, cg.TX * cg.TY, c->resident_bwd, c->bwd_simt, (const uint4*)c->rec.p,
                                          g->feat, (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p,
                                          (const uint32_t*)c->tile_order.p, cg, rc,
                                          (CallState*)c->cs.p, (uint64_t)(c->tlist.bytes / 4), grad_F, grad_A,

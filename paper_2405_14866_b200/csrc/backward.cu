@@ -612,21 +612,11 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
 }
 
 template <int C>
-static cudaError_t launch_bwd_tc(int tiles, const uint4* rec, const void* feat, const uint32_t* tlist, const uint2* trng,
+static cudaError_t launch_bwd_tc(int tiles, int resident, const uint4* rec, const void* feat, const uint32_t* tlist, const uint2* trng,
                                  const uint32_t* order, CompositeGeom cg, RasterConsts rc, CallState* cs,
                                  uint64_t list_cap, const float* GF, const float* GA, float* d_mean2, float* d_conic,
                                  float* d_alpha, float* d_feat, cudaStream_t st) {
     const size_t smem = sizeof(BwdBuf<C>);
-    static int resident = 0;
-    if (resident == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_composite_bwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_bwd_tc<C>, 32, smem);
-        resident = std::max(1, sms * std::max(1, per_sm));
-    }
     cudaError_t e = cudaMemsetAsync(&cs->scan_counter[7], 0, 4, st);
     if (e != cudaSuccess) return e;
     k_composite_bwd_tc<C><<<std::min(4 * tiles, resident), 32, smem, st>>>(
@@ -635,19 +625,48 @@ static cudaError_t launch_bwd_tc(int tiles, const uint4* rec, const void* feat, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const uint4* rec, const void* feat, const uint32_t* tlist,
+// Per-device preparation (ta_context_create, the context's device current): shared-memory opt-ins of
+// the backward kernels and the co-resident grid of the persistent tensor-core backward per C.
+template <int C>
+static cudaError_t prepare_bwd_tc(int num_sms, int* resident) {
+    const size_t smem = sizeof(BwdBuf<C>);
+    cudaError_t e = cudaFuncSetAttribute(k_composite_bwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_bwd_tc<C>, 32, smem))) return e;
+    *resident = std::max(1, num_sms * std::max(1, per_sm));
+    return cudaSuccess;
+}
+
+cudaError_t prepare_composite_bwd(int num_sms, int resident[4]) {
+    const int smem = (int)((size_t)kBwdBatch * (16 + 16 + 4 + 4 * (size_t)64));
+    cudaError_t e;
+#define TA_BWD_ATTR(CC)                                                                                                  \
+    if ((e = cudaFuncSetAttribute(k_composite_bwd<CC, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) ||  \
+        (e = cudaFuncSetAttribute(k_composite_bwd<CC, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))      \
+        return e;
+    TA_BWD_ATTR(8) TA_BWD_ATTR(16) TA_BWD_ATTR(32) TA_BWD_ATTR(64)
+#undef TA_BWD_ATTR
+    resident[0] = 1;
+    if ((e = prepare_bwd_tc<16>(num_sms, &resident[1])) || (e = prepare_bwd_tc<32>(num_sms, &resident[2])) ||
+        (e = prepare_bwd_tc<64>(num_sms, &resident[3])))
+        return e;
+    return cudaSuccess;
+}
+
+cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const int* resident, bool simt, const uint4* rec, const void* feat, const uint32_t* tlist,
                                  const uint2* trng, const uint32_t* order, CompositeGeom cg, RasterConsts rc,
                                  CallState* cs, uint64_t list_cap, const float* GF, const float* GA, float* d_mean2,
                                  float* d_conic, float* d_alpha, float* d_feat, cudaStream_t st) {
     const size_t smem = (size_t)kBwdBatch * (16 + 16 + 4 + 4 * (size_t)C);
     k_bwd_zero<<<1184, 256, 0, st>>>(cs, C, d_mean2, d_conic, d_alpha, d_feat);
-    if (fbytes == 2 && tiles > 0 && !getenv("TA_BWD_SIMT")) {
+    if (fbytes == 2 && tiles > 0 && !simt) {
         switch (C) {
-            case 16: return launch_bwd_tc<16>(tiles, rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
+            case 16: return launch_bwd_tc<16>(tiles, resident[1], rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
                                               d_conic, d_alpha, d_feat, st);
-            case 32: return launch_bwd_tc<32>(tiles, rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
+            case 32: return launch_bwd_tc<32>(tiles, resident[2], rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
                                               d_conic, d_alpha, d_feat, st);
-            case 64: return launch_bwd_tc<64>(tiles, rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
+            case 64: return launch_bwd_tc<64>(tiles, resident[3], rec, feat, tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2,
                                               d_conic, d_alpha, d_feat, st);
             default: break;
         }
@@ -655,12 +674,10 @@ cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const uint4* rec,
 #define TA_BWD(CC)                                                                                                      \
     case CC: {                                                                                                          \
         if (fbytes == 2) {                                                                                              \
-            cudaFuncSetAttribute(k_composite_bwd<CC, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
             k_composite_bwd<CC, __half><<<tiles, kBwdThreads, smem, st>>>(rec, static_cast<const __half*>(feat), tlist, \
                                                                           trng, cg, rc, cs, list_cap, GF, GA, d_mean2,  \
                                                                           d_conic, d_alpha, d_feat);                    \
         } else {                                                                                                        \
-            cudaFuncSetAttribute(k_composite_bwd<CC, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
             k_composite_bwd<CC, float><<<tiles, kBwdThreads, smem, st>>>(rec, static_cast<const float*>(feat), tlist,   \
                                                                          trng, cg, rc, cs, list_cap, GF, GA, d_mean2,   \
                                                                          d_conic, d_alpha, d_feat);                     \

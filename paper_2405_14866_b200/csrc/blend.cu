@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(256) k_blend(BlendTable bt, TargetCam cam, con
             ws = fadd(ws, w);
         }
     }
-    // Eq. 10
+    // Eq. 10; no weight at all is a hole even when w_min = 0 (holes are colour 0)
     float o0 = 0.0f, o1 = 0.0f, o2 = 0.0f;
-    if (ws >= bt.w_min) {
+    if (ws > 0.0f && ws >= bt.w_min) {
         o0 = fdiv(acc0, ws); o1 = fdiv(acc1, ws); o2 = fdiv(acc2, ws);
     }
     rgb[(size_t)pix * 3 + 0] = o0;

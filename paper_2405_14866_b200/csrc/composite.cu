@@ -934,29 +934,12 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 }
 
 template <int C>
-static cudaError_t launch_tc(int tiles, const uint4* rec, const void* feat, const uint32_t* list, const uint2* offs,
-                             uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs, uint64_t list_cap,
-                             float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
+static cudaError_t launch_tc(int tiles, int resident, const uint4* rec, const void* feat, const uint32_t* list,
+                             const uint2* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs,
+                             uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
     const size_t smem = sizeof(TcBuf<C>) * kWarps;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_composite_tc<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_composite_tc<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
     if (tiles == 0) return cudaSuccess;
     // persistent warps: as many CTAs as are co-resident (more would only find the block counter spent)
-    static int resident = 0;
-    if (resident == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false>, kThreads, smem);
-        if (const char* e = getenv("TA_TC_CTAS_PER_SM")) per_sm = std::min(per_sm, atoi(e));   // tuning knob
-        resident = std::max(1, sms * std::max(1, per_sm));
-    }
     const int grid = std::min(tiles, resident);
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     const __half* fh = static_cast<const __half*>(feat);
@@ -973,15 +956,6 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
                               const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
                               cudaStream_t st) {
     const size_t smem = sizeof(WarpBuf<C>) * kWarps;
-    static bool attr_set = false;   // per template instance; set once per process
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_composite<C, FT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_composite<C, FT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
     if (tiles == 0) return cudaSuccess;
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     if (ncontrib)
@@ -993,13 +967,46 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
     return cudaGetLastError();
 }
 
-cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
+// Per-device launch preparation (called by ta_context_create with the context's device current):
+// the dynamic shared-memory opt-in of every compositor instantiation (cudaFuncSetAttribute acts on
+// the current device only) and the co-resident CTA count of the persistent tensor-core compositor
+// for each C, capped at ctas_per_sm_cap (> 0) per SM.
+template <int C>
+static cudaError_t prepare_one(int num_sms, int cap, int* resident) {
+    const size_t smem_tc = sizeof(TcBuf<C>) * kWarps, smem = sizeof(WarpBuf<C>) * kWarps;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_composite_tc<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite<C, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_composite<C, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+        return e;
+    int per_sm = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false>, kThreads, smem_tc))) return e;
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    *resident = std::max(1, num_sms * std::max(1, per_sm));
+    return cudaSuccess;
+}
+
+cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[4]) {
+    cudaError_t e;
+    if ((e = prepare_one<8>(num_sms, ctas_per_sm_cap, &resident[0])) ||
+        (e = prepare_one<16>(num_sms, ctas_per_sm_cap, &resident[1])) ||
+        (e = prepare_one<32>(num_sms, ctas_per_sm_cap, &resident[2])) ||
+        (e = prepare_one<64>(num_sms, ctas_per_sm_cap, &resident[3])))
+        return e;
+    return cudaSuccess;
+}
+
+int c_slot(int C) { return C == 8 ? 0 : C == 16 ? 1 : C == 32 ? 2 : 3; }
+
+cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, const uint4* rec, const void* feat,
                              const uint32_t* list, const uint2* offs, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                              int32_t* ncontrib, cudaStream_t st) {
 #define TA_CASE(CC)                                                                                           \
     case CC:                                                                                                  \
-        return fbytes == 2 ? launch_tc<CC>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st) \
+        return fbytes == 2 ? launch_tc<CC>(tiles, resident[c_slot(CC)], rec, feat, list, offs, order, cg, rc, cs, list_cap, F, \
+                                           A, ncontrib, st)                                                   \
                            : launch_one<CC, float>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st);
     switch (C) {
         TA_CASE(8)

@@ -85,12 +85,17 @@ struct CompositeGeom {
 void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
                        const CallState* cs, uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng,
                        cudaStream_t st);
-cudaError_t launch_composite(int C, int fbytes, int tiles, const uint4* rec, const void* feat,
+// per-device preparation (ta_context_create): shared-memory opt-ins + persistent grid sizes per C
+// (slot c_slot(C): C = 8, 16, 32, 64)
+cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[4]);
+int c_slot(int C);
+cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, const uint4* rec, const void* feat,
                              const uint32_t* tlist, const uint2* trng, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                              int32_t* ncontrib, cudaStream_t st);
 // backward.cu
-cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const uint4* rec, const void* feat, const uint32_t* tlist,
+cudaError_t prepare_composite_bwd(int num_sms, int resident[4]);
+cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const int* resident, bool simt, const uint4* rec, const void* feat, const uint32_t* tlist,
                                  const uint2* trng, const uint32_t* order, CompositeGeom cg, RasterConsts rc,
                                  CallState* cs, uint64_t list_cap, const float* GF, const float* GA, float* d_mean2,
                                  float* d_conic, float* d_alpha, float* d_feat, cudaStream_t st);

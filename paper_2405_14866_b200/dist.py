@@ -10,7 +10,7 @@ Everything here works with any backend (NCCL on GPUs, gloo on CPU for the tests)
 """
 from __future__ import annotations
 
-from typing import List, Sequence
+from typing import List, Optional, Sequence
 
 
 def shard(n_items: int, rank: int, world: int) -> List[int]:
@@ -20,26 +20,49 @@ def shard(n_items: int, rank: int, world: int) -> List[int]:
     return list(range(rank * n_items // world, (rank + 1) * n_items // world))
 
 
-def broadcast_gaussians(tensors: Sequence, n_dev, src: int = 0, group=None) -> int:
-    """Broadcast a Gaussian set from `src`: first the device count n (int64 tensor [1]), then the
-    first n rows of each array in `tensors` (pos_alpha, cov, feat).  Returns n."""
+def broadcast_gaussians(tensors: Sequence, n_dev, src: int = 0, group=None, rows: Optional[int] = None) -> Optional[int]:
+    """Broadcast a Gaussian set from `src`: the device count n (int64 tensor [1]) and the leading rows of
+    each array in `tensors` (pos_alpha, cov, feat).
+
+    With `rows` (a host-side upper bound on n, e.g. the previous frame's count; rows >= n is the
+    caller's contract) nothing is read back to the host: the first `rows` rows are broadcast and the
+    receivers' ta_rasterize(n = -1) reads the true n from the broadcast n_dev, so the call is fully
+    stream-ordered.  Without it, n is read back (one host synchronisation) and exactly n rows are sent.
+    Returns n when it was read back, else None."""
     import torch.distributed as dist
     dist.broadcast(n_dev, src, group=group)
-    n = int(n_dev.item())
+    n = rows
+    if n is None:
+        n = int(n_dev.item())
     for t in tensors:
         if n:
             dist.broadcast(t[:n], src, group=group)
-    return n
+    return None if rows is not None else n
 
 
 def gather_views(local_views: Sequence, n_views: int, rank: int, world: int, dst: int = 0, group=None):
     """Gather every rank's rendered views (tensors of identical shape) to `dst` in global view
-    order; returns the list of n_views tensors on dst, None elsewhere.  Uses point-to-point
-    send/recv so per-rank counts may differ by one."""
+    order; returns the list of n_views tensors on dst, None elsewhere.  When every rank holds the same
+    number of views (n_views % world == 0) this is one collective gather (ncclGather over NVLink /
+    NVSwitch on GPUs: rank 0's ingress carries (world-1)/world of the bytes) per local view slot;
+    otherwise point-to-point send/recv (per-rank counts differ by one)."""
     import torch
     import torch.distributed as dist
     if world == 1:
         return list(local_views)
+    if n_views % world == 0:
+        per = n_views // world
+        out = [None] * n_views if rank == dst else None
+        for k in range(per):
+            t = local_views[k].contiguous()
+            if rank == dst:
+                bufs = [t if r == dst else torch.empty_like(t) for r in range(world)]
+                dist.gather(t, gather_list=bufs, dst=dst, group=group)
+                for r in range(world):
+                    out[r * per + k] = bufs[r]
+            else:
+                dist.gather(t, dst=dst, group=group)
+        return out
     if rank == dst:
         out = [None] * n_views
         for r in range(world):

@@ -38,7 +38,7 @@ def oracle_params(scene, **kw):
     return oracle.make_params(default_scale=scene.default_scale, default_opacity=scene.default_opacity, **kw)
 
 
-def gpu_params(scene, flags=2, **kw):
+def gpu_params(scene, flags=0, **kw):
     import paper_2405_14866_b200 as tb
     return tb.default_params(default_scale=scene.default_scale, default_opacity=scene.default_opacity, flags=flags,
                              **kw)
@@ -60,8 +60,12 @@ def gaussians_to_host(g):
                 feat=g.feat[:n].cpu().numpy())
 
 
-def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True):
-    """Rasterize and pull every stage's output back to the host."""
+def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True, counts=True):
+    """Rasterize with `params` as given -- by default flags = 0, the compositor instantiation bench.py
+    times -- and pull every stage's output back to the host.  With `counts`, the same call is
+    repeated with TA_FLAG_DEBUG_COUNTS added (the counters instantiation): its F and A must be
+    bit-identical to the timed call, and its per-pixel composited-pair counts are returned."""
+    import ctypes
     import torch
     import paper_2405_14866_b200 as tb
     K, R, t = sg.cam_arrays(cam)
@@ -82,6 +86,17 @@ def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True):
     out["list"] = d2h(d.tile_list, d.K, np.uint32)
     if d.n_contrib:
         out["n_contrib"] = d2h(d.n_contrib, cam.H * cam.W, np.int32).reshape(cam.H, cam.W)
+    elif counts:
+        pc = tb.default_params()
+        ctypes.memmove(ctypes.byref(pc), ctypes.byref(params), ctypes.sizeof(pc))
+        pc.flags = params.flags | tb.TA_FLAG_DEBUG_COUNTS
+        F2, A2 = tb.rasterize(ctx, g, K, R, t, cam.H, cam.W, pc, n=n)
+        torch.cuda.synchronize()
+        assert torch.equal(F2.view(torch.int32), F.view(torch.int32)), "counters instantiation changed F"
+        assert torch.equal(A2.view(torch.int32), A.view(torch.int32)), "counters instantiation changed A"
+        d2 = ctx.debug_last()
+        out["n_contrib"] = d2h(d2.n_contrib, cam.H * cam.W, np.int32).reshape(cam.H, cam.W)
+        out["work"] = list(d2.work)
     return out
 
 

@@ -56,7 +56,7 @@ def test_defaults_and_status_strings():
     p = tb.default_params()
     assert abs(p.dilation - 0.3) < 1e-7 and abs(p.alpha_max - 0.99) < 1e-7
     assert p.alpha_min == ctypes.c_float(1.0 / 255.0).value and p.t_eps == ctypes.c_float(1e-4).value
-    assert p.cull_sigma == 3.0 and p.flags == 0
+    assert p.cull_sigma == 3.0 and p.flags == 0 and p.exact_exp == 1
     L = tb.lib()
     assert L.ta_status_string(0) == b"TA_OK" and L.ta_status_string(5) == b"TA_ERR_CAPACITY"
     assert b"sm_100a" in L.ta_build_info()

@@ -111,3 +111,16 @@ def test_identity_view_and_errors(ctx):
         with pytest.raises(tb.TaError):
             ctx.blend(structs, [c], tb.default_params(), tb.default_blend_params(**bad), tb.intrinsics(K),
                       tb.extrinsics(R, t), 64, 64, z, out)
+
+
+def test_w_min_zero_background_is_zero_not_nan(ctx):
+    """w_min = 0: pixels without any weight (background, z_fused = 0) are holes of colour 0 on the GPU
+    too (no 0/0), bit-exact against the oracle."""
+    s = sg.make_config("c3", res=96)
+    cam = sg.make_targets("c4", res=96, n_targets=3)[1]
+    colors = [sg.view_colors(v.cam) for v in s.views]
+    zf, rgb, ws = gpu_blend(ctx, s.views, colors, cam, w_min=0.0)
+    zo, ro, wo = oracle_blend(s.views, colors, cam, w_min=0.0)
+    assert np.all(np.isfinite(rgb)) and (ws == 0).sum() > 100
+    check_bits(ws, wo)
+    check_bits(rgb, ro)

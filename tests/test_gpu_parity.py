@@ -28,7 +28,12 @@ def oracle_lib():
     return oracle
 
 
-def full_parity(ctx, O, scene, tidx=0, tiles=None, **pkw):
+def full_parity(ctx, O, scene, tidx=0, tiles=None, async_=False, **pkw):
+    """Every stage of the CUDA path against the oracle on one scene and target.  The rasterize call
+    runs the instantiation bench.py times (flags = 0; with async_, TA_FLAG_ASYNC on a context sized
+    by ta_reserve as in bench.py), then again with TA_FLAG_DEBUG_COUNTS, which must give the same bits
+    (tests/_parity.gpu_rasterize)."""
+    import paper_2405_14866_b200 as tb
     gp = P.gpu_params(scene, **pkw)
     op = P.oracle_params(scene, **pkw)
     g = P.gpu_unproject(ctx, scene, gp)
@@ -36,7 +41,15 @@ def full_parity(ctx, O, scene, tidx=0, tiles=None, **pkw):
     go = O.unproject(scene, op)
     P.check_unproject(gh, go)
     cam = scene.targets[tidx]
-    out = P.gpu_rasterize(ctx, g, cam, gp)
+    rctx = ctx
+    if async_:
+        sizing = P.gpu_rasterize(ctx, g, cam, gp, counts=False)
+        rctx = tb.Context(0)
+        rctx.reserve(g.capacity, max(int(sizing["Kc"] * 1.05), 1) + 1024, cam.H, cam.W)
+        gp = P.gpu_params(scene, flags=tb.TA_FLAG_ASYNC, **pkw)
+    out = P.gpu_rasterize(rctx, g, cam, gp)
+    if async_:
+        assert not rctx.check_overflow()
     K, R, t = sg.cam_arrays(cam)
     pr = O.project(go, K, R, t, cam.H, cam.W, op)
     P.check_project(out, pr, go["alpha"])
@@ -46,6 +59,16 @@ def full_parity(ctx, O, scene, tidx=0, tiles=None, **pkw):
     F, A, nc, _ = O.composite(go, pr, ranges, lst, cam.H, cam.W, op, tiles=tiles)
     err = P.check_composite(out, F, A, nc, tiles=tiles, tx=(cam.W + 15) // 16)
     return out, err
+
+
+def sample_tiles(ranges, TX, n_longest, n_random, seed):
+    """The n_longest longest tile lists, n_random seeded random non-empty tiles and the 4 corners."""
+    lens = ranges[:, 1].astype(np.int64) - ranges[:, 0]
+    nonempty = np.nonzero(lens)[0]
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([np.argsort(lens, kind="stable")[-n_longest:],
+                                     rng.choice(nonempty, min(n_random, len(nonempty)), replace=False),
+                                     [0, TX - 1, len(lens) - TX, len(lens) - 1]])).astype(np.int32)
 
 
 def test_tiny_config(ctx, oracle_lib):
@@ -68,31 +91,104 @@ def test_c2_full(ctx, oracle_lib):
     full_parity(ctx, oracle_lib, sg.make_config("c2"))
 
 
+def test_c2_full_async(ctx, oracle_lib):
+    """configs[1] in bench.py's launch mode: TA_FLAG_ASYNC on a ta_reserve'd context (no host
+    synchronisation inside ta_rasterize) -- every stage, every pixel against the oracle."""
+    full_parity(ctx, oracle_lib, sg.make_config("c2"), async_=True)
+
+
 def test_c3_reduced_ragged(ctx, oracle_lib):
     """configs[2] distributions at 256^2 sources, ragged 200 x 136 target."""
     full_parity(ctx, oracle_lib, sg.make_config("c3", res=256, target_hw=(136, 200)))
 
 
-def test_c3_full_size_sampled_tiles(ctx, oracle_lib):
-    """configs[2] at full size (4 x 1024^2, ~1.67M Gaussians, 1024^2 target) in the launch
-    configuration bench.py times: a1-a5 bit-exact in full; a6 on sampled tiles incl. the longest lists."""
-    s = sg.make_config("c3")
-    cam = s.targets[0]
-    TX = (cam.W + 15) // 16
-    # tiles: the 8 longest lists + 24 seeded random non-empty tiles + the 4 corners
+def _c3_sampled_tiles(s, cam, n_longest=16, n_random=48, seed=0):
     import oracle as O
     op = P.oracle_params(s)
     go = O.unproject(s, op)
     K, R, t = sg.cam_arrays(cam)
     pr = O.project(go, K, R, t, cam.H, cam.W, op)
     ranges, _ = O.tile_lists(pr, go["ids"], cam.H, cam.W)
-    lens = ranges[:, 1].astype(np.int64) - ranges[:, 0]
-    nonempty = np.nonzero(lens)[0]
-    rng = np.random.default_rng(0)
-    tiles = np.unique(np.concatenate([np.argsort(lens)[-8:], rng.choice(nonempty, 24, replace=False),
-                                      [0, TX - 1, len(lens) - TX, len(lens) - 1]])).astype(np.int32)
-    out, err = full_parity(ctx, oracle_lib, s, tiles=tiles)
+    return sample_tiles(ranges, (cam.W + 15) // 16, n_longest, n_random, seed)
+
+
+@pytest.mark.parametrize("async_", [False, True])
+def test_c3_full_size_sampled_tiles(ctx, oracle_lib, async_):
+    """configs[2] at full size (4 x 1024^2, ~1.67M Gaussians, 1024^2 target) in the launch
+    configuration bench.py times (flags = 0, and TA_FLAG_ASYNC after ta_reserve): a1-a5 bit-exact in
+    full; a6 on 68 sampled tiles incl. the 16 longest lists, every stage checked against the oracle."""
+    s = sg.make_config("c3")
+    tiles = _c3_sampled_tiles(s, s.targets[0])
+    assert len(tiles) >= 64
+    out, err = full_parity(ctx, oracle_lib, s, tiles=tiles, async_=async_)
     assert out["n"] == 1666464
+
+
+def test_c3_frame_timed_equals_counters_instantiation(ctx):
+    """A whole c3 frame (1024^2, C = 32 fp16) rendered by the timed compositor instantiation
+    (flags = 0) and by the counters instantiation (TA_FLAG_DEBUG_COUNTS) is bit-identical in F and A
+    at every pixel (the oracle comparisons run both; this pins it on the full frame)."""
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("c3")
+    g = P.gpu_unproject(ctx, s, P.gpu_params(s))
+    K, R, t = sg.cam_arrays(s.targets[0])
+    F0, A0 = tb.rasterize(ctx, g, K, R, t, 1024, 1024, P.gpu_params(s, flags=0))
+    F2, A2 = tb.rasterize(ctx, g, K, R, t, 1024, 1024, P.gpu_params(s, flags=tb.TA_FLAG_DEBUG_COUNTS))
+    torch.cuda.synchronize()
+    assert torch.equal(F0.view(torch.int32), F2.view(torch.int32))
+    assert torch.equal(A0.view(torch.int32), A2.view(torch.int32))
+    assert float(A0.max()) > 0.9
+
+
+def test_c4_bench_targets_full_size(ctx, oracle_lib):
+    """configs[3] exactly as bench.py renders it: the full c3 Gaussian set (4 x 1024^2 sources) into 4
+    of the 32 parallax targets (phi = -15, -5.3, +5.3, +15 deg) at 1024^2, TA_FLAG_ASYNC on reserved
+    contexts over 4 CUDA streams with overlapping views.  Per target: records, order and every tile
+    list bit-exact; F / A / composited counts on 40 sampled tiles (incl. the 12 longest lists)."""
+    import torch
+    import oracle as O
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("c3")
+    targets = sg.make_targets("c4")
+    picks = [0, 10, 21, 31]
+    gp = P.gpu_params(s)
+    op = P.oracle_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    go = O.unproject(s, op)
+    kc = 0
+    for j in picks:
+        P.gpu_rasterize(ctx, g, targets[j], gp, debug=False)
+        kc = max(kc, ctx.debug_last().Kc)
+    ctxs = [tb.Context(0) for _ in picks]
+    streams = [torch.cuda.Stream() for _ in picks]
+    pa = P.gpu_params(s, flags=tb.TA_FLAG_ASYNC)
+    outs = []
+    for cx, st, j in zip(ctxs, streams, picks):
+        cx.reserve(g.capacity, int(kc * 1.05) + 4096, 1024, 1024)
+    torch.cuda.synchronize()
+    for cx, st, j in zip(ctxs, streams, picks):        # overlapping views, as in bench.py
+        K, R, t = sg.cam_arrays(targets[j])
+        F = torch.empty((1024, 1024, s.C), device="cuda")
+        A = torch.empty((1024, 1024), device="cuda")
+        cx.rasterize(g, -1, tb.intrinsics(K), tb.extrinsics(R, t), 1024, 1024, pa, F, A, st)
+        outs.append((F, A))
+    torch.cuda.synchronize()
+    for cx, j, (F, A) in zip(ctxs, picks, outs):
+        assert not cx.check_overflow()
+        cam = targets[j]
+        out = P.gpu_rasterize(cx, g, cam, pa)          # debug views of this target (same async call)
+        assert np.array_equal(out["F"].view(np.uint32), F.cpu().numpy().view(np.uint32))
+        assert np.array_equal(out["A"].view(np.uint32), A.cpu().numpy().view(np.uint32))
+        K, R, t = sg.cam_arrays(cam)
+        pr = O.project(go, K, R, t, cam.H, cam.W, op)
+        P.check_project(out, pr, go["alpha"])
+        P.check_order(out, pr, go["ids"])
+        ranges, lst = O.tile_lists(pr, go["ids"], cam.H, cam.W)
+        P.check_lists(out, ranges, lst)
+        tiles = sample_tiles(ranges, 64, 12, 24, j)
+        Fo, Ao, nc, _ = O.composite(go, pr, ranges, lst, cam.H, cam.W, op, tiles=tiles)
+        P.check_composite(out, Fo, Ao, nc, tiles=tiles, tx=64)
 
 
 def test_wide_target_64px_coarse_bins(ctx, oracle_lib):

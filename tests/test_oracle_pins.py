@@ -583,6 +583,22 @@ def test_blend_two_views_equal_weights_average(oracle_lib):
     assert np.allclose(rgb[2:7, 2:7], np.float32([0.4, 0.3, 0.3]), atol=1e-7)
 
 
+def test_blend_zero_weight_is_hole_even_with_w_min_zero(oracle_lib):
+    """S:308 / S:333: a pixel with no valid sample is a hole of colour 0 -- also when the hole
+    threshold w_min is 0 (no 0/0): background pixels of the rig (z_fused = 0) and pixels no view sees
+    stay exactly 0 and finite."""
+    import oracle
+    s = sg.make_config("c3", res=96)
+    cam = sg.make_targets("c4", res=96, n_targets=3)[1]
+    colors = [sg.view_colors(v.cam) for v in s.views]
+    _, zf, _ = oracle.zbuffer(s.views, cam, 0.1, radius=1)
+    rgb, ws = oracle.blend(s.views, colors, cam, zf, w_min=0.0)
+    assert np.all(np.isfinite(rgb))
+    assert (ws == 0).sum() > 100 and np.all(rgb[ws == 0] == 0.0)
+    rgb1, _ = oracle.blend(s.views, colors, cam, zf)
+    assert np.array_equal(rgb[ws >= 1e-4], rgb1[ws >= 1e-4])
+
+
 def test_blend_textured_body_psnr_and_convexity(oracle_lib):
     """S:312 (derived): the occlusion-free Lambertian synthetic scene (the world-space texture on the
     upper body) blended from the 4 rig views into a parallax target matches the texture at the
@@ -677,3 +693,82 @@ def test_backward_matches_finite_differences(oracle_lib):
             assert abs(fd - an[idx]) <= 2e-3 * max(1.0, abs(fd)), (name, idx, fd, an[idx])
             checked += 1
     assert checked >= 16, checked
+
+
+# ------------------------------------------------------------------------------ R8: the box is a conservative 3-sigma bound
+
+def _min_q_outside_box(rect, mean, conic, H, W):
+    """Smallest q = d^T conic d over the image pixels OUTSIDE each Gaussian's pixel box, in float64.
+    q is convex and the centre lies inside the box (R18 rounding), so on each half-plane beyond a box
+    edge the minimum is on the pixel line next to that edge; along the line it is at one of the two
+    integers around the continuous minimiser (clamped to the image).  Edges on the image border have
+    no outside pixels.  Returns one value per Gaussian (inf if the box covers the whole image)."""
+    x0, x1, y0, y1 = (rect[:, k].astype(np.float64) for k in range(4))
+    mx, my = mean[:, 0], mean[:, 1]
+    a, b, c = conic[:, 0, 0], conic[:, 0, 1], conic[:, 1, 1]
+    best = np.full(len(rect), np.inf)
+
+    def along(fixed, is_x, ok):
+        # points (fixed, y) (is_x) or (x, fixed); minimiser of the other coordinate, clamped
+        if is_x:
+            dx = fixed - mx
+            ys = my - b * dx / c
+            for yy in (np.floor(ys), np.ceil(ys)):
+                dy = np.clip(yy, 0, H - 1) - my
+                q = a * dx * dx + 2 * b * dx * dy + c * dy * dy
+                np.minimum(best, np.where(ok, q, np.inf), out=best)
+        else:
+            dy = fixed - my
+            xs = mx - b * dy / a
+            for xx in (np.floor(xs), np.ceil(xs)):
+                dx = np.clip(xx, 0, W - 1) - mx
+                q = a * dx * dx + 2 * b * dx * dy + c * dy * dy
+                np.minimum(best, np.where(ok, q, np.inf), out=best)
+
+    along(x0 - 1, True, x0 > 0)
+    along(x1 + 1, True, x1 < W - 1)
+    along(y0 - 1, False, y0 > 0)
+    along(y1 + 1, False, y1 < H - 1)
+    return best
+
+
+def _r8_margin(oracle_lib, scene, cam):
+    """fp32 oracle boxes (a2) vs the exact float64 ellipse of definition64: min q outside the boxes."""
+    from oracle import definition64 as D
+    go = oracle_lib.unproject(scene)
+    K, R, t = sg.cam_arrays(cam)
+    pr = oracle_lib.project(go, K, R, t, cam.H, cam.W)
+    g64 = D.unproject(scene)
+    p64 = D.project(g64, cam)
+    vis = pr["visible"].astype(bool)
+    assert vis.sum() > 0
+    assert np.all(p64["visible"][vis]), "fp32-visible Gaussian culled in float64"
+    conic = np.linalg.inv(p64["cov2"][vis])
+    q = _min_q_outside_box(pr["rect"][vis].astype(np.int64), p64["mean"][vis], conic, cam.H, cam.W)
+    return float(q.min()), int(vis.sum())
+
+
+@pytest.mark.parametrize("cfg,res", [("c2", 512), ("c3", 512), ("c5", 512)])
+def test_r8_box_conservative_rig(oracle_lib, cfg, res):
+    """DESIGN.md R8 / R18: the fp32 pixel box (h = 3 sqrt(Sigma'_xx)(1 + 2^-10) + 2^-10) contains every
+    pixel whose exact (float64) Mahalanobis q is <= 9, so including the box in the inclusion predicate
+    never drops a 3-sigma pixel: on the c2-, c3- and c5-shaped rigs (anisotropic, random rotations)
+    every pixel outside every visible Gaussian's box has float64 q > 9."""
+    s = sg.make_config(cfg, res=res, n_targets=1) if cfg == "c5" else sg.make_config(cfg, res=res)
+    qmin, nvis = _r8_margin(oracle_lib, s, s.targets[0])
+    assert nvis > 10000
+    assert qmin > 9.0, qmin
+
+
+def test_r8_box_conservative_random_anisotropic(oracle_lib):
+    """R8 on 24 random anisotropic scenes (random rotations, log-normal scales), 8 of them with one
+    axis stretched x 8 (needle-like footprints at every orientation): no pixel outside an fp32 box
+    has float64 q <= 9."""
+    worst = np.inf
+    for seed in range(24):
+        s = sg.make_random_scene(seed, H=40 + seed, W=64 - seed, n_src=20)
+        if seed % 3 == 0:
+            s.views[0].scale[..., seed % 3] *= 8.0
+        qmin, _ = _r8_margin(oracle_lib, s, s.targets[0])
+        worst = min(worst, qmin)
+    assert worst > 9.0, worst

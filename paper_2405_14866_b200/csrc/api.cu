@@ -33,7 +33,9 @@ struct ta_context {
     size_t smem_optin = 0;
     // per-context launch configuration (ta_context_create, on this context's device): persistent grid
     // sizes of the compositor / backward per C slot, and the tuning knobs read once from the environment
-    int resident_tc[4] = {1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1};
+    int resident_tc[4] = {1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1}, resident_tm[4] = {0, 1, 1, 1};
+    int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default), 2 = tensor-memory kernel
+                                  // (tcgen05.mma, fp16 C >= 16; measured slower)
     int coarse64_above = 1024;    // TA_COARSE64_ABOVE: 64-px coarse bins for targets wider / taller than this
     bool bwd_simt = false;        // TA_BWD_SIMT: force the plain backward kernel
     std::string err;
@@ -239,7 +241,10 @@ ta_status ta_context_create(int32_t device, ta_context** out) {
     if (const char* e = getenv("TA_COARSE64_ABOVE")) c->coarse64_above = atoi(e);   // tuning knobs
     c->bwd_simt = getenv("TA_BWD_SIMT") != nullptr;
     const int cap = getenv("TA_TC_CTAS_PER_SM") ? atoi(getenv("TA_TC_CTAS_PER_SM")) : 0;
+    if (const char* e = getenv("TA_COMPOSITOR")) c->compositor = atoi(e);
+    const int cap_tm = getenv("TA_TM_CTAS_PER_SM") ? atoi(getenv("TA_TM_CTAS_PER_SM")) : 0;
     if (prepare_composite(c->num_sms, cap, c->resident_tc) != cudaSuccess ||
+        prepare_composite_tm(c->num_sms, cap_tm, c->resident_tm) != cudaSuccess ||
         prepare_composite_bwd(c->num_sms, c->resident_bwd) != cudaSuccess) {
         cudaGetLastError();
         cudaFreeHost(c->pinned);
@@ -609,10 +614,22 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     TA_LAUNCHED(c);
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);
-    cudaError_t e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, c->resident_tc, rec, g->feat, (const uint32_t*)c->tlist.p,
-                                     (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
-                                     (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
-                                     counts ? (int32_t*)c->ncontrib.p : nullptr, s);
+    cudaError_t e;
+    if (g->feat_dtype == TA_F16 && g->C >= 16 && c->compositor == 2) {
+        // tensor-memory compositor (tcgen05.mma, accumulators in TMEM); exact_exp = 0 selects its SFU exp
+        if (T > 0) launch_tile_order((const uint2*)c->trng.p, cg, (uint32_t*)c->tile_order.p, s);
+        e = T > 0 ? launch_composite_tm(g->C, T, c->resident_tm, fast_exp, rec, g->feat, (const uint32_t*)c->tlist.p,
+                                        (const uint2*)c->trng.p, (const uint32_t*)c->tile_order.p, cg, rc, cs,
+                                        (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
+                                        counts ? (int32_t*)c->ncontrib.p : nullptr, s)
+                  : cudaSuccess;
+    } else {
+        // persistent-warp compositors: mma.sync (fp16 features) / SIMT (fp32 features)
+        e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, c->resident_tc, fast_exp, rec, g->feat,
+                             (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
+                             (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
+                             counts ? (int32_t*)c->ncontrib.p : nullptr, s);
+    }
     if (e != cudaSuccess) return cuda_fail(c, e, "composite launch");
     c->launches += 2;   // k_tile_order + k_composite
     tm.end();

@@ -112,7 +112,7 @@ struct WarpBuf {
 // reach its still-active pixels (conservative), stages them in a warp-private shared buffer (splat
 // record + fp32 feature row) and composites them; the 4 warps of a tile share the list reads
 // through L1.
-template <int C, typename FT, bool kCounts>
+template <int C, typename FT, bool kCounts, bool kFast>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 2 : 4))
 k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const uint32_t* __restrict__ clist,
             const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
@@ -241,7 +241,7 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
             if (kCounts) wk[2] += 1;
             if (!__any_sync(0xffffffffu, inA || inB)) continue;
             if (kCounts) wk[3] += 1;
-            const float2 e = exp_det2(mul2(bc2(-0.5f), q));
+            const float2 e = exp2v<kFast>(mul2(bc2(-0.5f), q));
             const float2 ae = mul2(bc2(G2.y), e);
             const float2 a = make_float2(fminf(rc.alpha_max, ae.x), fminf(rc.alpha_max, ae.y));
             inA = inA && a.x >= rc.alpha_min;
@@ -516,7 +516,7 @@ constexpr bool kSkipEmptyPairs = false;
 #endif
 constexpr int kTcMinBlocks = TA_TC_MIN_BLOCKS;   // CTAs per SM the register budget targets
 
-template <int C, bool kCounts>
+template <int C, bool kCounts, bool kFast>
 __global__ void __launch_bounds__(kThreads, (C >= 64 ? 3 : kTcMinBlocks))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
                const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
@@ -758,7 +758,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                             const float qm1 = (act1 && has1 && ((b1 >> ol) & 1u)) ? q.y : -kInf;
                             if (kCounts) wk[2] += has1 ? 2 : 1;
                             if (!kSkipEmptyPairs || __any_sync(0xffffffffu, fmaxf(qm0, qm1) >= qlo)) {
-                                const float2 e = exp_det2(q);
+                                const float2 e = exp2v<kFast>(q);
                                 const float2 ae = mul2(make_float2(P2.z, P2.w), e);             // 2^11 alpha e
                                 const float2 a = make_float2(fminf(amx, ae.x), fminf(amx, ae.y)); // 2^11 alpha'
                                 const float2 om = fma2(a, bc2(-1.0f / 2048.0f), bc2(1.0f));      // fl(1 - alpha')
@@ -814,8 +814,8 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                                 if (kCounts) wk[2] += has1 ? 2 : 1;
                                 if (!kSkipEmptyPairs || __any_sync(0xffffffffu, ((mA0 | mA1) & actA) | ((mB0 | mB1) & actB))) {
                                     // exp / alpha' of both entries are independent of T: computed side by side
-                                    const float2 x0 = exp_det2(q0);
-                                    const float2 x1 = exp_det2(q1);
+                                    const float2 x0 = exp2v<kFast>(q0);
+                                    const float2 x1 = exp2v<kFast>(q1);
                                     const float2 ae0 = mul2(bc2(H0.y), x0), ae1 = mul2(bc2(H1.y), x1);   // 2^11 alpha e
                                     const float2 a0 = make_float2(fminf(amx, ae0.x), fminf(amx, ae0.y));
                                     const float2 a1 = make_float2(fminf(amx, ae1.x), fminf(amx, ae1.y));
@@ -934,7 +934,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 }
 
 template <int C>
-static cudaError_t launch_tc(int tiles, int resident, const uint4* rec, const void* feat, const uint32_t* list,
+static cudaError_t launch_tc(int tiles, int resident, bool fast, const uint4* rec, const void* feat, const uint32_t* list,
                              const uint2* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs,
                              uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
     const size_t smem = sizeof(TcBuf<C>) * kWarps;
@@ -943,27 +943,32 @@ static cudaError_t launch_tc(int tiles, int resident, const uint4* rec, const vo
     const int grid = std::min(tiles, resident);
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     const __half* fh = static_cast<const __half*>(feat);
-    if (ncontrib)
-        k_composite_tc<C, true><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
-    else
-        k_composite_tc<C, false><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib);
+#define TA_TC(K, FA) k_composite_tc<C, K, FA><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib)
+    if (ncontrib) {
+        if (fast) TA_TC(true, true); else TA_TC(true, false);
+    } else {
+        if (fast) TA_TC(false, true); else TA_TC(false, false);
+    }
+#undef TA_TC
     return cudaGetLastError();
 }
 
 template <int C, typename FT>
-static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, const uint32_t* list,
+static cudaError_t launch_one(int tiles, bool fast, const uint4* rec, const void* feat, const uint32_t* list,
                               const uint2* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc,
                               const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
                               cudaStream_t st) {
     const size_t smem = sizeof(WarpBuf<C>) * kWarps;
     if (tiles == 0) return cudaSuccess;
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
-    if (ncontrib)
-        k_composite<C, FT, true><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, order, cg,
-                                                               rc, cs, list_cap, F, A, ncontrib);
-    else
-        k_composite<C, FT, false><<<tiles, kThreads, smem, st>>>(rec, static_cast<const FT*>(feat), list, offs, order,
-                                                                cg, rc, cs, list_cap, F, A, ncontrib);
+    const FT* ff = static_cast<const FT*>(feat);
+#define TA_ONE(K, FA) k_composite<C, FT, K, FA><<<tiles, kThreads, smem, st>>>(rec, ff, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib)
+    if (ncontrib) {
+        if (fast) TA_ONE(true, true); else TA_ONE(true, false);
+    } else {
+        if (fast) TA_ONE(false, true); else TA_ONE(false, false);
+    }
+#undef TA_ONE
     return cudaGetLastError();
 }
 
@@ -973,15 +978,20 @@ static cudaError_t launch_one(int tiles, const uint4* rec, const void* feat, con
 // for each C, capped at ctas_per_sm_cap (> 0) per SM.
 template <int C>
 static cudaError_t prepare_one(int num_sms, int cap, int* resident) {
-    const size_t smem_tc = sizeof(TcBuf<C>) * kWarps, smem = sizeof(WarpBuf<C>) * kWarps;
+    const int smem_tc = (int)(sizeof(TcBuf<C>) * kWarps), smem = (int)(sizeof(WarpBuf<C>) * kWarps);
+    const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_composite_tc<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc)) ||
-        (e = cudaFuncSetAttribute(k_composite_tc<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc)) ||
-        (e = cudaFuncSetAttribute(k_composite<C, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_composite<C, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+    if ((e = cudaFuncSetAttribute(k_composite_tc<C, false, false>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true, false>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, false, true>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true, true>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite<C, float, false, false>, A, smem)) ||
+        (e = cudaFuncSetAttribute(k_composite<C, float, true, false>, A, smem)) ||
+        (e = cudaFuncSetAttribute(k_composite<C, float, false, true>, A, smem)) ||
+        (e = cudaFuncSetAttribute(k_composite<C, float, true, true>, A, smem)))
         return e;
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false>, kThreads, smem_tc))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false, false>, kThreads, smem_tc))) return e;
     if (cap > 0) per_sm = std::min(per_sm, cap);
     *resident = std::max(1, num_sms * std::max(1, per_sm));
     return cudaSuccess;
@@ -997,17 +1007,22 @@ cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[4])
     return cudaSuccess;
 }
 
+void launch_tile_order(const uint2* trng, CompositeGeom cg, uint32_t* order, cudaStream_t st) {
+    k_tile_order<<<1, 1024, 0, st>>>(trng, cg, order);
+}
+
 int c_slot(int C) { return C == 8 ? 0 : C == 16 ? 1 : C == 32 ? 2 : 3; }
 
-cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, const uint4* rec, const void* feat,
-                             const uint32_t* list, const uint2* offs, uint32_t* order, CompositeGeom cg,
+cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, bool fast, const uint4* rec,
+                             const void* feat, const uint32_t* list, const uint2* offs, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                              int32_t* ncontrib, cudaStream_t st) {
-#define TA_CASE(CC)                                                                                           \
-    case CC:                                                                                                  \
-        return fbytes == 2 ? launch_tc<CC>(tiles, resident[c_slot(CC)], rec, feat, list, offs, order, cg, rc, cs, list_cap, F, \
-                                           A, ncontrib, st)                                                   \
-                           : launch_one<CC, float>(tiles, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib, st);
+#define TA_CASE(CC)                                                                                              \
+    case CC:                                                                                                     \
+        return fbytes == 2 ? launch_tc<CC>(tiles, resident[c_slot(CC)], fast, rec, feat, list, offs, order, cg, rc, cs, \
+                                           list_cap, F, A, ncontrib, st)                                         \
+                           : launch_one<CC, float>(tiles, fast, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, \
+                                                   ncontrib, st);
     switch (C) {
         TA_CASE(8)
         TA_CASE(16)

@@ -89,10 +89,18 @@ void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGe
 // (slot c_slot(C): C = 8, 16, 32, 64)
 cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[4]);
 int c_slot(int C);
-cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, const uint4* rec, const void* feat,
+cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, bool fast_exp, const uint4* rec, const void* feat,
                              const uint32_t* tlist, const uint2* trng, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                              int32_t* ncontrib, cudaStream_t st);
+// heaviest-first tile order (by list length) for the persistent compositors
+void launch_tile_order(const uint2* trng, CompositeGeom cg, uint32_t* order, cudaStream_t st);
+// composite_tm.cu: tensor-memory compositor (fp16 features, C in {16, 32, 64}); resident[c_slot(C)]
+cudaError_t prepare_composite_tm(int num_sms, int ctas_per_sm_cap, int resident[4]);
+cudaError_t launch_composite_tm(int C, int tiles, const int* resident, bool fast_exp, const uint4* rec, const void* feat,
+                                const uint32_t* tlist, const uint2* trng, const uint32_t* order, CompositeGeom cg,
+                                RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
+                                int32_t* ncontrib, cudaStream_t st);
 // backward.cu
 cudaError_t prepare_composite_bwd(int num_sms, int resident[4]);
 cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const int* resident, bool simt, const uint4* rec, const void* feat, const uint32_t* tlist,

@@ -59,6 +59,22 @@ __device__ __forceinline__ float2 exp_det2(float2 x) {
     return mul2(p, s);
 }
 
+// exp of the staged argument x (= -q/2) for two values: the fixed sequence exp_det (R13,
+// bit-identical to the oracle) or, for the opt-in fast mode (ta_raster_params.exact_exp = 0), the SFU:
+// ex2.approx(x * log2 e) -- a few ulp from exp, so alpha' and, rarely, a stop decision may differ.
+template <bool kFast>
+__device__ __forceinline__ float2 exp2v(float2 x) {
+    if constexpr (kFast) {
+        const float2 y = mul2(x, bc2(1.44269504088896341f));
+        float a, b;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(a) : "f"(y.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(y.y));
+        return make_float2(a, b);
+    } else {
+        return exp_det2(x);
+    }
+}
+
 // Lanes of an 8x8 block (lane l: column l&7, row l>>3 (+4 for pixel B)) whose pixel lies inside the
 // box [gx0,gx1]x[gy0,gy1]; computed once per staged entry instead of once per pixel.
 __device__ __forceinline__ uint32_t box_lane_mask(int gx0, int gx1, int gy0, int gy1, int bx0, int ry) {

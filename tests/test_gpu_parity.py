@@ -457,3 +457,19 @@ def test_invalid_arguments_are_rejected(ctx):
     with pytest.raises(tb.TaError) as e:
         ctx.unproject(views, gp, odd)
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3r"])
+def test_tensor_memory_compositor_parity(oracle_lib, cfg):
+    """The opt-in tensor-memory compositor (TA_COMPOSITOR=2: tcgen05.mma with the C-channel accumulators
+    in TMEM, one 16 x 16 tile per 4-warp CTA) against the oracle: every stage, every pixel (c2 and the
+    ragged reduced c3); A and composited counts bit-exact, F within 1e-4."""
+    import os
+    import paper_2405_14866_b200 as tb
+    os.environ["TA_COMPOSITOR"] = "2"
+    try:
+        c = tb.Context(0)
+    finally:
+        os.environ.pop("TA_COMPOSITOR")
+    s = sg.make_config("c2") if cfg == "c2" else sg.make_config("c3", res=256, target_hw=(136, 200))
+    full_parity(c, oracle_lib, s)

@@ -157,6 +157,29 @@ ta_status ta_rasterize(ta_context* ctx, const ta_gaussians* g, int64_t n, const 
                        float* feat_out, float* alpha_out, void* stream);
 
 /*
+ * north_star (a) -- the fused front end: lift the foreground pixels of V source views (a1), project and
+ * cull them for T targets (a2) in ONE pass over the source maps (128-bit loads), then bin, sort and
+ * composite each target (a3-a6) exactly as ta_rasterize does.  Equivalent to ta_unproject followed by
+ * ta_rasterize(n = -1) per target -- same ids (view-major, row-major compaction), same records, same
+ * output bits -- but the Gaussians' world position / covariance (48 B each) are never written to or
+ * re-read from memory; only the feature rows are compacted (the compositor's operand).  Use it when few
+ * targets are rendered per frame (a single view, the paper's two eyes); for many targets per frame
+ * (the 32-view display) ta_unproject once + ta_rasterize per view moves fewer bytes.
+ *   views / V / params  as ta_unproject (C, feat_dtype describe the views' feature maps)
+ *   T                   1 <= T <= 4 targets, all H x W
+ *   K_tgt, RT_tgt       host arrays of T cameras
+ *   feat_out, alpha_out host arrays of T device pointers: float [H][W][C] (16-byte aligned), float [H][W]
+ * Scratch (context-owned, grow-only): sum_v H_v W_v x (C x feature bytes + T x 40 B); targets 1..T-1 run
+ * their sort / bin / composite chains on child contexts and streams owned by ctx, concurrently with
+ * target 0, and the call completes on `stream`.  ta_debug_last describes target 0.  Errors as
+ * ta_unproject + ta_rasterize; T outside [1, 4] is TA_ERR_INVALID_ARG.
+ */
+ta_status ta_render_sources(ta_context* ctx, const ta_source_view* views, int32_t V, int32_t C, ta_dtype feat_dtype,
+                            const ta_raster_params* params, int32_t T, const ta_intrinsics* K_tgt,
+                            const ta_extrinsics* RT_tgt, int32_t H, int32_t W, float* const* feat_out,
+                            float* const* alpha_out, void* stream);
+
+/*
  * cascade depth initialisation (cam0's disparity "is
  * converted to a depth map and then lifted to a 3D point cloud.  These points are rasterized to the
  * viewpoints of cam2 and cam3.  Z-buffers are extracted and converted back to disparity maps";

@@ -44,6 +44,12 @@ struct ta_context {
     uint32_t sort_epoch = 0;      // per-call tag of the depth-sort look-back words (sort_hist)
     DevBuf tlist, trng;           // per-tile lists (tiles-per-bin x the coarse-list capacity) and their (start, count)
     DevBuf zkey;                  // ta_zbuffer: 64-bit z-buffer words
+    DevBuf ffeat, frec, fkey, fval, fstats, fn;   // fused front end: compact features, per-target records / keys
+    // fused front end, targets 1..T-1: child contexts (own scratch) + streams, so the targets' sort / bin /
+    // composite chains run concurrently after the shared front end
+    ta_context* aux[kMaxFrontTargets - 1] = {nullptr, nullptr, nullptr};
+    cudaStream_t aux_stream[kMaxFrontTargets - 1] = {nullptr, nullptr, nullptr};
+    cudaEvent_t aux_ev[kMaxFrontTargets] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
     // last rasterize call
@@ -56,6 +62,9 @@ struct ta_context {
     int64_t last_n = 0;
     const void* last_feat = nullptr;
     RasterConsts last_rc{};
+    const void* last_rec = nullptr;           // the arrays the last call's debug view reads
+    const void* last_k[2] = {nullptr, nullptr};
+    const void* last_v[2] = {nullptr, nullptr};
     DevBuf dbg_offs, dbg_list;
     // stage profiling
     bool profiling = false;
@@ -210,7 +219,13 @@ const char* ta_build_info(void) {
     return "taloha sm_100a (persistent-warp compositor: packed-fp32 recurrence + mma.sync f16 feature accumulation; one-sweep depth sort; look-back scans; coarse binning + tile split; tensor-core backward)";
 }
 
-uint64_t ta_launch_count(const ta_context* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t ta_launch_count(const ta_context* ctx) {
+    if (!ctx) return 0;
+    uint64_t n = ctx->launches;
+    for (int k = 0; k < kMaxFrontTargets - 1; k++)
+        if (ctx->aux[k]) n += ctx->aux[k]->launches;
+    return n;
+}
 
 ta_status ta_context_create(int32_t device, ta_context** out) {
     if (!out) return TA_ERR_INVALID_ARG;
@@ -261,10 +276,16 @@ ta_status ta_context_destroy(ta_context* c) {
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->cs, &c->status, &c->rec, &c->boxes, &c->tile_order, &c->keys0, &c->keys1, &c->vals0, &c->vals1, &c->sort_hist,
                       &c->bin_offs, &c->list, &c->ncontrib, &c->ucounts, &c->ustatus, &c->dbg_offs, &c->dbg_list,
-                      &c->tlist, &c->trng, &c->zkey};
+                      &c->tlist, &c->trng, &c->zkey, &c->ffeat, &c->frec, &c->fkey, &c->fval, &c->fstats, &c->fn};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->pinned) cudaFreeHost(c->pinned);
+    for (int k = 0; k < kMaxFrontTargets - 1; k++) {
+        if (c->aux[k]) ta_context_destroy(c->aux[k]);
+        if (c->aux_stream[k]) cudaStreamDestroy(c->aux_stream[k]);
+    }
+    for (int k = 0; k < kMaxFrontTargets; k++)
+        if (c->aux_ev[k]) cudaEventDestroy(c->aux_ev[k]);
     for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto& p : c->pool) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     delete c;
@@ -415,6 +436,53 @@ ta_status build_view_table(ta_context* c, const ta_source_view* views, int32_t V
     return TA_OK;
 }
 
+void fill_cam(const ta_intrinsics& K, const ta_extrinsics& RT, int H, int W, TargetCam* cam) {
+    cam->fx = K.fx; cam->fy = K.fy; cam->cx = K.cx; cam->cy = K.cy;
+    memcpy(cam->R, RT.R, sizeof(cam->R));
+    memcpy(cam->t, RT.t, sizeof(cam->t));
+    cam->W = W; cam->H = H;
+    cam->Wm1f = (float)(W - 1);
+    cam->Hm1f = (float)(H - 1);
+}
+
+void fill_consts(const ta_raster_params& p, RasterConsts* rc) {
+    rc->dilation = p.dilation; rc->alpha_max = p.alpha_max; rc->alpha_min = p.alpha_min; rc->t_eps = p.t_eps;
+    rc->cull_sigma = p.cull_sigma; rc->z_near = p.z_near;
+    rc->q_max = p.cull_sigma * p.cull_sigma;
+}
+
+// One rasterization (a2 -- a6) of a Gaussian set into one target.  Gaussian-set mode (pos_alpha / cov
+// given): k_project writes the splat records into context scratch.  Pre-projected mode (rec / k0 / v0 /
+// stats given, from the fused front end): the records, depth keys and visibility statistics exist
+// already and the pipeline starts at the depth sort.
+struct RasterJob {
+    const float4* pos_alpha = nullptr;
+    const float4* cov = nullptr;
+    uint4* rec = nullptr;
+    uint32_t* k0 = nullptr;
+    uint32_t* v0 = nullptr;
+    const uint32_t* stats = nullptr;
+    const void* feat = nullptr;
+    int C = 0, fbytes = 2;
+    int64_t n = -1;                    // host count or -1 (read n_dev on the device)
+    const int64_t* n_dev = nullptr;
+    int64_t cap = 0;                   // upper bound on n (scratch sizing)
+    TargetCam cam{};
+    RasterConsts rc{};
+    int H = 0, W = 0;
+    bool async = false, counts = false, fast_exp = false;
+    float* F = nullptr;
+    float* A = nullptr;
+    cudaStream_t s = nullptr;
+};
+
+ta_status raster_pipeline(ta_context* c, const RasterJob& job);
+
+bool params_ok(const ta_raster_params& p) {
+    return (p.cull_sigma > 0.0f && p.cull_sigma <= 12.0f) && (p.alpha_max > 0.0f && p.alpha_max < 1.0f) &&
+           (p.t_eps > 0.0f && p.t_eps < 1.0f) && (p.alpha_min >= 0.0f) && (p.dilation >= 0.0f) && std::isfinite(p.z_near);
+}
+
 }  // namespace
 
 extern "C" {
@@ -496,11 +564,41 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     ta_status st;
     if (!finite_cam(*K, *RT, c, &st)) return st;
     cudaSetDevice(c->device);
-    cudaStream_t s = (cudaStream_t)stream;
-    const bool async = (p->flags & TA_FLAG_ASYNC) != 0;
-    const bool counts = (p->flags & TA_FLAG_DEBUG_COUNTS) != 0;
+    RasterJob job;
+    job.pos_alpha = (const float4*)g->pos_alpha;
+    job.cov = (const float4*)g->cov;
+    job.feat = g->feat;
+    job.C = g->C;
+    job.fbytes = g->feat_dtype == TA_F16 ? 2 : 4;
+    job.n = n;
+    job.n_dev = g->n_dev;
+    job.cap = n >= 0 ? n : g->capacity;
+    job.H = H; job.W = W;
+    fill_cam(*K, *RT, H, W, &job.cam);
+    fill_consts(*p, &job.rc);
+    if (p->exact_exp != 0 && p->exact_exp != 1) return fail(c, TA_ERR_INVALID_ARG, "exact_exp must be 0 or 1");
+    job.fast_exp = p->exact_exp == 0;
+    job.async = (p->flags & TA_FLAG_ASYNC) != 0;
+    job.counts = (p->flags & TA_FLAG_DEBUG_COUNTS) != 0;
+    job.F = feat_out; job.A = alpha_out;
+    job.s = (cudaStream_t)stream;
+    return raster_pipeline(c, job);
+}
 
-    const int64_t cap = n >= 0 ? n : g->capacity;
+}  // extern "C"
+
+namespace {
+
+ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
+    ta_status st;
+    const int64_t cap = job.cap, n = job.n;
+    const int H = job.H, W = job.W;
+    const bool async = job.async, counts = job.counts, fast_exp = job.fast_exp;
+    const TargetCam& cam = job.cam;
+    const RasterConsts& rc = job.rc;
+    cudaStream_t s = job.s;
+    float* feat_out = job.F;
+    float* alpha_out = job.A;
     BinGeom bg;
     if ((st = bin_geometry(c, H, W, cap, &bg)) != TA_OK) return st;
     const int NB = bg.TX * bg.TY;                      // coarse bins
@@ -523,41 +621,28 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
             return st;
     }
 
-    TargetCam cam;
-    cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
-    memcpy(cam.R, RT->R, sizeof(cam.R));
-    memcpy(cam.t, RT->t, sizeof(cam.t));
-    cam.W = W; cam.H = H;
-    cam.Wm1f = (float)(W - 1);
-    cam.Hm1f = (float)(H - 1);
-    RasterConsts rc;
-    rc.dilation = p->dilation; rc.alpha_max = p->alpha_max; rc.alpha_min = p->alpha_min; rc.t_eps = p->t_eps;
-    rc.cull_sigma = p->cull_sigma; rc.z_near = p->z_near;
-    rc.q_max = p->cull_sigma * p->cull_sigma;
-    if (p->exact_exp != 0 && p->exact_exp != 1) return fail(c, TA_ERR_INVALID_ARG, "exact_exp must be 0 or 1");
-    const bool fast_exp = p->exact_exp == 0;
 
     CallState* cs = (CallState*)c->cs.p;
     unsigned long long* status = (unsigned long long*)c->status.p;
     const uint32_t region = c->status_region;
     const int n_status = (int)(region * kScanSlots);
-    uint32_t* k0 = (uint32_t*)c->keys0.p; uint32_t* k1 = (uint32_t*)c->keys1.p;
-    uint32_t* v0 = (uint32_t*)c->vals0.p; uint32_t* v1 = (uint32_t*)c->vals1.p;
+    const bool pre = job.rec != nullptr;
+    uint32_t* k0 = pre ? job.k0 : (uint32_t*)c->keys0.p; uint32_t* k1 = (uint32_t*)c->keys1.p;
+    uint32_t* v0 = pre ? job.v0 : (uint32_t*)c->vals0.p; uint32_t* v1 = (uint32_t*)c->vals1.p;
     unsigned long long* sort_lb = (unsigned long long*)c->sort_hist.p;
     if (++c->sort_epoch == 0) c->sort_epoch = 1;     // 0 would match zeroed look-back words
     const uint32_t epoch = c->sort_epoch;
     uint32_t* offs = (uint32_t*)c->bin_offs.p;
-    uint4* rec = (uint4*)c->rec.p;
+    uint4* rec = pre ? job.rec : (uint4*)c->rec.p;
 
     StageTimer tm(c, s);
     tm.begin(TA_STAGE_PROJECT);
-    k_init<<<std::min(1024, (n_status + 255) / 256 + 1), 256, 0, s>>>(cs, status, n_status, n, g->n_dev,
-                                                                       kBinTileRanks(bg.nw), (uint32_t)NB);
+    k_init<<<std::min(1024, (n_status + 255) / 256 + 1), 256, 0, s>>>(cs, status, n_status, n, job.n_dev,
+                                                                       kBinTileRanks(bg.nw), (uint32_t)NB, job.stats);
     TA_LAUNCHED(c);
     const int64_t cap_blocks = (cap + 255) / 256;
-    if (cap_blocks > 0) {
-        k_project<<<(unsigned)((cap + 511) / 512), 256, 0, s>>>((const float4*)g->pos_alpha, (const float4*)g->cov, cam, rc, cs,
-                                                       rec, k0, v0);
+    if (cap_blocks > 0 && !pre) {
+        k_project<<<(unsigned)((cap + 511) / 512), 256, 0, s>>>(job.pos_alpha, job.cov, cam, rc, cs, rec, k0, v0);
         TA_LAUNCHED(c);
     }
     tm.end();
@@ -615,17 +700,17 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     tm.end();
     tm.begin(TA_STAGE_COMPOSITE);
     cudaError_t e;
-    if (g->feat_dtype == TA_F16 && g->C >= 16 && c->compositor == 2) {
+    if (job.fbytes == 2 && job.C >= 16 && c->compositor == 2) {
         // tensor-memory compositor (tcgen05.mma, accumulators in TMEM); exact_exp = 0 selects its SFU exp
         if (T > 0) launch_tile_order((const uint2*)c->trng.p, cg, (uint32_t*)c->tile_order.p, s);
-        e = T > 0 ? launch_composite_tm(g->C, T, c->resident_tm, fast_exp, rec, g->feat, (const uint32_t*)c->tlist.p,
+        e = T > 0 ? launch_composite_tm(job.C, T, c->resident_tm, fast_exp, rec, job.feat, (const uint32_t*)c->tlist.p,
                                         (const uint2*)c->trng.p, (const uint32_t*)c->tile_order.p, cg, rc, cs,
                                         (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
                                         counts ? (int32_t*)c->ncontrib.p : nullptr, s)
                   : cudaSuccess;
     } else {
         // persistent-warp compositors: mma.sync (fp16 features) / SIMT (fp32 features)
-        e = launch_composite(g->C, g->feat_dtype == TA_F16 ? 2 : 4, T, c->resident_tc, fast_exp, rec, g->feat,
+        e = launch_composite(job.C, job.fbytes, T, c->resident_tc, fast_exp, rec, job.feat,
                              (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
                              (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
                              counts ? (int32_t*)c->ncontrib.p : nullptr, s);
@@ -637,11 +722,133 @@ ta_status ta_rasterize(ta_context* c, const ta_gaussians* g, int64_t n, const ta
     c->last_TX = cg.TX; c->last_TY = cg.TY; c->last_P = bg.P; c->last_H = H; c->last_W = W;
     c->last_cg = cg;
     c->last_counts = counts;
-    c->last_C = g->C;
-    c->last_fbytes = g->feat_dtype == TA_F16 ? 2 : 4;
+    c->last_C = job.C;
+    c->last_fbytes = job.fbytes;
     c->last_n = n;
-    c->last_feat = g->feat;
+    c->last_feat = job.feat;
     c->last_rc = rc;
+    c->last_rec = rec;
+    c->last_k[0] = k0; c->last_k[1] = k1;
+    c->last_v[0] = v0; c->last_v[1] = v1;
+    return TA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+
+ta_status ta_render_sources(ta_context* c, const ta_source_view* views, int32_t V, int32_t C, ta_dtype feat_dtype,
+                            const ta_raster_params* p, int32_t T, const ta_intrinsics* K_tgt, const ta_extrinsics* RT_tgt,
+                            int32_t H, int32_t W, float* const* feat_out, float* const* alpha_out, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!views || !p || !K_tgt || !RT_tgt || !feat_out || !alpha_out)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_render_sources: NULL argument");
+    if (V < 1 || V > TA_MAX_VIEWS) return fail(c, TA_ERR_UNSUPPORTED, "ta_render_sources: V = %d not in [1, %d]", V, TA_MAX_VIEWS);
+    if (T < 1 || T > kMaxFrontTargets) return fail(c, TA_ERR_INVALID_ARG, "T = %d not in [1, %d]", T, kMaxFrontTargets);
+    if (!supported_C(C)) return fail(c, TA_ERR_UNSUPPORTED, "C = %d not in {8,16,32,64}", C);
+    if (feat_dtype != TA_F32 && feat_dtype != TA_F16) return fail(c, TA_ERR_UNSUPPORTED, "unknown dtype");
+    if (H < 1 || W < 1 || H > 32767 || W > 32767) return fail(c, TA_ERR_INVALID_ARG, "bad target size %d x %d", H, W);
+    if (!params_ok(*p))
+        return fail(c, TA_ERR_INVALID_ARG, "raster params out of range (0 < cull_sigma <= 12, 0 < alpha_max < 1, "
+                                           "0 < t_eps < 1, alpha_min >= 0, dilation >= 0)");
+    if (p->exact_exp != 0 && p->exact_exp != 1) return fail(c, TA_ERR_INVALID_ARG, "exact_exp must be 0 or 1");
+    ta_status st;
+    for (int t = 0; t < T; t++) {
+        if (!feat_out[t] || !alpha_out[t]) return fail(c, TA_ERR_INVALID_ARG, "target %d: NULL output", t);
+        if (((uintptr_t)feat_out[t]) & 15) return fail(c, TA_ERR_INVALID_ARG, "target %d: feat_out not 16-byte aligned", t);
+        if (!finite_cam(K_tgt[t], RT_tgt[t], c, &st)) return st;
+    }
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int fbytes = feat_dtype == TA_F16 ? 2 : 4;
+    ViewTable vt;
+    int64_t pixels = 0;
+    uint32_t blocks = 0;
+    if ((st = build_view_table(c, views, V, p, true, C, fbytes, &vt, &pixels, &blocks)) != TA_OK) return st;
+    if (pixels >= (1ll << 31)) return fail(c, TA_ERR_CAPACITY, "more than 2^31 source pixels");
+    const size_t cap = (size_t)std::max<int64_t>(pixels, 1);
+    if ((st = grow(c, c->ucounts, ((size_t)blocks + 16) * 4)) != TA_OK) return st;
+    const uint32_t tiles = scan_tiles(blocks);
+    if ((st = grow(c, c->ustatus, ((size_t)tiles + 8) * 8)) != TA_OK) return st;
+    if ((st = grow(c, c->ffeat, cap * (size_t)C * fbytes)) != TA_OK ||
+        (st = grow(c, c->frec, cap * 32 * (size_t)T)) != TA_OK || (st = grow(c, c->fkey, cap * 4 * (size_t)T)) != TA_OK ||
+        (st = grow(c, c->fval, cap * 4 * (size_t)T)) != TA_OK || (st = grow(c, c->fstats, 16 * 4 * kMaxFrontTargets)) != TA_OK ||
+        (st = grow(c, c->fn, 64)) != TA_OK)
+        return st;
+    RasterConsts rc;
+    fill_consts(*p, &rc);
+    FrontTargets ft;
+    memset(&ft, 0, sizeof(ft));
+    ft.T = T;
+    for (int t = 0; t < T; t++) {
+        fill_cam(K_tgt[t], RT_tgt[t], H, W, &ft.cam[t]);
+        ft.rec[t] = (uint4*)c->frec.p + 2 * cap * t;
+        ft.key[t] = (uint32_t*)c->fkey.p + cap * t;
+        ft.val[t] = (uint32_t*)c->fval.p + cap * t;
+    }
+    uint32_t* stats = (uint32_t*)c->fstats.p;
+    int64_t* n_dev = (int64_t*)c->fn.p;
+    StageTimer tm(c, s);
+    tm.begin(TA_STAGE_PROJECT);
+    TA_CUDA(c, cudaMemsetAsync(c->ustatus.p, 0, ((size_t)tiles + 8) * 8, s));
+    k_front_stats_init<<<1, 32, 0, s>>>(stats, T);
+    TA_LAUNCHED(c);
+    k_unproject_count<<<blocks, kUnprojThreads, 0, s>>>(vt, (uint32_t*)c->ucounts.p);
+    TA_LAUNCHED(c);
+    unsigned long long* ust = (unsigned long long*)c->ustatus.p;
+    launch_scan((uint32_t*)c->ucounts.p, nullptr, blocks, ust, (uint32_t*)(ust + tiles + 4), (unsigned long long*)n_dev, s);
+    TA_LAUNCHED(c);
+    k_front_fused<<<blocks, kUnprojThreads, 0, s>>>(vt, (const uint32_t*)c->ucounts.p, ft, rc, c->ffeat.p, stats);
+    TA_LAUNCHED(c);
+    tm.end();
+    // targets 1..T-1 run on child contexts / streams concurrently with target 0 (after the front end)
+    for (int t = 1; t < T; t++) {
+        if (!c->aux[t - 1]) {
+            ta_status cst = ta_context_create(c->device, &c->aux[t - 1]);
+            if (cst != TA_OK) return fail(c, cst, "child context for target %d", t);
+            c->aux[t - 1]->compositor = c->compositor;
+            TA_CUDA(c, cudaStreamCreateWithFlags(&c->aux_stream[t - 1], cudaStreamNonBlocking));
+        }
+    }
+    for (int k = 0; k < T; k++)
+        if (!c->aux_ev[k]) TA_CUDA(c, cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
+    if (T > 1) {
+        TA_CUDA(c, cudaEventRecord(c->aux_ev[0], s));
+        for (int t = 1; t < T; t++) TA_CUDA(c, cudaStreamWaitEvent(c->aux_stream[t - 1], c->aux_ev[0], 0));
+    }
+    for (int t = 0; t < T; t++) {
+        ta_context* ct = t == 0 ? c : c->aux[t - 1];
+        ct->profiling = c->profiling && t == 0;
+        RasterJob job;
+        job.rec = ft.rec[t];
+        job.k0 = ft.key[t];
+        job.v0 = ft.val[t];
+        job.stats = stats + 3 * t;
+        job.feat = c->ffeat.p;
+        job.C = C;
+        job.fbytes = fbytes;
+        job.n = -1;
+        job.n_dev = n_dev;
+        job.cap = (int64_t)cap;
+        job.cam = ft.cam[t];
+        job.rc = rc;
+        job.H = H; job.W = W;
+        job.fast_exp = p->exact_exp == 0;
+        job.async = (p->flags & TA_FLAG_ASYNC) != 0;
+        job.counts = (p->flags & TA_FLAG_DEBUG_COUNTS) != 0;
+        job.F = feat_out[t];
+        job.A = alpha_out[t];
+        job.s = t == 0 ? s : c->aux_stream[t - 1];
+        if ((st = raster_pipeline(ct, job)) != TA_OK) {
+            if (ct != c) fail(c, st, "target %d: %s", t, ct->err.c_str());
+            return st;
+        }
+    }
+    for (int t = 1; t < T; t++) {                         // the call completes on `stream` only
+        TA_CUDA(c, cudaEventRecord(c->aux_ev[t], c->aux_stream[t - 1]));
+        TA_CUDA(c, cudaStreamWaitEvent(s, c->aux_ev[t], 0));
+    }
     return TA_OK;
 }
 
@@ -772,7 +979,7 @@ ta_status ta_rasterize_backward(ta_context* c, const ta_gaussians* g, int64_t n,
     cudaSetDevice(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const CompositeGeom& cg = c->last_cg;
-    cudaError_t e = launch_composite_bwd(g->C, fbytes, cg.TX * cg.TY, c->resident_bwd, c->bwd_simt, (const uint4*)c->rec.p,
+    cudaError_t e = launch_composite_bwd(g->C, fbytes, cg.TX * cg.TY, c->resident_bwd, c->bwd_simt, (const uint4*)c->last_rec,
                                          g->feat, (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p,
                                          (const uint32_t*)c->tile_order.p, cg, rc,
                                          (CallState*)c->cs.p, (uint64_t)(c->tlist.bytes / 4), grad_F, grad_A,
@@ -823,9 +1030,9 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     out->tiles_x = cg.TX;
     out->tiles_y = cg.TY;
     out->sort_passes = passes;
-    out->records = (const uint32_t*)c->rec.p;
-    out->depth_keys = (const uint32_t*)((passes & 1) ? c->keys1.p : c->keys0.p);
-    out->order = (const uint32_t*)((passes & 1) ? c->vals1.p : c->vals0.p);
+    out->records = (const uint32_t*)c->last_rec;
+    out->depth_keys = (const uint32_t*)c->last_k[passes & 1];
+    out->order = (const uint32_t*)c->last_v[passes & 1];
     out->tile_offsets = (const uint32_t*)c->dbg_offs.p;
     out->tile_list = (const uint32_t*)c->dbg_list.p;
     out->n_contrib = c->last_counts ? (const int32_t*)c->ncontrib.p : nullptr;

@@ -55,7 +55,7 @@ constexpr int kUnprojPix = 4 * kUnprojThreads;   // pixels per block
 
 // raster.cu
 __global__ void k_init(CallState* cs, unsigned long long* status, int n_status, int64_t n_host,
-                       const int64_t* n_dev, uint32_t bin_ranks, uint32_t nbins);
+                       const int64_t* n_dev, uint32_t bin_ranks, uint32_t nbins, const uint32_t* stats);
 __global__ void k_project(const float4* pos_alpha, const float4* cov, TargetCam cam, RasterConsts rc,
                           CallState* cs, uint4* rec, uint32_t* key0, uint32_t* val0);
 __global__ void k_sort_digits(const uint32_t* keys, CallState* cs);
@@ -136,6 +136,18 @@ __global__ void k_zb_resolve(const unsigned long long* zk, uint32_t n, float fx,
 
 // unproject.cu
 __global__ void k_unproject_count(ViewTable vt, uint32_t* counts);
+// fused front end (north_star (a)): up to kMaxFrontTargets targets per call
+constexpr int kMaxFrontTargets = 4;
+struct FrontTargets {
+    TargetCam cam[kMaxFrontTargets];
+    uint4* rec[kMaxFrontTargets];
+    uint32_t* key[kMaxFrontTargets];
+    uint32_t* val[kMaxFrontTargets];
+    int T;
+};
+__global__ void k_front_fused(ViewTable vt, const uint32_t* offs, FrontTargets ft, RasterConsts rc, void* feat_out,
+                              uint32_t* stats);
+__global__ void k_front_stats_init(uint32_t* stats, int T);
 __global__ void k_unproject_write(ViewTable vt, const uint32_t* offs, float4* pos_alpha, float4* cov, void* feat);
 
 }  // namespace ta

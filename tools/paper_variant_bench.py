@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """the paper-exact frame -- lift cam0 + cam2 + cam3 (1024^2, R = I, C = 32 fp16)
 and rasterize the viewer's two eye targets (1024^2) -- timed per frame with CUDA events (median of
-20 frames after 5 warm-ups; the two eyes on two streams / contexts).  One JSON line (dev tool)."""
+20 frames after 5 warm-ups).  Two paths: the two-call API (ta_unproject, then ta_rasterize per eye on
+two streams / contexts) and the fused front end (ta_render_sources with both eyes in one call, one
+stream).  256 MB L2 flush between frames.  One JSON line (dev tool)."""
 import json
 import os
 import statistics
@@ -48,20 +50,46 @@ def main():
             e2.record(sd)
             st.wait_event(e2)
 
-    for _ in range(5):
-        frame()
-    ts = []
-    for _ in range(20):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        frame()
-        b.record(st)
-        b.synchronize()
-        ts.append(a.elapsed_time(b))
-    ms = statistics.median(ts)
+    cf = tb.Context(0)
+    fouts = [(torch.empty((c.H, c.W, 32), dtype=torch.float32, device="cuda"),
+              torch.empty((c.H, c.W), dtype=torch.float32, device="cuda")) for c in s.targets]
+    Ks, RTs = [c[0] for c in cams], [c[1] for c in cams]
+    cf.render_sources(views, 32, "f16", psync, Ks, RTs, 1024, 1024, [o[0] for o in fouts], [o[1] for o in fouts], st)
+
+    def frame_fused():
+        cf.render_sources(views, 32, "f16", pasync, Ks, RTs, 1024, 1024, [o[0] for o in fouts], [o[1] for o in fouts], st)
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def timed(fn):
+        for _ in range(5):
+            fn()
+        ts = []
+        for _ in range(20):
+            flush.add_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        ts.sort()
+        return {"median": ts[len(ts) // 2], "min": ts[0], "p90": ts[int(0.9 * len(ts))]}
+
+    def frame_one_stream():
+        ctxs[0].unproject(views, psync, g, st)
+        for (Ki, Ri, H, W), (F, A) in zip(cams, outs):
+            ctxs[0].rasterize(g, -1, Ki, Ri, H, W, pasync, F, A, st)
+
+    two = timed(frame)
+    two1 = timed(frame_one_stream)
+    fus = timed(frame_fused)
+    same = all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for (a, _), (b, _) in zip(outs, fouts)) and \
+        all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for (_, a), (_, b) in zip(outs, fouts))
     print(json.dumps({"workload": "paper-exact frame: 3 x 1024^2 lifted (R = I) + 2 eye targets 1024^2, C = 32",
-                      "n_gaussians": int(g.n), "ms_per_frame": ms, "frames_per_s": 1e3 / ms,
-                      "ms_min": min(ts), "ms_p90": sorted(ts)[int(0.9 * len(ts))]}))
+                      "n_gaussians": int(g.n), "two_call_ms": two, "two_call_one_stream_ms": two1, "fused_ms": fus,
+                      "frames_per_s": {"two_call": 1e3 / two["median"], "fused": 1e3 / fus["median"]},
+                      "outputs_bit_identical": bool(same)}))
 
 
 if __name__ == "__main__":

@@ -41,7 +41,6 @@ struct ta_context {
     std::string err;
     uint64_t launches = 0;
     DevBuf cs, status, rec, boxes, tile_order, keys0, keys1, vals0, vals1, sort_hist, bin_offs, list, ncontrib, ucounts, ustatus;
-    uint32_t sort_epoch = 0;      // per-call tag of the depth-sort look-back words (sort_hist)
     DevBuf tlist, trng;           // per-tile lists (tiles-per-bin x the coarse-list capacity) and their (start, count)
     DevBuf zkey;                  // ta_zbuffer: 64-bit z-buffer words
     DevBuf ffeat, frec, fkey, fval, fstats, fn;   // fused front end: compact features, per-target records / keys
@@ -630,8 +629,6 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
     uint32_t* k0 = pre ? job.k0 : (uint32_t*)c->keys0.p; uint32_t* k1 = (uint32_t*)c->keys1.p;
     uint32_t* v0 = pre ? job.v0 : (uint32_t*)c->vals0.p; uint32_t* v1 = (uint32_t*)c->vals1.p;
     unsigned long long* sort_lb = (unsigned long long*)c->sort_hist.p;
-    if (++c->sort_epoch == 0) c->sort_epoch = 1;     // 0 would match zeroed look-back words
-    const uint32_t epoch = c->sort_epoch;
     uint32_t* offs = (uint32_t*)c->bin_offs.p;
     uint4* rec = pre ? job.rec : (uint4*)c->rec.p;
 
@@ -654,7 +651,7 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
         TA_LAUNCHED(c);
         for (int pass = 0; pass < 4; pass++) {
             k_sort_pass<<<sort_blocks, kSortWarps * 32, 0, s>>>(k0, k1, v0, v1, pass, cs,
-                                                                sort_lb + (size_t)pass * 256 * parts_max, epoch, rec,
+                                                                sort_lb + (size_t)pass * 256 * parts_max, rec,
                                                                 (uint2*)c->boxes.p);
             TA_LAUNCHED(c);
         }

@@ -97,6 +97,7 @@ struct CallState {
     uint32_t bin_len;              // NB * bin_P + 1 (bin-major run starts + the total)
     uint32_t bin_P;                // rank tiles of this call (ceil(n / ranks per tile))
     uint32_t overflow;             // sticky: entries exceeded the list capacity (not reset by k_init)
+    uint32_t epoch;                // depth-sort look-back tag of the current call (advanced by k_init)
     uint32_t scan_counter[8];      // tile counters of the look-back scans (one per scan)
     unsigned long long work[8];    // compositor work counters (TA_FLAG_DEBUG_COUNTS only, reset by k_init)
     uint32_t digit_hist[4][256];   // depth sort: global digit histogram of each pass (k_sort_digits)

@@ -60,7 +60,7 @@ __global__ void k_project(const float4* pos_alpha, const float4* cov, TargetCam 
                           CallState* cs, uint4* rec, uint32_t* key0, uint32_t* val0);
 __global__ void k_sort_digits(const uint32_t* keys, CallState* cs);
 __global__ void k_sort_pass(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int pass,
-                            CallState* cs, unsigned long long* lb, uint32_t epoch, const uint4* rec, uint2* boxes);
+                            CallState* cs, unsigned long long* lb, const uint4* rec, uint2* boxes);
 __global__ void k_gather_boxes(const uint4* rec, const uint32_t* vals_a, const uint32_t* vals_b, const CallState* cs,
                                uint2* boxes);
 __global__ void k_bin_count(const uint2* boxes, const CallState* cs, BinGeom bg, uint32_t* counts);

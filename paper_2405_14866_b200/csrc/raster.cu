@@ -39,6 +39,7 @@ __global__ void k_init(CallState* __restrict__ cs, unsigned long long* __restric
         if (cs->bin_P == 0) cs->bin_P = 1;
         cs->bin_len = nbins * cs->bin_P + 1;
         for (int k = 0; k < 8; k++) cs->scan_counter[k] = 0u;
+        cs->epoch = cs->epoch + 1u == 0u ? 1u : cs->epoch + 1u;   // 0 would match zeroed look-back words
         for (int k = 0; k < 8; k++) cs->work[k] = 0ull;
     }
     if (blockIdx.x == 0)
@@ -156,7 +157,8 @@ __device__ __forceinline__ uint32_t block256_excl(uint32_t v, uint32_t* s) {
 }
 
 // Look-back words: epoch << 32 | flag << 30 | count (flag 1: this partition's count, 2: inclusive
-// prefix over partitions 0..p).  The epoch (per call) makes stale words of earlier calls invisible.
+// prefix over partitions 0..p).  The epoch (per call, a device counter advanced by k_init, so graph
+// replays advance it too) makes stale words of earlier calls invisible.
 constexpr uint64_t kLbAgg = 1ull << 30, kLbInc = 2ull << 30;
 constexpr uint32_t kLbMask = (1u << 30) - 1u;
 
@@ -164,7 +166,7 @@ constexpr uint32_t kLbMask = (1u << 30) - 1u;
 __global__ void __launch_bounds__(kSortWarps * 32) k_sort_pass(uint32_t* __restrict__ keys_a, uint32_t* __restrict__ keys_b,
                                                                uint32_t* __restrict__ vals_a, uint32_t* __restrict__ vals_b,
                                                                int pass, CallState* __restrict__ cs,
-                                                               unsigned long long* __restrict__ lb, uint32_t epoch,
+                                                               unsigned long long* __restrict__ lb,
                                                                const uint4* __restrict__ rec, uint2* __restrict__ boxes) {
     static_assert(kSortWarps * 32 == 256, "one thread per digit");
     constexpr int kChunks = kSortKeysPerWarp / 32;
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_pass(uint32_t* __restr
         tot += c;
     }
     unsigned long long* my = lb + (size_t)part * 256 + d;
+    const uint32_t epoch = cs->epoch;                  // per call, advanced by k_init on the device
     const unsigned long long ep = (unsigned long long)epoch << 32;
     if (part == 0) *(volatile unsigned long long*)my = ep | kLbInc | tot;
     else *(volatile unsigned long long*)my = ep | kLbAgg | tot;

@@ -212,12 +212,16 @@ ta_status ta_zbuffer(ta_context* ctx, const ta_source_view* views, int32_t V, co
  *   colors     host array of V device pointers, view i's colour image float [H_i][W_i][3]
  *   rgb_out    device float [H][W][3];  wsum_out  device float [H][W] (the denominator) or NULL
  * Reads params->d_min, z_near.  Errors: TA_ERR_INVALID_ARG for NULL pointers, bad sizes, bad cameras,
- * delta <= 0, edge_tau <= 0, w_min < 0.
+ * delta <= 0, edge_tau <= 0, w_min < 0, tau_c < 0.
  */
 typedef struct {
     float delta;       /* Eq. 9 SDF threshold (m), default 0.01 */
     float edge_tau;    /* edge mask: max central depth gradient (m / px), default 0.02 */
-    float w_min;       /* hole threshold on sum w_i, default 1e-4 */
+    float w_min;       /* hole threshold on sum w_i (a pixel with sum w_i = 0 is always a hole), default 1e-4 */
+    float tau_c;       /* appearance-consistency mask (l.430-433 names it; SPEC.md l.331's reading, DESIGN.md
+                          R24): a sample is kept iff its colour is within tau_c (linear RGB distance) of the
+                          pixel's weighted median sample (the medoid minimising sum_j w_j |c_j - c_i|);
+                          default 0.15, 0 = mask off */
 } ta_blend_params;
 void ta_default_blend_params(ta_blend_params* bp);
 ta_status ta_blend(ta_context* ctx, const ta_source_view* views, int32_t V, const float* const* colors,

@@ -249,13 +249,14 @@ class _BView(C.Structure):
 
 
 class _BParams(C.Structure):
-    _fields_ = [("delta", C.c_float), ("edge_tau", C.c_float), ("w_min", C.c_float)]
+    _fields_ = [("delta", C.c_float), ("edge_tau", C.c_float), ("w_min", C.c_float), ("tau_c", C.c_float)]
 
 
-def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, params=None):
+def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, tau_c=0.15, params=None):
     """NEXT #1 (Eqs. 6-10; R24): occlusion-aware blending of the input
     views' colours into `cam` over the fused depth z_fused[H, W] (0 = none, e.g. zbuffer(...)[1]).
-    colors: list of [H_i, W_i, 3] float32.  Returns (rgb[H, W, 3] f32, wsum[H, W] f32)."""
+    colors: list of [H_i, W_i, 3] float32; tau_c: appearance-consistency threshold (SPEC.md l.331, 0 = off).
+    Returns (rgb[H, W, 3] f32, wsum[H, W] f32)."""
     p = params or make_params()
     keep = []
     arr = (_BView * len(views))()
@@ -275,7 +276,7 @@ def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, pa
         for j in range(3):
             b.t[j] = float(t[j])
         b.baseline = float(np.float32(v.baseline))
-    bp = _BParams(float(delta), float(edge_tau), float(w_min))
+    bp = _BParams(float(delta), float(edge_tau), float(w_min), float(tau_c))
     Kn, Rn, tn = _cam(cam)
     zf = np.ascontiguousarray(z_fused, np.float32)
     rgb = np.empty((cam.H, cam.W, 3), np.float32)

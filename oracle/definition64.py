@@ -169,10 +169,12 @@ def zbuffer(views, cam, radius=1, z_near=0.01, d_min=0.0):
     return np.where(np.isfinite(best), best, 0.0)
 
 
-def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, z_near=0.01, d_min=0.0):
+def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, z_near=0.01, d_min=0.0, tau_c=0.15):
     """NEXT #1 (Eqs. 6-10) in float64 with array operations: lift every pixel of
     z_fused, project into each view, bilinear colour / depth, Occ, edge mask, finite-difference
-    normal, cos / distance weights, normalised sum.  Returns (rgb[H, W, 3], wsum[H, W]) float64."""
+    normal, cos / distance weights, the appearance-consistency mask (the weighted
+    medoid of the weighted samples by a full distance matrix, keep samples within tau_c of it; 0 = off),
+    normalised sum.  Returns (rgb[H, W, 3], wsum[H, W]) float64."""
     H, W = cam.H, cam.W
     f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
     R, t = f32(cam.R), f32(cam.t)
@@ -184,8 +186,7 @@ def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, z_
     C0 = -t @ R
     ray = Xw - C0
     ray /= np.linalg.norm(ray, axis=1, keepdims=True)
-    acc = np.zeros((len(z), 3))
-    ws = np.zeros(len(z))
+    Wv, Cv = [], []
     for v, col in zip(views, colors):
         sc = v.cam
         Ri, ti = f32(sc.R), f32(sc.t)
@@ -234,8 +235,20 @@ def blend(views, colors, cam, z_fused, delta=0.01, edge_tau=0.02, w_min=1e-4, z_
         c = col.astype(np.float64)
         cb = ((c[y0, x0] * (1 - ax)[:, None] + c[y0, x1] * ax[:, None]) * (1 - ay)[:, None] +
               (c[y1, x0] * (1 - ax)[:, None] + c[y1, x1] * ax[:, None]) * ay[:, None])
-        acc += w[:, None] * np.nan_to_num(cb)
-        ws += w
+        Wv.append(w)
+        Cv.append(np.nan_to_num(cb))
+    Wm = np.stack(Wv, 1)                      # [pixels, views]
+    Cm = np.stack(Cv, 1)                      # [pixels, views, 3]
+    if tau_c > 0:
+        # weighted medoid: the sample minimising the weighted sum of colour distances (ties: lowest view)
+        dist = np.linalg.norm(Cm[:, :, None, :] - Cm[:, None, :, :], axis=3)        # [p, i, j]
+        cost = np.einsum("pij,pj->pi", dist, Wm)
+        cost = np.where(Wm > 0, cost, np.inf)
+        med = Cm[np.arange(len(z)), np.argmin(cost, axis=1)]
+        keep = np.linalg.norm(Cm - med[:, None, :], axis=2) <= tau_c
+        Wm = np.where(keep, Wm, 0.0)
+    acc = np.einsum("pv,pvk->pk", Wm, Cm)
+    ws = Wm.sum(1)
     rgb = np.zeros((H, W, 3))
     wsum = np.zeros((H, W))
     good = ws >= w_min

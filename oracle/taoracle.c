@@ -513,8 +513,12 @@ void tao_zbuffer_resolve(int64_t n, const uint64_t* zkey, float fx, float baseli
  *     bilinear taps x0 = min(floor(u), W-2) (0 when W == 1), x1 = min(x0+1, W-1), likewise y;
  *     lerp(a, b, t) = fma(t, b - a, a), rows first; all four depth taps must be valid;
  *   - M_i: the input mask (through tap validity), the edge mask max(|z_r - z_l|, |z_d - z_u|)/2
- *     <= edge_tau at the nearest pixel rint(x_i.uv), and a valid normal there (4 neighbours valid);
- *     the appearance-consistency mask of l.433 is not defined by the paper and not applied;
+ *     <= edge_tau at the nearest pixel rint(x_i.uv), a valid normal there (4 neighbours valid), and the
+ *     appearance-consistency mask of l.433 (not defined by the paper; SPEC.md l.331's reading): over
+ *     the samples that pass everything else (weight w_i > 0), m = the weighted median sample (the
+ *     weighted medoid: the c_i minimising sum_j w_j |c_j - c_i|_2, ties to the lower view index), and a
+ *     sample is kept iff |c_i - m|^2 <= tau_c^2 (tau_c = 0: mask off) -- a first pass computes every
+ *     w_i, c_i and m, a second one blends; the medoid itself is always kept;
  *   - n_i: cross product of the central differences of the lifted camera-space points
  *     (SPEC.md l.120), normalised, flipped to face camera i, rotated to world (R_i^T n);
  *   - cos<r, n_i> = max(0, -r_hat . n_w) with r_hat the unit ray from the novel centre to the point;
@@ -532,7 +536,8 @@ typedef struct {
     const float* color;   /* [H][W][3] */
 } tao_bview;
 
-typedef struct { float delta, edge_tau, w_min; } tao_bparams;
+typedef struct { float delta, edge_tau, w_min, tau_c; } tao_bparams;
+#define TAO_MAX_BLEND_VIEWS 16
 
 static int bview_depth(const tao_bview* v, int x, int y, const tao_params* p, float* z) {
     if (x < 0 || y < 0 || x >= v->W || y >= v->H) return 0;
@@ -548,6 +553,7 @@ static float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
 void tao_blend(int V, const tao_bview* views, const tao_params* p, const tao_bparams* bp, const tao_intr* K,
                const tao_extr* RT, int H, int W, const float* zf, float* rgb, float* wsum) {
+    if (V > TAO_MAX_BLEND_VIEWS) V = TAO_MAX_BLEND_VIEWS;
     const float* R = RT->R;
     const float* t = RT->t;
     /* novel camera centre C = R^T (0 - t) */
@@ -558,6 +564,8 @@ void tao_blend(int V, const tao_bview* views, const tao_params* p, const tao_bpa
         for (int u = 0; u < W; u++) {
             int64_t pix = (int64_t)v * W + u;
             float acc[3] = {0.0f, 0.0f, 0.0f}, ws = 0.0f;
+            float sw[TAO_MAX_BLEND_VIEWS], sc[TAO_MAX_BLEND_VIEWS][3];   /* pass 1: every view's w_i, c_i */
+            int ns = 0;
             float z = zf[pix];
             if (z > 0.0f) {
                 /* Eq. 6: Pi_novel^-1(u, v, z_fused) */
@@ -629,10 +637,35 @@ void tao_blend(int V, const tao_bview* views, const tao_params* p, const tao_bpa
                     for (int k = 0; k < 3; k++) {
                         float a00 = col[((int64_t)y0 * bv->W + x0) * 3 + k], a10 = col[((int64_t)y0 * bv->W + x1) * 3 + k];
                         float a01 = col[((int64_t)y1 * bv->W + x0) * 3 + k], a11 = col[((int64_t)y1 * bv->W + x1) * 3 + k];
-                        float ck = lerpf(lerpf(a00, a10, ax), lerpf(a01, a11, ax), ay);
-                        acc[k] = fmaf(w, ck, acc[k]);
+                        sc[ns][k] = lerpf(lerpf(a00, a10, ax), lerpf(a01, a11, ax), ay);
                     }
-                    ws = ws + w;
+                    sw[ns++] = w;
+                }
+                /* appearance consistency: m = the weighted median sample (medoid): the c_i
+                   minimising sum_j w_j |c_j - c_i| (sums in view order, ties to the lower index) */
+                float m[3] = {0.0f, 0.0f, 0.0f};
+                if (bp->tau_c > 0.0f && ns > 0) {
+                    float best = INFINITY;
+                    int bi = 0;
+                    for (int i = 0; i < ns; i++) {
+                        float cost = 0.0f;
+                        for (int j = 0; j < ns; j++) {
+                            float e0 = sc[j][0] - sc[i][0], e1 = sc[j][1] - sc[i][1], e2 = sc[j][2] - sc[i][2];
+                            cost = fmaf(sw[j], sqrtf(dot3(e0, e1, e2, e0, e1, e2)), cost);
+                        }
+                        if (cost < best) { best = cost; bi = i; }
+                    }
+                    for (int k = 0; k < 3; k++) m[k] = sc[bi][k];
+                }
+                const float tau2 = bp->tau_c * bp->tau_c;
+                /* pass 2: Eq. 10 sums over the consistent samples, in view order */
+                for (int i = 0; i < ns; i++) {
+                    if (bp->tau_c > 0.0f) {
+                        float d0 = sc[i][0] - m[0], d1 = sc[i][1] - m[1], d2 = sc[i][2] - m[2];
+                        if (!(dot3(d0, d1, d2, d0, d1, d2) <= tau2)) continue;
+                    }
+                    for (int k = 0; k < 3; k++) acc[k] = fmaf(sw[i], sc[i][k], acc[k]);
+                    ws = ws + sw[i];
                 }
             }
             /* Eq. 10; sum w = 0 is a hole even for w_min = 0 (hole colour 0) */

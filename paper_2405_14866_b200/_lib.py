@@ -51,7 +51,7 @@ class RasterParams(C.Structure):
 
 
 class BlendParams(C.Structure):
-    _fields_ = [("delta", C.c_float), ("edge_tau", C.c_float), ("w_min", C.c_float)]
+    _fields_ = [("delta", C.c_float), ("edge_tau", C.c_float), ("w_min", C.c_float), ("tau_c", C.c_float)]
 
 
 class DebugView(C.Structure):

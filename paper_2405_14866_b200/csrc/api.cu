@@ -896,6 +896,7 @@ void ta_default_blend_params(ta_blend_params* bp) {
     bp->delta = 0.01f;
     bp->edge_tau = 0.02f;
     bp->w_min = 1e-4f;
+    bp->tau_c = 0.15f;
 }
 
 ta_status ta_blend(ta_context* c, const ta_source_view* views, int32_t V, const float* const* colors,
@@ -907,9 +908,9 @@ ta_status ta_blend(ta_context* c, const ta_source_view* views, int32_t V, const 
         return fail(c, TA_ERR_INVALID_ARG, "ta_blend: NULL argument");
     if (V < 1 || V > TA_MAX_VIEWS) return fail(c, TA_ERR_UNSUPPORTED, "ta_blend: V = %d not in [1, %d]", V, TA_MAX_VIEWS);
     if (H < 1 || W < 1 || H > 32767 || W > 32767) return fail(c, TA_ERR_INVALID_ARG, "bad target size %d x %d", H, W);
-    if (!(bp->delta > 0.0f) || !(bp->edge_tau > 0.0f) || !(bp->w_min >= 0.0f) || !std::isfinite(bp->delta) ||
-        !std::isfinite(bp->edge_tau) || !std::isfinite(bp->w_min))
-        return fail(c, TA_ERR_INVALID_ARG, "blend params: delta > 0, edge_tau > 0, w_min >= 0");
+    if (!(bp->delta > 0.0f) || !(bp->edge_tau > 0.0f) || !(bp->w_min >= 0.0f) || !(bp->tau_c >= 0.0f) ||
+        !std::isfinite(bp->delta) || !std::isfinite(bp->edge_tau) || !std::isfinite(bp->w_min) || !std::isfinite(bp->tau_c))
+        return fail(c, TA_ERR_INVALID_ARG, "blend params: delta > 0, edge_tau > 0, w_min >= 0, tau_c >= 0");
     if (!std::isfinite(p->z_near) || !std::isfinite(p->d_min)) return fail(c, TA_ERR_INVALID_ARG, "non-finite params");
     ta_status st;
     if (!finite_cam(*K, *RT, c, &st)) return st;
@@ -917,7 +918,7 @@ ta_status ta_blend(ta_context* c, const ta_source_view* views, int32_t V, const 
     memset(&bt, 0, sizeof(bt));
     bt.V = V;
     bt.d_min = p->d_min; bt.z_near = p->z_near;
-    bt.delta = bp->delta; bt.edge_tau = bp->edge_tau; bt.w_min = bp->w_min;
+    bt.delta = bp->delta; bt.edge_tau = bp->edge_tau; bt.w_min = bp->w_min; bt.tau_c = bp->tau_c;
     for (int i = 0; i < V; i++) {
         const ta_source_view& s = views[i];
         if (s.H < 1 || s.W < 1 || s.H > 32767 || s.W > 32767)

@@ -4,7 +4,8 @@
 // views into the novel camera) is lifted (Pi_novel^-1), projected into each input view (Eq. 6),
 // colour and depth are sampled bilinearly there (Eq. 7), weighted by
 // w_i = M_i * Occ * cos<r, n_i> / ||x_i^cam|| (Eqs. 8-9) and normalised (Eq. 10).  DESIGN.md R24
-// fixes the open points (tap rule, edge mask, finite-difference normals, cosine clamp, holes).
+// fixes the open points (tap rule, edge mask, appearance-consistency mask, finite-difference normals,
+// cosine clamp, holes).
 // One thread per novel pixel; views in index order; every step is the fp32 sequence of the
 // oracle's tao_blend written with explicit __f*_rn intrinsics (no contraction), so the result
 // is bit-identical to it.  The input maps are gathered through the read-only path (L1/L2): the
@@ -35,6 +36,8 @@ __global__ void __launch_bounds__(256) k_blend(BlendTable bt, TargetCam cam, con
     if (pix >= npix) return;
     const int v = (int)(pix / (uint32_t)cam.W), u = (int)(pix - (uint32_t)v * cam.W);
     float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f, ws = 0.0f;
+    float sw[kMaxViews], sc[kMaxViews][3];              // pass 1: every contributing view's w_i, c_i
+    int ns = 0;
     const float z = zf[pix];
     if (z > 0.0f) {
         const float* R = cam.R;
@@ -111,14 +114,41 @@ __global__ void __launch_bounds__(256) k_blend(BlendTable bt, TargetCam cam, con
             const float* c10 = bv.color + ((size_t)y0 * bv.W + x1) * 3;
             const float* c01 = bv.color + ((size_t)y1 * bv.W + x0) * 3;
             const float* c11 = bv.color + ((size_t)y1 * bv.W + x1) * 3;
-            float ck[3];
 #pragma unroll
             for (int k = 0; k < 3; k++)
-                ck[k] = lerp_rn(lerp_rn(__ldg(c00 + k), __ldg(c10 + k), ax), lerp_rn(__ldg(c01 + k), __ldg(c11 + k), ax), ay);
-            acc0 = ffma(w, ck[0], acc0);
-            acc1 = ffma(w, ck[1], acc1);
-            acc2 = ffma(w, ck[2], acc2);
-            ws = fadd(ws, w);
+                sc[ns][k] = lerp_rn(lerp_rn(__ldg(c00 + k), __ldg(c10 + k), ax), lerp_rn(__ldg(c01 + k), __ldg(c11 + k), ax), ay);
+            sw[ns++] = w;
+        }
+        // M_i's appearance-consistency mask (R24): m = the weighted median sample (medoid,
+        // the c_i minimising sum_j w_j |c_j - c_i|, ties to the lower view), keep |c_i - m|^2 <= tau_c^2
+        float m0 = 0.0f, m1 = 0.0f, m2 = 0.0f;
+        if (bt.tau_c > 0.0f && ns > 0) {
+            float best = __int_as_float(0x7f800000);
+            int bi = 0;
+#pragma unroll 1
+            for (int i = 0; i < ns; i++) {
+                float cost = 0.0f;
+#pragma unroll 1
+                for (int j = 0; j < ns; j++) {
+                    const float e0 = fsub(sc[j][0], sc[i][0]), e1 = fsub(sc[j][1], sc[i][1]), e2 = fsub(sc[j][2], sc[i][2]);
+                    cost = ffma(sw[j], fsqrt(dot3(e0, e1, e2, e0, e1, e2)), cost);
+                }
+                if (cost < best) { best = cost; bi = i; }
+            }
+            m0 = sc[bi][0]; m1 = sc[bi][1]; m2 = sc[bi][2];
+        }
+        const float tau2 = fmul(bt.tau_c, bt.tau_c);
+        // pass 2: Eq. 10 sums over the consistent samples, in view order
+#pragma unroll 1
+        for (int i = 0; i < ns; i++) {
+            if (bt.tau_c > 0.0f) {
+                const float d0 = fsub(sc[i][0], m0), d1 = fsub(sc[i][1], m1), d2 = fsub(sc[i][2], m2);
+                if (!(dot3(d0, d1, d2, d0, d1, d2) <= tau2)) continue;
+            }
+            acc0 = ffma(sw[i], sc[i][0], acc0);
+            acc1 = ffma(sw[i], sc[i][1], acc1);
+            acc2 = ffma(sw[i], sc[i][2], acc2);
+            ws = fadd(ws, sw[i]);
         }
     }
     // Eq. 10; no weight at all is a hole even when w_min = 0 (holes are colour 0)

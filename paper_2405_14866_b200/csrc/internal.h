@@ -124,7 +124,7 @@ struct BlendView {
 struct BlendTable {
     BlendView v[kMaxViews];
     int V;
-    float d_min, z_near, delta, edge_tau, w_min;
+    float d_min, z_near, delta, edge_tau, w_min, tau_c;
 };
 __global__ void k_blend(BlendTable bt, TargetCam cam, const float* zf, float* rgb, float* wsum);
 

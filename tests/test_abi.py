@@ -34,7 +34,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_c(tmp_path):
     structs = {"ta_intrinsics": _lib.Intrinsics, "ta_extrinsics": _lib.Extrinsics, "ta_source_view": _lib.SourceView,
-               "ta_gaussians": _lib.Gaussians, "ta_raster_params": _lib.RasterParams, "ta_debug_view": _lib.DebugView}
+               "ta_gaussians": _lib.Gaussians, "ta_raster_params": _lib.RasterParams, "ta_debug_view": _lib.DebugView,
+               "ta_blend_params": _lib.BlendParams}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')

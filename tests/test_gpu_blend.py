@@ -124,3 +124,22 @@ def test_w_min_zero_background_is_zero_not_nan(ctx):
     assert np.all(np.isfinite(rgb)) and (ws == 0).sum() > 100
     check_bits(ws, wo)
     check_bits(rgb, ro)
+
+
+@pytest.mark.parametrize("tau_c", [0.15, 0.0])
+def test_appearance_consistency_mask_bit_exact(ctx, tau_c):
+    """The appearance-consistency mask (R24): the textured rig with view 2's colours
+    shifted by +0.5 in green (an inconsistent view), blended into a parallax target -- colours and weight
+    sums bit-exact against the oracle with the mask on (the shifted view is dropped wherever the others
+    agree) and off."""
+    s = sg.make_config("c3", res=192)
+    cam = sg.make_targets("c4", res=192, n_targets=3)[1]
+    colors = [sg.view_colors(v.cam) for v in s.views]
+    colors[2] = colors[2] + np.float32([0.0, 0.5, 0.0])
+    zf, rgb, ws = gpu_blend(ctx, s.views, colors, cam, tau_c=tau_c)
+    zo, ro, wo = oracle_blend(s.views, colors, cam, tau_c=tau_c)
+    check_bits(ws, wo)
+    check_bits(rgb, ro)
+    if tau_c > 0:
+        zf0, rgb0, ws0 = gpu_blend(ctx, s.views, colors, cam, tau_c=0.0)
+        assert (ws < ws0).mean() > 0.05          # the mask removed weight somewhere

@@ -574,13 +574,40 @@ def test_blend_cosine_and_grazing(oracle_lib):
 
 
 def test_blend_two_views_equal_weights_average(oracle_lib):
-    """two views with equal weights and colours a, b -> (a + b) / 2."""
+    """two views with equal weights and colours a, b -> (a + b) / 2 (|a - b| = 0.122 within the
+    appearance-consistency threshold tau_c = 0.15; with the mask off the same holds for any colours)."""
     import oracle
-    va, ca = _plane_view(9, 9, 50.0, 1.5, (0.2, 0.4, 0.6))
-    vb, cb = _plane_view(9, 9, 50.0, 1.5, (0.6, 0.2, 0.0))
+    va, ca = _plane_view(9, 9, 50.0, 1.5, (0.4, 0.3, 0.5))
+    vb, cb = _plane_view(9, 9, 50.0, 1.5, (0.5, 0.35, 0.45))
     _, zf, _ = oracle.zbuffer([va], va.cam, 0.1, radius=0)
     rgb, ws = oracle.blend([va, vb], [ca, cb], va.cam, zf)
-    assert np.allclose(rgb[2:7, 2:7], np.float32([0.4, 0.3, 0.3]), atol=1e-7)
+    assert np.allclose(rgb[2:7, 2:7], np.float32([0.45, 0.325, 0.475]), atol=1e-7)
+    vc, cc = _plane_view(9, 9, 50.0, 1.5, (0.6, 0.2, 0.0))
+    rgb, ws = oracle.blend([va, vc], [ca, cc], va.cam, zf, tau_c=0.0)
+    assert np.allclose(rgb[2:7, 2:7], np.float32([0.5, 0.25, 0.25]), atol=1e-7)
+
+
+def test_blend_appearance_consistency_drops_outlier(oracle_lib):
+    """SPEC.md l.300 / l.331 (the appearance-consistency mask of P:430-433): three equally weighted views
+    of a plane, two agreeing colours a, b and an outlier o (|o - a| = 0.8 > tau_c): the weighted median
+    sample is a or b, o is dropped, I_blend = (a + b) / 2 exactly like two views; the outlier's weight
+    leaves the denominator (wsum = 2 w instead of 3 w).  A tau_c above every distance (or 0 = off)
+    restores the three-view mean; the medoid is a sample, so a pixel never loses all its samples."""
+    import oracle
+    va, ca = _plane_view(9, 9, 50.0, 1.5, (0.4, 0.3, 0.5))
+    vb, cb = _plane_view(9, 9, 50.0, 1.5, (0.45, 0.3, 0.5))
+    vo, co = _plane_view(9, 9, 50.0, 1.5, (0.4, 0.3, 1.3))
+    _, zf, _ = oracle.zbuffer([va], va.cam, 0.1, radius=0)
+    rgb, ws = oracle.blend([va, vb, vo], [ca, cb, co], va.cam, zf)
+    _, ws1 = oracle.blend([va], [ca], va.cam, zf)
+    assert np.allclose(rgb[2:7, 2:7], np.float32([0.425, 0.3, 0.5]), atol=1e-7)
+    assert np.allclose(ws[2:7, 2:7], 2 * ws1[2:7, 2:7], rtol=1e-6)
+    for tau in (0.0, 2.0):
+        rgb3, ws3 = oracle.blend([va, vb, vo], [ca, cb, co], va.cam, zf, tau_c=tau)
+        assert np.allclose(rgb3[2:7, 2:7], np.float32([(0.4 + 0.45 + 0.4) / 3, 0.3, (0.5 + 0.5 + 1.3) / 3]), atol=1e-6)
+        assert np.allclose(ws3[2:7, 2:7], 3 * ws1[2:7, 2:7], rtol=1e-6)
+    rgb2, ws2 = oracle.blend([vo, va], [co, ca], va.cam, zf)        # two disagreeing views: the medoid survives
+    assert np.all(ws2[2:7, 2:7] > 0) and np.allclose(rgb2[2:7, 2:7], np.float32([0.4, 0.3, 1.3]), atol=1e-7)
 
 
 def test_blend_zero_weight_is_hole_even_with_w_min_zero(oracle_lib):

@@ -27,7 +27,7 @@ for rep in sys.argv[1:]:
                  "dram_read": get("dram__bytes_read.sum"), "dram_write": get("dram__bytes_write.sum"),
                  "kernel": vals[h.index("Kernel Name")].split("(")[0].replace("void ", ""),
                  "grid": col("launch__grid_size"), "block": col("launch__block_size"),
-                 "duration_us": None if dur is None else dur * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+                 "duration_us": None if dur is None else dur * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
                                                                  "second": 1e6}.get(units[h.index("gpu__time_duration.sum")], 1.0),
                  "source": os.path.basename(rep)}
 path = os.path.join(ROOT, "profiles", "traffic.json")

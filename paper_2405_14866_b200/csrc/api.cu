@@ -448,6 +448,9 @@ void fill_consts(const ta_raster_params& p, RasterConsts* rc) {
     rc->dilation = p.dilation; rc->alpha_max = p.alpha_max; rc->alpha_min = p.alpha_min; rc->t_eps = p.t_eps;
     rc->cull_sigma = p.cull_sigma; rc->z_near = p.z_near;
     rc->q_max = p.cull_sigma * p.cull_sigma;
+    rc->q_lo_half = -0.5f * rc->q_max;
+    rc->a_max_2k = 2048.0f * p.alpha_max;
+    rc->a_min_2k = 2048.0f * p.alpha_min;
 }
 
 // One rasterization (a2 -- a6) of a Gaussian set into one target.  Gaussian-set mode (pos_alpha / cov
@@ -964,6 +967,9 @@ ta_status ta_rasterize_backward(ta_context* c, const ta_gaussians* g, int64_t n,
     rc.dilation = p->dilation; rc.alpha_max = p->alpha_max; rc.alpha_min = p->alpha_min; rc.t_eps = p->t_eps;
     rc.cull_sigma = p->cull_sigma; rc.z_near = p->z_near;
     rc.q_max = p->cull_sigma * p->cull_sigma;
+    rc.q_lo_half = -0.5f * rc.q_max;
+    rc.a_max_2k = 2048.0f * p->alpha_max;
+    rc.a_min_2k = 2048.0f * p->alpha_min;
     // the pass reuses the forward call's records and tile lists: it must be the same Gaussian set,
     // feature layout, count and constants (a different C would index the feature rows with the wrong
     // stride); grad_F is read with 16-byte vector loads

@@ -555,7 +555,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         const float pxf = (float)px;
         const float2 py2 = make_float2((float)pyA, (float)pyB);
         const float qmax = rc.q_max, teps = rc.t_eps;
-        const float qlo = -0.5f * qmax, amx = 2048.0f * rc.alpha_max, alo = 2048.0f * rc.alpha_min;
+        const float qlo = rc.q_lo_half, amx = rc.a_max_2k, alo = rc.a_min_2k;
         const float qlim = qmax * 1.015625f + 0.01f;
         const uint32_t lt = lanemask_lt();
 

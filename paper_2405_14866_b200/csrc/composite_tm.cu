@@ -198,7 +198,7 @@ k_composite_tm(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     const uint32_t n = cs->n;
     const int W = cg.W, H = cg.H;
     const float qmax = rc.q_max, teps = rc.t_eps;
-    const float qlo = -0.5f * qmax, amx = 2048.0f * rc.alpha_max, alo = 2048.0f * rc.alpha_min;
+    const float qlo = rc.q_lo_half, amx = rc.a_max_2k, alo = rc.a_min_2k;
     const float qlim = qmax * 1.015625f + 0.01f;
     uint32_t* const wq = &const_cast<CallState*>(cs)->scan_counter[6];
     const uint32_t ntiles = (uint32_t)(cg.TX * cg.TY);

@@ -15,6 +15,9 @@ struct TargetCam {
 
 struct RasterConsts {
     float dilation, alpha_max, alpha_min, t_eps, cull_sigma, z_near, q_max;
+    // the compositors' staged scalings (exact powers of two): -q_max / 2, 2^11 alpha_max, 2^11 alpha_min
+    // -- kernel parameters, so the per-entry compares and clamps read them as constant operands
+    float q_lo_half, a_max_2k, a_min_2k;
 };
 
 struct BinGeom {

@@ -511,8 +511,11 @@ __device__ __forceinline__ float2 tstep(float2 q, float2 a, uint32_t mA, uint32_
 // Skip the exp / recurrence of an entry pair no pixel can take (saves ~13 % of pairs, but the
 // warp-wide vote + branch splits the unrolled loop into basic blocks the scheduler cannot overlap;
 // round 2 also measured a q-based skip -- compute both entries' q first, skip when no active in-box
-// pixel has q <= q_max: 1.005 -> 1.11 ms on c3 -- and a per-row refinement of the fill's cull, the
-// active x span of each block row tested at the clamped 1D minimiser: 1.005 -> 1.46 ms).
+// pixel has q <= q_max: 1.005 -> 1.11 ms on c3 -- a per-row refinement of the fill's cull, the
+// active x span of each block row tested at the clamped 1D minimiser: 1.005 -> 1.46 ms -- and a
+// relevance pre-pass over each fill round's staged entries (q of every entry for the active pixels,
+// the kept slots compacted into a permutation the branch-free recurrence walks): 1.005 -> 1.51 ms,
+// the pre-pass alone costing ~29 warp instructions per staged entry).
 constexpr bool kSkipEmptyPairs = false;
 #ifndef TA_TC_MIN_BLOCKS
 #define TA_TC_MIN_BLOCKS 4

@@ -104,7 +104,10 @@ struct CallState {
 };
 
 constexpr int kSortWarps = 8;                                  // warps per block in the sort kernels
-constexpr int kSortKeysPerWarp = 256;                          // depth sort: keys per warp
+#ifndef TA_SORT_KEYS_PER_WARP
+#define TA_SORT_KEYS_PER_WARP 384   // 256: 111.6 us, 384: 106.3 us, 512: 115.9 us per c3 sort (round 2)
+#endif
+constexpr int kSortKeysPerWarp = TA_SORT_KEYS_PER_WARP;                          // depth sort: keys per warp
 constexpr int kSortKeysPerBlock = kSortWarps * kSortKeysPerWarp;   // keys per block (= partition)
 
 // Number of LSD passes of 8 bits covering the varying bits of the visible depth keys.

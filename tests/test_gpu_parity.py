@@ -473,3 +473,17 @@ def test_tensor_memory_compositor_parity(oracle_lib, cfg):
         os.environ.pop("TA_COMPOSITOR")
     s = sg.make_config("c2") if cfg == "c2" else sg.make_config("c3", res=256, target_hw=(136, 200))
     full_parity(c, oracle_lib, s)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3r"])
+def test_fp32_features_timed_instantiation(ctx, oracle_lib, cfg):
+    """fp32-stored features take k_composite<C, float, false> (the SIMT compositor; the counters
+    instantiation runs after it and must give the same bits): c2 at full size and the reduced ragged
+    c3 with their fp16 feature maps widened to fp32 (exact), every stage and every pixel against the
+    oracle."""
+    s = sg.make_config("c2") if cfg == "c2" else sg.make_config("c3", res=256, target_hw=(136, 200))
+    for v in s.views:
+        v.feat = v.feat.astype(np.float32)
+    s.feat_dtype = "f32"
+    out, err = full_parity(ctx, oracle_lib, s)
+    assert out["K"] > 0

@@ -487,3 +487,32 @@ def test_fp32_features_timed_instantiation(ctx, oracle_lib, cfg):
     s.feat_dtype = "f32"
     out, err = full_parity(ctx, oracle_lib, s)
     assert out["K"] > 0
+
+
+@pytest.mark.parametrize("case", [
+    dict(cull_sigma=2.0, alpha_max=0.9, alpha_min=0.0, t_eps=1e-2, dilation=0.0),
+    dict(cull_sigma=4.0, alpha_max=0.999, alpha_min=0.02, t_eps=1e-5, dilation=1.0),
+    dict(cull_sigma=3.0, alpha_max=0.5, alpha_min=1.0 / 255.0, t_eps=0.3, dilation=0.3),
+])
+@pytest.mark.parametrize("C,dt", [(32, "f16"), (8, "f16"), (16, "f32")])
+def test_non_default_raster_params(ctx, oracle_lib, case, C, dt):
+    """Every raster constant is a parameter (R7-R10): the box width and q cut (cull_sigma), the alpha'
+    clamp, the low-alpha skip, the stop threshold and the low-pass dilation away from their defaults,
+    through every compositor instantiation (fp16 mma.sync C = 32 / 8, fp32 SIMT) -- every stage and every
+    pixel against the oracle on a ragged random scene and the reduced rig."""
+    s = sg.make_random_scene(11 + C, H=53, W=77, C=C, n_src=28, feat_dtype=dt)
+    full_parity(ctx, oracle_lib, s, **case)
+    r = sg.make_config("c3", res=128, target_hw=(72, 88))
+    if dt == "f32" or C != 32:
+        for v in r.views:
+            v.feat = v.feat[..., :C].astype(np.float32 if dt == "f32" else np.float16)
+        r.C, r.feat_dtype = C, dt
+    full_parity(ctx, oracle_lib, r, **case)
+
+
+@pytest.mark.parametrize("hw", [(1, 1), (1, 37), (45, 1), (17, 16)])
+def test_degenerate_target_shapes(ctx, oracle_lib, hw):
+    """Single-pixel, single-row, single-column and one-tile-plus-one-row targets (ragged tiles, boxes
+    clamped to the image on every side): every stage and pixel against the oracle."""
+    s = sg.make_random_scene(5, H=hw[0], W=hw[1], C=16, n_src=24, feat_dtype="f16")
+    full_parity(ctx, oracle_lib, s)

@@ -256,11 +256,11 @@ def run_ours(args):
     from paper_2405_14866_b200 import dist as tdist
     mine = tdist.shard(n_views, rank, world)
     ctx = tb.Context(local)
-    # views alternate over `streams` (context, CUDA stream) pairs so one view's projection / sort /
-    # binning overlaps the previous view's compositing tail (one context per stream: its own scratch)
-    nstr = max(1, args.streams)
-    ctxs = [ctx] + [tb.Context(local) for _ in range(nstr - 1)]
-    side = [torch.cuda.Stream() for _ in range(nstr)]
+    # a frame's views go through one ta_rasterize_views call: inside the library they alternate over
+    # `streams` lanes ((context, CUDA stream) pairs owned by ctx) so one view's projection / sort /
+    # binning overlaps another's compositing
+    nstr = max(1, min(4, args.streams))
+    ctxs = [ctx]
     C_, H, W = 32, 1024, 1024
     cap = 4 * 1024 * 1024
     g = tb.GaussianBuffers(cap, C_, "f16", device=dev)
@@ -285,24 +285,20 @@ def run_ours(args):
         if world > 1:
             tdist.broadcast_gaussians((gb.pos_alpha, gb.cov, gb.feat), gb.n_dev, src=0, rows=bcast_rows["rows"])
 
+    Ks = [c[0] for c in cams]
+    RTs = [c[1] for c in cams]
+    Fs = [o[0] for o in outs]
+    As = [o[1] for o in outs]
+
+    def render(gb, p):
+        if cams:
+            ctx.rasterize_views(gb, -1, Ks, RTs, H, W, p, Fs, As, lanes=nstr, stream=stream)
+
     def step(p):
         if rank == 0:
             ctx.unproject(views, params_sync, g, stream)
         broadcast()
-        if nstr == 1:
-            for (Ki, Ri), (F, A) in zip(cams, outs):
-                ctx.rasterize(g, -1, Ki, Ri, H, W, p, F, A, stream)
-            return
-        ready = torch.cuda.Event()
-        ready.record(stream)
-        for sd in side:
-            sd.wait_event(ready)
-        for k, ((Ki, Ri), (F, A)) in enumerate(zip(cams, outs)):
-            ctxs[k % nstr].rasterize(g, -1, Ki, Ri, H, W, p, F, A, side[k % nstr])
-        for sd in side:
-            done = torch.cuda.Event()
-            done.record(sd)
-            stream.wait_event(done)
+        render(g, p)
 
     # Steady-state frame pipeline: two Gaussian sets; while the views of frame f render
     # from one set, the next frame is lifted (rank 0) and NCCL-broadcast into the other set on a
@@ -329,16 +325,9 @@ def run_ours(args):
         cur = pipe["k"] % 2
         if pipe["ready"] is None:
             pipe["ready"] = prepare(cur)
-        for sd in side:
-            sd.wait_event(pipe["ready"])
-        gb = gsets[cur]
-        for k, ((Ki, Ri), (F, A)) in enumerate(zip(cams, outs)):
-            ctxs[k % nstr].rasterize(gb, -1, Ki, Ri, H, W, p, F, A, side[k % nstr])
+        stream.wait_event(pipe["ready"])
+        render(gsets[cur], p)
         free = torch.cuda.Event()
-        for sd in side:
-            done = torch.cuda.Event()
-            done.record(sd)
-            stream.wait_event(done)
         free.record(stream)
         pipe["free"][cur] = free
         pipe["k"] += 1
@@ -355,8 +344,7 @@ def run_ours(args):
         kmax, kcmax = max(kmax, d.K), max(kcmax, d.Kc)
     n_g = g.n
     bcast_rows["rows"] = n_g                        # the frame's Gaussian count (same scene every frame)
-    for cx in ctxs:
-        cx.reserve(cap, int(kcmax * 1.05) + 4096, H, W)
+    ctx.reserve(cap, int(kcmax * 1.05) + 4096, H, W)    # also sizes the lanes' child contexts
 
     def barrier():
         if world > 1:
@@ -368,7 +356,7 @@ def run_ours(args):
     def sum_over_ranks(x):
         return tdist.reduce_scalar(x, "sum", device=dev)
 
-    timed_step = step_pipelined if nstr > 1 else step
+    timed_step = step_pipelined
     for _ in range(args.warmup):
         timed_step(params)
     torch.cuda.synchronize()
@@ -474,7 +462,7 @@ def run_ours(args):
 
     # ---------------- render + gather of every view to rank 0
     if world > 1 and not args.no_gather:
-        line["render_gather"] = render_gather(args, ctxs, side, g, cams, outs, mine, n_views, H, W, C_, params,
+        line["render_gather"] = render_gather(args, ctx, nstr, g, cams, outs, mine, n_views, H, W, C_, params,
                                               rank, world, stream, broadcast, barrier, max_over_ranks)
 
     # ---------------- end to end through the C ABI with host buffers
@@ -580,27 +568,17 @@ def c3_single_view(args, ctx, g, views, params, params_sync, H, W, C_, n_g, stre
                       "TA_FLAG_ASYNC after ta_reserve (no host sync inside the call)"}
 
 
-def render_gather(args, ctxs, side, g, cams, outs, mine, n_views, H, W, C_, params, rank, world, stream, broadcast,
+def render_gather(args, ctx, lanes, g, cams, outs, mine, n_views, H, W, C_, params, rank, world, stream, broadcast,
                   barrier, max_over_ranks):
     """Render + gather to rank 0: per step every rank renders its views (as in the
     timed step) and every view's F and A go to rank 0 by collective gathers (ncclGather over
     NVLink / NVSwitch).  Rank 0's ingress bound = (N-1)/N x 32 x 4HW(C+1) bytes / link bandwidth."""
     import torch
     from paper_2405_14866_b200 import dist as tdist
-    nstr = len(ctxs)
-
     def step():
         broadcast()
-        ready = torch.cuda.Event()
-        ready.record(stream)
-        for sd in side:
-            sd.wait_event(ready)
-        for k, ((Ki, Ri), (F, A)) in enumerate(zip(cams, outs)):
-            ctxs[k % nstr].rasterize(g, -1, Ki, Ri, H, W, params, F, A, side[k % nstr])
-        for sd in side:
-            done = torch.cuda.Event()
-            done.record(sd)
-            stream.wait_event(done)
+        ctx.rasterize_views(g, -1, [c[0] for c in cams], [c[1] for c in cams], H, W, params, [o[0] for o in outs],
+                            [o[1] for o in outs], lanes=lanes, stream=stream)
         tdist.gather_views([F for F, _ in outs], n_views, rank, world)
         tdist.gather_views([A for _, A in outs], n_views, rank, world)
 

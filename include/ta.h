@@ -157,6 +157,21 @@ ta_status ta_rasterize(ta_context* ctx, const ta_gaussians* g, int64_t n, const 
                        float* feat_out, float* alpha_out, void* stream);
 
 /*
+ * The multi-view display workload (the autostereoscopic screen shows every view
+ * from leftmost to rightmost): one Gaussian set rendered into T targets, all H x W, in one
+ * call.  Equivalent to T calls of ta_rasterize (identical output bits) but the targets are spread
+ * round-robin over `lanes` (1..4) lanes: lane 0 = ctx on `stream`, lanes 1.. = child contexts (own
+ * scratch) on child streams owned by ctx, forked from and joined back into `stream`, so one target's
+ * projection / sort / binning overlaps another's compositing.  ta_reserve on ctx also sizes the child
+ * contexts (needed for TA_FLAG_ASYNC).  K_tgt, RT_tgt: host arrays of T; feat_out, alpha_out: host
+ * arrays of T device pointers.  ta_debug_last describes the last target of lane 0.  Errors as
+ * ta_rasterize; T < 1 or lanes outside [1, 4] is TA_ERR_INVALID_ARG.
+ */
+ta_status ta_rasterize_views(ta_context* ctx, const ta_gaussians* g, int64_t n, int32_t T, const ta_intrinsics* K_tgt,
+                             const ta_extrinsics* RT_tgt, int32_t H, int32_t W, const ta_raster_params* params,
+                             float* const* feat_out, float* const* alpha_out, int32_t lanes, void* stream);
+
+/*
  * north_star (a) -- the fused front end: lift the foreground pixels of V source views (a1), project and
  * cull them for T targets (a2) in ONE pass over the source maps (128-bit loads), then bin, sort and
  * composite each target (a3-a6) exactly as ta_rasterize does.  Equivalent to ta_unproject followed by
@@ -281,8 +296,9 @@ typedef struct {
 } ta_debug_view;
 ta_status ta_debug_last(ta_context* ctx, ta_debug_view* out, void* stream);
 
-/* Synchronise `stream` and report whether any TA_FLAG_ASYNC call since the last check overflowed
-   reserved scratch (*overflowed = 1) -- TA_ERR_CAPACITY is also returned in that case. */
+/* Synchronise `stream` (and the context's lane streams) and report whether any TA_FLAG_ASYNC call since
+   the last check -- on the context or its lanes' child contexts -- overflowed reserved scratch
+   (*overflowed = 1); TA_ERR_CAPACITY is also returned in that case. */
 ta_status ta_check_overflow(ta_context* ctx, void* stream, int32_t* overflowed);
 
 /*

@@ -69,7 +69,7 @@ class Profile(C.Structure):
     _fields_ = [("ms", C.c_double * 7), ("calls", C.c_uint64 * 7)]
 
 
-EXPORTS = ("ta_render_sources", "ta_profile_enable", "ta_profile_read", "ta_default_params", "ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject",
+EXPORTS = ("ta_rasterize_views", "ta_render_sources", "ta_profile_enable", "ta_profile_read", "ta_default_params", "ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject",
            "ta_zbuffer", "ta_blend", "ta_default_blend_params", "ta_rasterize_backward",
            "ta_rasterize", "ta_debug_last", "ta_check_overflow", "ta_launch_count", "ta_status_string",
            "ta_last_error", "ta_build_info")
@@ -105,6 +105,8 @@ def lib(build_if_stale: bool = False):
     L.ta_zbuffer.argtypes = [P, C.POINTER(SourceView), i32, C.POINTER(RasterParams), C.POINTER(Intrinsics),
                              C.POINTER(Extrinsics), i32, i32, i32, C.c_float, P, P, P]
     L.ta_check_overflow.argtypes = [P, P, C.POINTER(i32)]
+    L.ta_rasterize_views.argtypes = [P, C.POINTER(Gaussians), i64, i32, C.POINTER(Intrinsics), C.POINTER(Extrinsics),
+                                     i32, i32, C.POINTER(RasterParams), C.POINTER(P), C.POINTER(P), i32, P]
     L.ta_render_sources.argtypes = [P, C.POINTER(SourceView), i32, i32, i32, C.POINTER(RasterParams), i32,
                                     C.POINTER(Intrinsics), C.POINTER(Extrinsics), i32, i32, C.POINTER(P), C.POINTER(P), P]
     L.ta_profile_enable.argtypes = [P, i32]
@@ -117,7 +119,7 @@ def lib(build_if_stale: bool = False):
     L.ta_last_error.restype = C.c_char_p
     L.ta_build_info.restype = C.c_char_p
     for name in ("ta_context_create", "ta_context_destroy", "ta_reserve", "ta_unproject", "ta_rasterize", "ta_zbuffer",
-                 "ta_blend", "ta_rasterize_backward", "ta_render_sources",
+                 "ta_blend", "ta_rasterize_backward", "ta_render_sources", "ta_rasterize_views",
                  "ta_debug_last", "ta_check_overflow", "ta_profile_enable", "ta_profile_read"):
         getattr(L, name).restype = i32
     _lib = L
@@ -222,6 +224,20 @@ class Context:
         gs = g.struct()
         self._check(lib().ta_rasterize(self._h, C.byref(gs), int(n), C.byref(K), C.byref(RT), int(H), int(W),
                                        C.byref(params), _ptr(feat_out), _ptr(alpha_out), _stream(stream)))
+
+    def rasterize_views(self, g: "GaussianBuffers", n, Ks, RTs, H, W, params: RasterParams, feat_outs, alpha_outs,
+                        lanes: int = 4, stream=None):
+        """Multi-view rendering (include/ta.h ta_rasterize_views): one Gaussian set into len(Ks) targets,
+        spread over `lanes` (context, stream) lanes inside the library; Ks / RTs = Intrinsics / Extrinsics
+        structs, feat_outs / alpha_outs = CUDA tensors [H, W, C] / [H, W] per target."""
+        T = len(Ks)
+        gs = g.struct()
+        ka = (Intrinsics * T)(*Ks)
+        ra = (Extrinsics * T)(*RTs)
+        fo = (C.c_void_p * T)(*[f.data_ptr() for f in feat_outs])
+        ao = (C.c_void_p * T)(*[a.data_ptr() for a in alpha_outs])
+        self._check(lib().ta_rasterize_views(self._h, C.byref(gs), int(n), T, ka, ra, int(H), int(W), C.byref(params),
+                                             fo, ao, int(lanes), _stream(stream)))
 
     def render_sources(self, views, C_: int, feat_dtype: str, params: RasterParams, Ks, RTs, H, W, feat_outs, alpha_outs,
                        stream=None):

@@ -49,6 +49,8 @@ struct ta_context {
     ta_context* aux[kMaxFrontTargets - 1] = {nullptr, nullptr, nullptr};
     cudaStream_t aux_stream[kMaxFrontTargets - 1] = {nullptr, nullptr, nullptr};
     cudaEvent_t aux_ev[kMaxFrontTargets] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t rsv_g = -1, rsv_e = 0;  // the last ta_reserve (applied to child contexts created later)
+    int32_t rsv_H = 0, rsv_W = 0;
     uint64_t* pinned = nullptr;
     uint32_t status_region = 0;   // words per scan slot
     // last rasterize call
@@ -480,6 +482,27 @@ struct RasterJob {
 
 ta_status raster_pipeline(ta_context* c, const RasterJob& job);
 
+// Child contexts (own scratch) + non-blocking streams for lanes 1..L-1 of the multi-target calls, and
+// the events that fork from / join into the caller's stream.  A reservation made on the parent is
+// applied to children created later.
+ta_status ensure_lanes(ta_context* c, int L) {
+    for (int k = 1; k < L; k++) {
+        if (!c->aux[k - 1]) {
+            ta_status cst = ta_context_create(c->device, &c->aux[k - 1]);
+            if (cst != TA_OK) return fail(c, cst, "child context %d", k);
+            c->aux[k - 1]->compositor = c->compositor;
+            if (cudaStreamCreateWithFlags(&c->aux_stream[k - 1], cudaStreamNonBlocking) != cudaSuccess)
+                return fail(c, TA_ERR_CUDA, "child stream %d", k);
+            if (c->rsv_g >= 0 && (cst = ta_reserve(c->aux[k - 1], c->rsv_g, c->rsv_e, c->rsv_H, c->rsv_W)) != TA_OK)
+                return fail(c, cst, "child reserve: %s", c->aux[k - 1]->err.c_str());
+        }
+    }
+    for (int k = 0; k < L; k++)
+        if (!c->aux_ev[k] && cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming) != cudaSuccess)
+            return fail(c, TA_ERR_CUDA, "lane event");
+    return TA_OK;
+}
+
 bool params_ok(const ta_raster_params& p) {
     return (p.cull_sigma > 0.0f && p.cull_sigma <= 12.0f) && (p.alpha_max > 0.0f && p.alpha_max < 1.0f) &&
            (p.t_eps > 0.0f && p.t_eps < 1.0f) && (p.alpha_min >= 0.0f) && (p.dilation >= 0.0f) && std::isfinite(p.z_near);
@@ -501,7 +524,12 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     BinGeom bg;
     if ((st = bin_geometry(c, H, W, max_gaussians, &bg)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, max_gaussians, H, W)) != TA_OK) return st;
-    return reserve_lists(c, (size_t)std::max<int64_t>(max_entries, 1), bg.shift);
+    if ((st = reserve_lists(c, (size_t)std::max<int64_t>(max_entries, 1), bg.shift)) != TA_OK) return st;
+    c->rsv_g = max_gaussians; c->rsv_e = max_entries; c->rsv_H = H; c->rsv_W = W;
+    for (int k = 0; k < kMaxFrontTargets - 1; k++)
+        if (c->aux[k] && (st = ta_reserve(c->aux[k], max_gaussians, max_entries, H, W)) != TA_OK)
+            return fail(c, st, "child context: %s", c->aux[k]->err.c_str());
+    return TA_OK;
 }
 
 ta_status ta_unproject(ta_context* c, const ta_source_view* views, int32_t V, const ta_raster_params* p,
@@ -738,6 +766,37 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
 extern "C" {
 
 
+ta_status ta_rasterize_views(ta_context* c, const ta_gaussians* g, int64_t n, int32_t T, const ta_intrinsics* K_tgt,
+                            const ta_extrinsics* RT_tgt, int32_t H, int32_t W, const ta_raster_params* p,
+                            float* const* feat_out, float* const* alpha_out, int32_t lanes, void* stream) {
+    if (!c) return TA_ERR_INVALID_ARG;
+    if (!g || !K_tgt || !RT_tgt || !p || !feat_out || !alpha_out)
+        return fail(c, TA_ERR_INVALID_ARG, "ta_rasterize_views: NULL argument");
+    if (T < 1) return fail(c, TA_ERR_INVALID_ARG, "T = %d < 1", T);
+    if (lanes < 1 || lanes > kMaxFrontTargets) return fail(c, TA_ERR_INVALID_ARG, "lanes = %d not in [1, %d]", lanes, kMaxFrontTargets);
+    cudaSetDevice(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = std::min<int>(lanes, T);
+    ta_status st;
+    if ((st = ensure_lanes(c, L)) != TA_OK) return st;
+    if (L > 1) {
+        TA_CUDA(c, cudaEventRecord(c->aux_ev[0], s));
+        for (int k = 1; k < L; k++) TA_CUDA(c, cudaStreamWaitEvent(c->aux_stream[k - 1], c->aux_ev[0], 0));
+    }
+    for (int t = 0; t < T; t++) {                  // targets round-robin over the lanes, in order per lane
+        const int k = t % L;
+        ta_context* ct = k == 0 ? c : c->aux[k - 1];
+        st = ta_rasterize(ct, g, n, &K_tgt[t], &RT_tgt[t], H, W, p, feat_out[t], alpha_out[t],
+                          k == 0 ? stream : (void*)c->aux_stream[k - 1]);
+        if (st != TA_OK) return ct == c ? st : fail(c, st, "target %d: %s", t, ct->err.c_str());
+    }
+    for (int k = 1; k < L; k++) {                  // the call completes on `stream`
+        TA_CUDA(c, cudaEventRecord(c->aux_ev[k], c->aux_stream[k - 1]));
+        TA_CUDA(c, cudaStreamWaitEvent(s, c->aux_ev[k], 0));
+    }
+    return TA_OK;
+}
+
 ta_status ta_render_sources(ta_context* c, const ta_source_view* views, int32_t V, int32_t C, ta_dtype feat_dtype,
                             const ta_raster_params* p, int32_t T, const ta_intrinsics* K_tgt, const ta_extrinsics* RT_tgt,
                             int32_t H, int32_t W, float* const* feat_out, float* const* alpha_out, void* stream) {
@@ -803,16 +862,7 @@ ta_status ta_render_sources(ta_context* c, const ta_source_view* views, int32_t 
     TA_LAUNCHED(c);
     tm.end();
     // targets 1..T-1 run on child contexts / streams concurrently with target 0 (after the front end)
-    for (int t = 1; t < T; t++) {
-        if (!c->aux[t - 1]) {
-            ta_status cst = ta_context_create(c->device, &c->aux[t - 1]);
-            if (cst != TA_OK) return fail(c, cst, "child context for target %d", t);
-            c->aux[t - 1]->compositor = c->compositor;
-            TA_CUDA(c, cudaStreamCreateWithFlags(&c->aux_stream[t - 1], cudaStreamNonBlocking));
-        }
-    }
-    for (int k = 0; k < T; k++)
-        if (!c->aux_ev[k]) TA_CUDA(c, cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
+    if ((st = ensure_lanes(c, T)) != TA_OK) return st;
     if (T > 1) {
         TA_CUDA(c, cudaEventRecord(c->aux_ev[0], s));
         for (int t = 1; t < T; t++) TA_CUDA(c, cudaStreamWaitEvent(c->aux_stream[t - 1], c->aux_ev[0], 0));
@@ -1080,8 +1130,16 @@ ta_status ta_check_overflow(ta_context* c, void* stream, int32_t* overflowed) {
     TA_CUDA(c, cudaStreamSynchronize(s));
     const uint32_t zero = 0;
     TA_CUDA(c, cudaMemcpy((char*)c->cs.p + offsetof(CallState, overflow), &zero, 4, cudaMemcpyHostToDevice));
-    if (overflowed) *overflowed = h.overflow ? 1 : 0;
-    return h.overflow ? fail(c, TA_ERR_CAPACITY, "tile-entry capacity overflowed in an async call") : TA_OK;
+    bool over = h.overflow != 0;
+    for (int k = 0; k < kMaxFrontTargets - 1; k++) {        // the lanes' child contexts
+        if (!c->aux[k]) continue;
+        TA_CUDA(c, cudaStreamSynchronize(c->aux_stream[k]));
+        int32_t o = 0;
+        ta_check_overflow(c->aux[k], (void*)c->aux_stream[k], &o);
+        over = over || o != 0;
+    }
+    if (overflowed) *overflowed = over ? 1 : 0;
+    return over ? fail(c, TA_ERR_CAPACITY, "tile-entry capacity overflowed in an async call") : TA_OK;
 }
 
 }  // extern "C"

@@ -516,3 +516,38 @@ def test_degenerate_target_shapes(ctx, oracle_lib, hw):
     clamped to the image on every side): every stage and pixel against the oracle."""
     s = sg.make_random_scene(5, H=hw[0], W=hw[1], C=16, n_src=24, feat_dtype="f16")
     full_parity(ctx, oracle_lib, s)
+
+
+@pytest.mark.parametrize("lanes,async_", [(1, False), (3, False), (4, True)])
+def test_rasterize_views_equals_single_calls(ctx, lanes, async_):
+    """ta_rasterize_views (one Gaussian set into T targets, spread over the context's lanes inside the
+    library) is bit-identical to T ta_rasterize calls, in sync mode and with TA_FLAG_ASYNC after
+    ta_reserve (which sizes the child contexts too); 7 parallax targets of the reduced c4."""
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("c4", res=256, target_hw=(200, 248), n_targets=7)
+    gp = P.gpu_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    refs, kc = [], 0
+    for cam in s.targets:
+        r = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
+        kc = max(kc, ctx.debug_last().Kc)
+        refs.append(r)
+    cx = tb.Context(0)
+    p = gp
+    if async_:
+        cx.reserve(g.capacity, int(kc * 1.1) + 1024, 200, 248)
+        p = P.gpu_params(s, flags=tb.TA_FLAG_ASYNC)
+    Ks, RTs = [], []
+    for cam in s.targets:
+        K, R, t = sg.cam_arrays(cam)
+        Ks.append(tb.intrinsics(K))
+        RTs.append(tb.extrinsics(R, t))
+    Fs = [torch.empty((200, 248, s.C), device="cuda") for _ in s.targets]
+    As = [torch.empty((200, 248), device="cuda") for _ in s.targets]
+    cx.rasterize_views(g, -1, Ks, RTs, 200, 248, p, Fs, As, lanes=lanes)
+    torch.cuda.synchronize()
+    assert not cx.check_overflow()
+    for F, A, r in zip(Fs, As, refs):
+        assert np.array_equal(F.cpu().numpy().view(np.uint32), r["F"].view(np.uint32))
+        assert np.array_equal(A.cpu().numpy().view(np.uint32), r["A"].view(np.uint32))

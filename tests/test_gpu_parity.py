@@ -551,3 +551,21 @@ def test_rasterize_views_equals_single_calls(ctx, lanes, async_):
     for F, A, r in zip(Fs, As, refs):
         assert np.array_equal(F.cpu().numpy().view(np.uint32), r["F"].view(np.uint32))
         assert np.array_equal(A.cpu().numpy().view(np.uint32), r["A"].view(np.uint32))
+
+
+def test_rasterize_views_invalid_arguments(ctx):
+    import torch
+    import paper_2405_14866_b200 as tb
+    s = sg.make_config("tiny", res=16)
+    gp = P.gpu_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    K, R, t = sg.cam_arrays(s.targets[0])
+    F = torch.empty((16, 16, 8), device="cuda")
+    A = torch.empty((16, 16), device="cuda")
+    for lanes in (0, 5):
+        with pytest.raises(tb.TaError) as e:
+            ctx.rasterize_views(g, -1, [tb.intrinsics(K)], [tb.extrinsics(R, t)], 16, 16, gp, [F], [A], lanes=lanes)
+        assert e.value.status == 1
+    with pytest.raises(tb.TaError) as e:
+        ctx.rasterize_views(g, -1, [], [], 16, 16, gp, [], [], lanes=2)
+    assert e.value.status == 1

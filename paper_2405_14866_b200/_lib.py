@@ -151,6 +151,12 @@ def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _raw(t):
+    """A device address: a CUDA tensor's data pointer, or an integer address as is (e.g. a peer mapping
+    opened with CUDA IPC, paper_2405_14866_b200.dist.PeerFrame)."""
+    return int(t) if isinstance(t, int) else t.data_ptr()
+
+
 def _stream(stream):
     if stream is None:
         import torch
@@ -229,13 +235,14 @@ class Context:
                         lanes: int = 4, stream=None):
         """Multi-view rendering (include/ta.h ta_rasterize_views): one Gaussian set into len(Ks) targets,
         spread over `lanes` (context, stream) lanes inside the library; Ks / RTs = Intrinsics / Extrinsics
-        structs, feat_outs / alpha_outs = CUDA tensors [H, W, C] / [H, W] per target."""
+        structs, feat_outs / alpha_outs = CUDA tensors [H, W, C] / [H, W] per target or integer device addresses
+        (e.g. views of another rank's frame buffer mapped over NVLink, dist.PeerFrame)."""
         T = len(Ks)
         gs = g.struct()
         ka = (Intrinsics * T)(*Ks)
         ra = (Extrinsics * T)(*RTs)
-        fo = (C.c_void_p * T)(*[f.data_ptr() for f in feat_outs])
-        ao = (C.c_void_p * T)(*[a.data_ptr() for a in alpha_outs])
+        fo = (C.c_void_p * T)(*[_raw(f) for f in feat_outs])
+        ao = (C.c_void_p * T)(*[_raw(a) for a in alpha_outs])
         self._check(lib().ta_rasterize_views(self._h, C.byref(gs), int(n), T, ka, ra, int(H), int(W), C.byref(params),
                                              fo, ao, int(lanes), _stream(stream)))
 

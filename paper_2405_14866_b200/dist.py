@@ -82,6 +82,80 @@ def gather_views(local_views: Sequence, n_views: int, rank: int, world: int, dst
     return None
 
 
+class _CAI:
+    """__cuda_array_interface__ wrapper of a raw device allocation (so torch can view it)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerFrame:
+    """The display rank's frame buffer -- F [n_views, H, W, C] and A [n_views, H, W], fp32 -- mapped into
+    every rank's address space with CUDA IPC, so each rank's compositor writes its views' tiles straight
+    into the display rank's memory (over NVLink / NVSwitch between GPUs): the render + gather of SURVEY
+    8(e)(ii) fused into the compositor's output stores, with no separate gather pass.  Pass
+    `view_ptrs(j)` as the feat_out / alpha_out of ta_rasterize_views (integer addresses are accepted).
+    Completion: every rank synchronises its stream, then a barrier; after it the display rank reads
+    `F` / `A` (torch views of the allocation).  The IPC handles travel by broadcast_object_list, so any
+    backend works (NCCL on GPUs, gloo in the tests)."""
+
+    def __init__(self, n_views: int, H: int, W: int, C: int, rank: int, world: int, dst: int = 0, group=None):
+        import torch
+        import torch.distributed as dist
+        from cuda.bindings import runtime as rt
+        self._rt = rt
+        self.n_views, self.H, self.W, self.C, self.rank, self.dst = n_views, H, W, C, rank, dst
+        self.fbytes = H * W * C * 4
+        self.abytes = H * W * 4
+        self.F = self.A = None
+        self._own = []
+        self._opened = []
+        if rank == dst:
+            err, pf = rt.cudaMalloc(n_views * self.fbytes)
+            assert err == rt.cudaError_t.cudaSuccess, err
+            err, pa = rt.cudaMalloc(n_views * self.abytes)
+            assert err == rt.cudaError_t.cudaSuccess, err
+            self._own = [pf, pa]
+            self.pF, self.pA = int(pf), int(pa)
+            self.F = torch.as_tensor(_CAI(self.pF, (n_views, H, W, C), "<f4"), device="cuda")
+            self.A = torch.as_tensor(_CAI(self.pA, (n_views, H, W), "<f4"), device="cuda")
+            handles = []
+            for p in (pf, pa):
+                err, h = rt.cudaIpcGetMemHandle(p)
+                assert err == rt.cudaError_t.cudaSuccess, err
+                handles.append(bytes(h.reserved))
+            obj = [handles]
+        else:
+            obj = [None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=dst, group=group)
+        if rank != dst:
+            ptrs = []
+            for hb in obj[0]:
+                h = rt.cudaIpcMemHandle_t()
+                h.reserved = hb
+                err, p = rt.cudaIpcOpenMemHandle(h, rt.cudaIpcMemLazyEnablePeerAccess)
+                assert err == rt.cudaError_t.cudaSuccess, err
+                ptrs.append(p)
+            self._opened = ptrs
+            self.pF, self.pA = int(ptrs[0]), int(ptrs[1])
+
+    def view_ptrs(self, j: int):
+        """(F, A) device addresses of view j in this rank's mapping of the frame."""
+        return self.pF + j * self.fbytes, self.pA + j * self.abytes
+
+    def close(self):
+        rt = self._rt
+        for p in self._opened:
+            rt.cudaIpcCloseMemHandle(p)
+        self._opened = []
+        self.F = self.A = None
+        for p in self._own:
+            rt.cudaFree(p)
+        self._own = []
+
+
 def reduce_scalar(x: float, op: str, device=None, group=None) -> float:
     """max / sum of a host scalar over ranks (timing is the max over ranks)."""
     import torch

@@ -469,7 +469,10 @@ struct TcBuf {
     static constexpr int WP = 36;      // weight row pitch (32-bit words): 144 B, odd number of 16-B chunks
     // C = 64: the accumulators of channels 32..63 live in shared memory (lane-private float4 slots)
     // and 32 entries are staged at a time, so 3 CTAs fit per SM instead of 2 (registers / smem)
-    static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : NT, NTS = NT - NTR;
+#ifndef TA_TC_NTR32
+#define TA_TC_NTR32 4
+#endif
+    static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : (C == 32 ? TA_TC_NTR32 : NT), NTS = NT - NTR;
     static constexpr int NB = C >= 64 ? 32 : TA_TC_NB;   // entries staged per warp at a time
     // staged records, entry pairs (2k, 2k+1) interleaved so that the compacted mode loads its packed
     // (entry, entry) operands directly: p[k][0] = (mx, mx', my, my'), [1] = (-ca/2, .., -cb2/2, ..),

@@ -615,10 +615,25 @@ def render_into_peer_frame(args, ctx, lanes, g, cams, mine, n_views, H, W, C_, p
     then a host barrier marks the frame complete on rank 0."""
     import torch
     from paper_2405_14866_b200 import dist as tdist
+    frame, why = None, ""
     try:
         frame = tdist.PeerFrame(n_views, H, W, C_, rank, world)
     except Exception as e:                      # no CUDA IPC / peer access on this box
-        return {"unavailable": f"{type(e).__name__}: {e}"}
+        why = f"{type(e).__name__}: {e}"
+    # every rank must take the same branch (the steps below are collectives)
+    ok = tdist.reduce_scalar(0.0 if frame is None else 1.0, "sum", device=torch.device("cuda")) == world
+    if not ok:
+        if frame is not None:
+            barrier()
+            if rank != 0:
+                frame.close()
+            barrier()
+            if rank == 0:
+                frame.close()
+        else:
+            barrier()
+            barrier()
+        return {"unavailable": why or "CUDA IPC mapping failed on another rank"}
     fp, ap = zip(*[frame.view_ptrs(j) for j in mine]) if mine else ((), ())
     Ks, RTs = [c[0] for c in cams], [c[1] for c in cams]
 

@@ -111,25 +111,31 @@ class PeerFrame:
         self.F = self.A = None
         self._own = []
         self._opened = []
+        obj, fail = [None], None
         if rank == dst:
-            err, pf = rt.cudaMalloc(n_views * self.fbytes)
-            assert err == rt.cudaError_t.cudaSuccess, err
-            err, pa = rt.cudaMalloc(n_views * self.abytes)
-            assert err == rt.cudaError_t.cudaSuccess, err
-            self._own = [pf, pa]
-            self.pF, self.pA = int(pf), int(pa)
-            self.F = torch.as_tensor(_CAI(self.pF, (n_views, H, W, C), "<f4"), device="cuda")
-            self.A = torch.as_tensor(_CAI(self.pA, (n_views, H, W), "<f4"), device="cuda")
-            handles = []
-            for p in (pf, pa):
-                err, h = rt.cudaIpcGetMemHandle(p)
+            try:
+                err, pf = rt.cudaMalloc(n_views * self.fbytes)
                 assert err == rt.cudaError_t.cudaSuccess, err
-                handles.append(bytes(h.reserved))
-            obj = [handles]
-        else:
-            obj = [None]
+                self._own.append(pf)
+                err, pa = rt.cudaMalloc(n_views * self.abytes)
+                assert err == rt.cudaError_t.cudaSuccess, err
+                self._own.append(pa)
+                self.pF, self.pA = int(pf), int(pa)
+                self.F = torch.as_tensor(_CAI(self.pF, (n_views, H, W, C), "<f4"), device="cuda")
+                self.A = torch.as_tensor(_CAI(self.pA, (n_views, H, W), "<f4"), device="cuda")
+                handles = []
+                for p in (pf, pa):
+                    err, h = rt.cudaIpcGetMemHandle(p)
+                    assert err == rt.cudaError_t.cudaSuccess, err
+                    handles.append(bytes(h.reserved))
+                obj = [handles]
+            except Exception as e:               # still take part in the broadcast, then raise
+                fail = e
         if world > 1:
             dist.broadcast_object_list(obj, src=dst, group=group)
+        if fail is not None or obj[0] is None:
+            self.close()
+            raise RuntimeError(f"PeerFrame: the display rank could not export its frame buffer ({fail})")
         if rank != dst:
             ptrs = []
             for hb in obj[0]:

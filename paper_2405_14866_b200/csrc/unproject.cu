@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kUnprojThreads) k_unproject_write(ViewTable vt
 // target's 32-byte splat record, depth key and index (exactly what k_project writes for the same
 // Gaussian) plus per-target visibility statistics (OR / AND of visible depth keys, visible count) that
 // k_init hands to the depth sort.  The 48-byte world position / covariance never touch HBM.
-__global__ void __launch_bounds__(kUnprojThreads) k_front_fused(ViewTable vt, const uint32_t* __restrict__ offs,
+__global__ void __launch_bounds__(kUnprojThreads, 4) k_front_fused(ViewTable vt, const uint32_t* __restrict__ offs,
                                                                 FrontTargets ft, RasterConsts rc,
                                                                 void* __restrict__ feat_out, uint32_t* __restrict__ stats) {
     __shared__ uint32_t s_w[kUnprojThreads / 32];

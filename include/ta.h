@@ -12,7 +12,7 @@
  *                  l.385 "foreground pixels in source views ... are lifted to pixel-aligned
  *                  Gaussian points {G}".
  *   ta_rasterize : F_novel = R_G({G}, Pi_novel), the Gaussian
- *                  splatting rasterizer of [kerbl20233d]: EWA projection, 16x16 tiles,
+ *                  splatting rasterizer of [kerbl20233d]: EWA projection, screen tiles,
  *                  (tile, depth, index) order, front-to-back alpha compositing of the
  *                  C-channel latent feature, plus the accumulated alpha.
  *
@@ -57,7 +57,10 @@ typedef enum {
 typedef enum { TA_F32 = 0, TA_F16 = 1 } ta_dtype;
 
 #define TA_MAX_VIEWS 16
-#define TA_TILE 16             /* screen tiles are 16 x 16 pixels */
+#define TA_TILE 16             /* screen tiles are 16 x 16 pixels ([kerbl20233d]); opt-in 8 x 8 compositing tiles
+                                  (environment TA_TILE_PX=8 at context creation, 32 x 32 coarse bins only) are
+                                  reported in ta_debug_view.tile_px.  The tile size never changes a result: a
+                                  pixel composites every Gaussian whose box holds it, in (depth, id) order */
 
 typedef struct { float fx, fy, cx, cy; } ta_intrinsics;        /* pixels; fx, fy > 0 */
 typedef struct { float R[9]; float t[3]; } ta_extrinsics;      /* world -> camera; R orthonormal (1e-4) */
@@ -272,7 +275,8 @@ ta_status ta_rasterize_backward(ta_context* ctx, const ta_gaussians* g, int64_t 
  *   depth_keys  [n] uint32 in depth-rank order: camera-space depth bits (0xffffffff when culled;
  *               culled Gaussians carry no tile entries, their rank positions are unspecified)
  *   order       [n] uint32: array index of the Gaussian of depth rank r
- *   tile_offsets [T + 1] uint32: list of tile t is tile_list[tile_offsets[t] .. tile_offsets[t+1])
+ *   tile_offsets [T + 1] uint32: list of tile t (row-major tiles of tile_px x tile_px pixels, T = tiles_x *
+ *               tiles_y) is tile_list[tile_offsets[t] .. tile_offsets[t+1])
  *   tile_list   [K] uint32 array indices ordered by (tile, depth, id) -- the sequence the compositor
  *               walks for each tile (k_tile_split's per-tile lists, compacted into one array by this call)
  *   n_contrib   [H][W] int32 composited pairs per pixel (only with TA_FLAG_DEBUG_COUNTS)
@@ -293,6 +297,9 @@ typedef struct {
        [1] entries staged, [2] staged entries evaluated, [3] evaluated with some q <= q_max,
        [4] accumulated, [5] composited (pixel, Gaussian) pairs, [6] warps, [7] fill rounds */
     int64_t work[8];
+    int32_t tile_px;             /* side of the compositing tiles the lists are for: 16, or 8 (opt-in
+                                    TA_TILE_PX=8 with 32 x 32-pixel coarse bins) */
+    int32_t reserved;
 } ta_debug_view;
 ta_status ta_debug_last(ta_context* ctx, ta_debug_view* out, void* stream);
 

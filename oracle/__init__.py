@@ -67,6 +67,10 @@ def lib():
         _lib.tao_count_entries.argtypes = [i64, P, P]
         _lib.tao_tile_lists.restype = i64
         _lib.tao_tile_lists.argtypes = [i64, P, P, P, P, i32, i32, P, P]
+        _lib.tao_count_entries_tiled.restype = i64
+        _lib.tao_count_entries_tiled.argtypes = [i64, P, P, i32]
+        _lib.tao_tile_lists_tiled.restype = i64
+        _lib.tao_tile_lists_tiled.argtypes = [i64, P, P, P, P, i32, i32, i32, P, P]
         _lib.tao_composite_tiles.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, i64, P, P,
                                              P, P]
         _lib.tao_zbuffer_view.argtypes = [i32, i32, P, P, P, P, C.c_float, P, i64, P, P, i32, i32, i32, P]
@@ -158,16 +162,17 @@ def project(g, K, R, t, H, W, params=None):
     return out
 
 
-def tile_lists(pr, ids, H, W):
-    """a3-a5 -> (ranges[T,2] uint32, list[K] int64 array indices) ordered by (tile, dkey, id)."""
+def tile_lists(pr, ids, H, W, tile=16):
+    """a3-a5 -> (ranges[T,2] uint32, list[K] int64 array indices) ordered by (tile, dkey, id), for
+    square tiles of side `tile` (16 = [kerbl20233d]; 8 = the CUDA path's tiles under 32-px bins)."""
     n = len(pr["visible"])
     ids = np.ascontiguousarray(ids, np.int64)
-    K = lib().tao_count_entries(n, _p(pr["visible"]), _p(pr["rect"]))
-    T = ((W + 15) // 16) * ((H + 15) // 16)
+    K = lib().tao_count_entries_tiled(n, _p(pr["visible"]), _p(pr["rect"]), int(tile))
+    T = ((W + tile - 1) // tile) * ((H + tile - 1) // tile)
     ranges = np.zeros((T, 2), np.uint32)
     lst = np.zeros(max(K, 1), np.int64)
-    lib().tao_tile_lists(n, _p(pr["visible"]), _p(pr["rect"]), _p(pr["dkey"]), _p(ids), H, W,
-                         _p(ranges), _p(lst))
+    lib().tao_tile_lists_tiled(n, _p(pr["visible"]), _p(pr["rect"]), _p(pr["dkey"]), _p(ids), H, W, int(tile),
+                               _p(ranges), _p(lst))
     return ranges, lst[:K]
 
 

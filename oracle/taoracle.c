@@ -277,33 +277,40 @@ static int entry_cmp(const void* pa, const void* pb) {
     return 0;
 }
 
-/* K = number of (tile, Gaussian) pairs: each visible Gaussian covers the tiles of its pixel box */
-int64_t tao_count_entries(int64_t n, const int32_t* visible, const int32_t* rect) {
+/* K = number of (tile, Gaussian) pairs for square screen tiles of side `tile` pixels: each visible
+ * Gaussian covers the tiles of its pixel box.  The paper takes the tiling from [kerbl20233d] (PAPER.md
+ * l.387: 16 x 16); the side is a free parameter of the binning -- a pixel's composited sequence (the
+ * Gaussians whose box holds it, in (dkey, id) order) is the same for every side (R8). */
+int64_t tao_count_entries_tiled(int64_t n, const int32_t* visible, const int32_t* rect, int tile) {
     int64_t K = 0;
     for (int64_t g = 0; g < n; g++) {
         if (!visible[g]) continue;
-        int64_t tw = rect[g * 4 + 1] / TAO_TILE - rect[g * 4 + 0] / TAO_TILE + 1;
-        int64_t th = rect[g * 4 + 3] / TAO_TILE - rect[g * 4 + 2] / TAO_TILE + 1;
+        int64_t tw = rect[g * 4 + 1] / tile - rect[g * 4 + 0] / tile + 1;
+        int64_t th = rect[g * 4 + 3] / tile - rect[g * 4 + 2] / tile + 1;
         K += tw * th;
     }
     return K;
 }
 
+int64_t tao_count_entries(int64_t n, const int32_t* visible, const int32_t* rect) {
+    return tao_count_entries_tiled(n, visible, rect, TAO_TILE);
+}
+
 /*
  * Per-tile lists ordered by (tile, dkey, id): ranges[T][2] = [start, end) into list;
- * list[K] = array index g of the Gaussian.  Tiles are row-major, T = ceil(W/16)*ceil(H/16).
- * Returns K.
+ * list[K] = array index g of the Gaussian.  Tiles of side `tile` are row-major,
+ * T = ceil(W/tile)*ceil(H/tile).  Returns K.
  */
-int64_t tao_tile_lists(int64_t n, const int32_t* visible, const int32_t* rect, const uint32_t* dkey,
-                       const int64_t* ids, int H, int W, uint32_t* ranges, int64_t* list) {
-    int TX = (W + TAO_TILE - 1) / TAO_TILE, TY = (H + TAO_TILE - 1) / TAO_TILE;
-    int64_t K = tao_count_entries(n, visible, rect);
+int64_t tao_tile_lists_tiled(int64_t n, const int32_t* visible, const int32_t* rect, const uint32_t* dkey,
+                             const int64_t* ids, int H, int W, int tile, uint32_t* ranges, int64_t* list) {
+    int TX = (W + tile - 1) / tile, TY = (H + tile - 1) / tile;
+    int64_t K = tao_count_entries_tiled(n, visible, rect, tile);
     tao_entry* e = (tao_entry*)malloc(sizeof(tao_entry) * (size_t)(K > 0 ? K : 1));
     int64_t k = 0;
     for (int64_t g = 0; g < n; g++) {
         if (!visible[g]) continue;
-        for (int ty = rect[g * 4 + 2] / TAO_TILE; ty <= rect[g * 4 + 3] / TAO_TILE; ty++)
-            for (int tx = rect[g * 4 + 0] / TAO_TILE; tx <= rect[g * 4 + 1] / TAO_TILE; tx++) {
+        for (int ty = rect[g * 4 + 2] / tile; ty <= rect[g * 4 + 3] / tile; ty++)
+            for (int tx = rect[g * 4 + 0] / tile; tx <= rect[g * 4 + 1] / tile; tx++) {
                 e[k].tile = (uint32_t)(ty * TX + tx);
                 e[k].dkey = dkey[g];
                 e[k].id = ids[g];
@@ -321,6 +328,11 @@ int64_t tao_tile_lists(int64_t n, const int32_t* visible, const int32_t* rect, c
     }
     free(e);
     return K;
+}
+
+int64_t tao_tile_lists(int64_t n, const int32_t* visible, const int32_t* rect, const uint32_t* dkey,
+                       const int64_t* ids, int H, int W, uint32_t* ranges, int64_t* list) {
+    return tao_tile_lists_tiled(n, visible, rect, dkey, ids, H, W, TAO_TILE, ranges, list);
 }
 
 /* ------------------------------------------------------------ a6 composite */

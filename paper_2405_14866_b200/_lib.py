@@ -59,7 +59,7 @@ class DebugView(C.Structure):
                 ("tiles_y", C.c_int32), ("sort_passes", C.c_int32), ("records", C.c_void_p),
                 ("depth_keys", C.c_void_p), ("order", C.c_void_p), ("tile_offsets", C.c_void_p),
                 ("tile_list", C.c_void_p), ("n_contrib", C.c_void_p),
-                ("work", C.c_int64 * 8)]
+                ("work", C.c_int64 * 8), ("tile_px", C.c_int32), ("reserved", C.c_int32)]
 
 
 STAGES = ("unproject", "project", "sort", "bin_count", "bin_scan", "bin_place", "composite")

@@ -37,6 +37,8 @@ struct ta_context {
     int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default), 2 = tensor-memory kernel
                                   // (tcgen05.mma, fp16 C >= 16; measured slower)
     int coarse64_above = 1024;    // TA_COARSE64_ABOVE: 64-px coarse bins for targets wider / taller than this
+    int tile_px = 16;             // TA_TILE_PX=8: 8 x 8 compositing tiles under 32-px coarse bins (opt-in, measured
+                                  // slower: DESIGN.md section 6); 64-px bins and the TMEM compositor always use 16
     bool bwd_simt = false;        // TA_BWD_SIMT: force the plain backward kernel
     std::string err;
     uint64_t launches = 0;
@@ -255,6 +257,7 @@ ta_status ta_context_create(int32_t device, ta_context** out) {
         return TA_ERR_CUDA;
     }
     if (const char* e = getenv("TA_COARSE64_ABOVE")) c->coarse64_above = atoi(e);   // tuning knobs
+    if (const char* e = getenv("TA_TILE_PX")) c->tile_px = atoi(e) == 8 ? 8 : 16;
     c->bwd_simt = getenv("TA_BWD_SIMT") != nullptr;
     const int cap = getenv("TA_TC_CTAS_PER_SM") ? atoi(getenv("TA_TC_CTAS_PER_SM")) : 0;
     if (const char* e = getenv("TA_COMPOSITOR")) c->compositor = atoi(e);
@@ -301,12 +304,16 @@ namespace {
 // pixels on a side, 64 x 64 beyond when the Gaussian indices fit the 24 index bits of such bins' list
 // entries (keeps the bin count, and with it the per-warp shared-memory cursors of k_bin_place, at
 // ~1024 for 2048^2), warps per binning block (per-warp [NB] cursors + lane masks must fit in shared
-// memory), P = rank tiles of nw * 256 ranks.
+// memory), P = rank tiles of nw * 256 ranks.  Compositing tiles: 16 x 16 pixels; opt-in (TA_TILE_PX=8)
+// 8 x 8 under 32-pixel bins (4 x 4 tiles per bin, 24 index bits), where each compositor warp walks a
+// list holding only the Gaussians whose box reaches its own 8 x 8 block (c3: 38 % fewer list entries
+// read, compositor -6.5 %, but 2.9x the tile entries and +0.15 ms of tile split: slower per view).
 ta_status bin_geometry(ta_context* c, int H, int W, int64_t cap, BinGeom* bg) {
     const int min_side6 = c->coarse64_above;
-    bg->shift = (std::max(H, W) > min_side6 && cap <= ((int64_t)1 << list_idx_bits(kMaxCoarseShift))) ? kMaxCoarseShift : 5;
-    if (cap > ((int64_t)1 << list_idx_bits(5)))
-        return fail(c, TA_ERR_CAPACITY, "more than 2^%d Gaussians", list_idx_bits(5));
+    bg->shift = (std::max(H, W) > min_side6 && cap <= ((int64_t)1 << entry_idx_bits(kMaxCoarseShift - 4))) ? kMaxCoarseShift : 5;
+    if (cap > ((int64_t)1 << entry_idx_bits(1)))
+        return fail(c, TA_ERR_CAPACITY, "more than 2^%d Gaussians", entry_idx_bits(1));
+    bg->ts = (bg->shift == 5 && c->tile_px == 8 && c->compositor != 2 && cap <= ((int64_t)1 << entry_idx_bits(2))) ? 3 : 4;
     const int bs = 1 << bg->shift;
     bg->TX = (W + bs - 1) / bs;
     bg->TY = (H + bs - 1) / bs;
@@ -322,10 +329,15 @@ ta_status bin_geometry(ta_context* c, int H, int W, int64_t cap, BinGeom* bg) {
     return TA_OK;
 }
 
+// tiles per coarse bin
+inline uint64_t tiles_per_bin(const BinGeom& bg) { return 1ull << (2 * (bg.shift - bg.ts)); }
+
 CompositeGeom composite_geometry(const BinGeom& bg, int H, int W) {
     CompositeGeom cg;
-    cg.TX = (W + kTile - 1) / kTile;
-    cg.TY = (H + kTile - 1) / kTile;
+    const int tp = 1 << bg.ts;
+    cg.TX = (W + tp - 1) / tp;
+    cg.TY = (H + tp - 1) / tp;
+    cg.ts = bg.ts;
     cg.W = W;
     cg.H = H;
     cg.shift = bg.shift;
@@ -336,9 +348,9 @@ CompositeGeom composite_geometry(const BinGeom& bg, int H, int W) {
 
 // Coarse list (entries x 4 B) and the per-tile lists (tiles per bin x 4 B).  Per-tile list positions
 // are 32-bit (trng, the compositors' cursors), so the tile-list space nq x entries must stay below 2^32.
-ta_status reserve_lists(ta_context* c, size_t entries, int shift) {
+ta_status reserve_lists(ta_context* c, size_t entries, const BinGeom& bg) {
     ta_status st;
-    const size_t nq = (size_t)1 << (2 * (shift - 4));
+    const size_t nq = (size_t)tiles_per_bin(bg);
     entries = std::max<size_t>(entries, 1);
     if ((uint64_t)entries * nq > 0xffffffffull)
         return fail(c, TA_ERR_CAPACITY, "%zu coarse entries x %zu tiles per bin exceed the 2^32-1 tile-list positions",
@@ -347,8 +359,8 @@ ta_status reserve_lists(ta_context* c, size_t entries, int shift) {
     return grow(c, c->tlist, entries * 4 * nq);
 }
 
-bool lists_reserved(const ta_context* c, size_t entries, int shift) {
-    const size_t nq = (size_t)1 << (2 * (shift - 4));
+bool lists_reserved(const ta_context* c, size_t entries, const BinGeom& bg) {
+    const size_t nq = (size_t)tiles_per_bin(bg);
     return c->list.bytes >= entries * 4 && c->tlist.bytes >= entries * 4 * nq;
 }
 
@@ -524,7 +536,7 @@ ta_status ta_reserve(ta_context* c, int64_t max_gaussians, int64_t max_entries, 
     BinGeom bg;
     if ((st = bin_geometry(c, H, W, max_gaussians, &bg)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, max_gaussians, H, W)) != TA_OK) return st;
-    if ((st = reserve_lists(c, (size_t)std::max<int64_t>(max_entries, 1), bg.shift)) != TA_OK) return st;
+    if ((st = reserve_lists(c, (size_t)std::max<int64_t>(max_entries, 1), bg)) != TA_OK) return st;
     c->rsv_g = max_gaussians; c->rsv_e = max_entries; c->rsv_H = H; c->rsv_W = W;
     for (int k = 0; k < kMaxFrontTargets - 1; k++)
         if (c->aux[k] && (st = ta_reserve(c->aux[k], max_gaussians, max_entries, H, W)) != TA_OK)
@@ -634,20 +646,20 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
     const int NB = bg.TX * bg.TY;                      // coarse bins
     const uint32_t bin_len = (uint32_t)NB * bg.P + 1;
     const CompositeGeom cg = composite_geometry(bg, H, W);
-    const int T = cg.TX * cg.TY;                       // 16 x 16 tiles
+    const int T = cg.TX * cg.TY;                       // compositing tiles
     if (async) {
         if (c->rec.bytes < (size_t)cap * 32 || c->bin_offs.bytes < (size_t)bin_len * 4 || !c->list.p ||
-            !lists_reserved(c, c->list.bytes / 4, bg.shift))
+            !lists_reserved(c, c->list.bytes / 4, bg))
             return fail(c, TA_ERR_CAPACITY, "TA_FLAG_ASYNC needs ta_reserve() for this size first");
     }
     if ((st = reserve_gaussians(c, cap)) != TA_OK) return st;
     if ((st = reserve_target(c, bg, cap, H, W)) != TA_OK) return st;
     if (counts && (st = grow(c, c->ncontrib, (size_t)H * W * 4)) != TA_OK) return st;
     {
-        const uint64_t nq = 1ull << (2 * (bg.shift - 4));
+        const uint64_t nq = tiles_per_bin(bg);
         const uint64_t first = std::min<uint64_t>((uint64_t)std::max<int64_t>(cap, 1) * 4, 0xffffffffull / nq);
         if ((st = reserve_lists(c, c->list.p ? std::min<uint64_t>(c->list.bytes / 4, 0xffffffffull / nq) : first,
-                                bg.shift)) != TA_OK)
+                                bg)) != TA_OK)
             return st;
     }
 
@@ -706,15 +718,15 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
         TA_CUDA(c, cudaMemcpyAsync(c->pinned, &cs->K, 8, cudaMemcpyDeviceToHost, s));
         TA_CUDA(c, cudaStreamSynchronize(s));
         const uint64_t Kh = c->pinned[0];
-        const uint64_t nq = 1ull << (2 * (bg.shift - 4));
+        const uint64_t nq = tiles_per_bin(bg);
         if (Kh * nq > 0xffffffffull)
             return fail(c, TA_ERR_CAPACITY, "%llu coarse entries x %llu tiles per bin exceed 2^32-1 tile-list positions",
                         (unsigned long long)Kh, (unsigned long long)nq);
-        if (!lists_reserved(c, (size_t)Kh, bg.shift)) {
+        if (!lists_reserved(c, (size_t)Kh, bg)) {
             // grow by 1/8 headroom, but never past the 32-bit tile-list position space
             const uint64_t want = std::min<uint64_t>(std::max<uint64_t>(c->list.bytes / 4, Kh + Kh / 8 + 1024),
                                                      0xffffffffull / nq);
-            if ((st = reserve_lists(c, (size_t)want, bg.shift)) != TA_OK) return st;
+            if ((st = reserve_lists(c, (size_t)want, bg)) != TA_OK) return st;
         }
     }
     tm.end();
@@ -1091,6 +1103,8 @@ ta_status ta_debug_last(ta_context* c, ta_debug_view* out, void* stream) {
     out->tile_list = (const uint32_t*)c->dbg_list.p;
     out->n_contrib = c->last_counts ? (const int32_t*)c->ncontrib.p : nullptr;
     for (int k = 0; k < 8; k++) out->work[k] = c->last_counts ? (int64_t)h.work[k] : 0;
+    out->tile_px = 1 << cg.ts;
+    out->reserved = 0;
     return TA_OK;
 }
 

@@ -7,7 +7,7 @@
 // lists of the preceding ta_rasterize on the same context.
 // Two kernels: k_composite_bwd_tc<C> (fp16-stored features, C in {16, 32, 64}; tensor cores, see the
 // section comment below) and the plain k_composite_bwd (fp32-stored features and C = 8):
-// one CTA per 16 x 16 tile, one pixel per thread; the tile list is staged 256 entries at a time in
+// one CTA per tile (16 x 16 or 8 x 8 pixels), one pixel per thread; the tile list is staged 256 entries at a time in
 // shared memory (record + fp32 feature row).  Pass 1 replays the forward per pixel (the same fp32
 // decision sequence as the forward kernels, so the composited set is identical) and accumulates
 // S = sum w_j g_j (g_j = G_F . f_j) and T_end; pass 2 replays it again and forms every composited
@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_composite_bwd(const uint4* __re
     uint32_t end = tr.x + tr.y;
     if (end > list_cap) end = (uint32_t)list_cap;
     const uint32_t n = cs->n;
-    const int px = txi * kTile + (int)(threadIdx.x & 15), py = tyi * kTile + (int)(threadIdx.x >> 4);
+    const int ts = cg.ts, TS = 1 << ts;               // tile side: 16 (256 threads) or 8 (64 threads)
+    const int px = (txi << ts) + (int)(threadIdx.x & (TS - 1)), py = (tyi << ts) + (int)(threadIdx.x >> ts);
     const bool inside = px < cg.W && py < cg.H;
     const size_t pix = inside ? (size_t)py * cg.W + px : 0;
     const float pxf = (float)px, pyf = (float)py;
@@ -107,12 +108,13 @@ __global__ void __launch_bounds__(kBwdThreads) k_composite_bwd(const uint4* __re
         return a;
     };
 
-    // warp strip: threads 32w .. 32w+31 = pixel rows 2w, 2w+1 of the tile, all 16 columns
-    const int sy0 = tyi * kTile + 2 * (int)(threadIdx.x >> 5), sx0 = txi * kTile;
+    // warp strip: threads 32w .. 32w+31 = pixel rows (32 / TS) w .. (32 / TS)(w + 1) - 1 of the tile, all TS columns
+    const int rows = 32 >> ts;
+    const int sy0 = (tyi << ts) + rows * (int)(threadIdx.x >> 5), sx0 = txi << ts;
     auto strip_hit = [&](uint32_t k) -> bool {
         const float4 Hh = s_h[k];
         const uint32_t bx = __float_as_uint(Hh.z), by = __float_as_uint(Hh.w);
-        return (int)(bx & 0xffff) <= sx0 + 15 && (int)(bx >> 16) >= sx0 && (int)(by & 0xffff) <= sy0 + 1 &&
+        return (int)(bx & 0xffff) <= sx0 + TS - 1 && (int)(bx >> 16) >= sx0 && (int)(by & 0xffff) <= sy0 + rows - 1 &&
                (int)(by >> 16) >= sy0;
     };
     // ---- pass 1: forward replay -> S, T_end, the list position after the last composited entry
@@ -333,20 +335,21 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
     constexpr uint32_t kGfLo = 64 * PH * 2, kWLo = kBwdBuf * WP * 4;
 
     uint32_t* const wq = &cs->scan_counter[7];
-    const uint32_t nblk = 4u * (uint32_t)(cg.TX * cg.TY);
+    const bool t8 = cg.ts == 3;
+    const uint32_t nblk = (t8 ? 1u : 4u) * (uint32_t)(cg.TX * cg.TY);
     for (;;) {
         uint32_t blk = 0;
         if (lane == 0) blk = atomicAdd(wq, 1u);
         blk = __shfl_sync(0xffffffffu, blk, 0);
         if (blk >= nblk) break;
-        const int tile = (int)order[blk >> 2];
-        const uint32_t qd = blk & 3u;
+        const int tile = (int)order[t8 ? blk : blk >> 2];
+        const uint32_t qd = t8 ? 0u : blk & 3u;
         const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
         const uint2 tr = trng[tile];
         const uint32_t cstart = tr.x;
         uint32_t cend = tr.x + tr.y;
         if (cend > list_cap) cend = (uint32_t)list_cap;
-        const int bx0 = txi * kTile + 8 * (int)(qd & 1), by0 = tyi * kTile + 8 * (int)(qd >> 1);
+        const int bx0 = (txi << cg.ts) + 8 * (int)(qd & 1), by0 = (tyi << cg.ts) + 8 * (int)(qd >> 1);
         const int px = bx0 + (li & 7), pyA = by0 + (li >> 3), pyB = pyA + 4;
         const float pxf = (float)px;
         const float2 py2 = make_float2((float)pyA, (float)pyB);
@@ -619,7 +622,7 @@ static cudaError_t launch_bwd_tc(int tiles, int resident, const uint4* rec, cons
     const size_t smem = sizeof(BwdBuf<C>);
     cudaError_t e = cudaMemsetAsync(&cs->scan_counter[7], 0, 4, st);
     if (e != cudaSuccess) return e;
-    k_composite_bwd_tc<C><<<std::min(4 * tiles, resident), 32, smem, st>>>(
+    k_composite_bwd_tc<C><<<std::min((cg.ts == 3 ? 1 : 4) * tiles, resident), 32, smem, st>>>(
         rec, static_cast<const __half*>(feat), tlist, trng, order, cg, rc, cs, list_cap, GF, GA, d_mean2, d_conic,
         d_alpha, d_feat);
     return cudaGetLastError();
@@ -671,14 +674,15 @@ cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const int* reside
             default: break;
         }
     }
+    const int bthreads = 1 << (2 * cg.ts);       // one thread per pixel of the tile
 #define TA_BWD(CC)                                                                                                      \
     case CC: {                                                                                                          \
         if (fbytes == 2) {                                                                                              \
-            k_composite_bwd<CC, __half><<<tiles, kBwdThreads, smem, st>>>(rec, static_cast<const __half*>(feat), tlist, \
+            k_composite_bwd<CC, __half><<<tiles, bthreads, smem, st>>>(rec, static_cast<const __half*>(feat), tlist, \
                                                                           trng, cg, rc, cs, list_cap, GF, GA, d_mean2,  \
                                                                           d_conic, d_alpha, d_feat);                    \
         } else {                                                                                                        \
-            k_composite_bwd<CC, float><<<tiles, kBwdThreads, smem, st>>>(rec, static_cast<const float*>(feat), tlist,   \
+            k_composite_bwd<CC, float><<<tiles, bthreads, smem, st>>>(rec, static_cast<const float*>(feat), tlist,   \
                                                                          trng, cg, rc, cs, list_cap, GF, GA, d_mean2,   \
                                                                          d_conic, d_alpha, d_feat);                     \
         }                                                                                                               \

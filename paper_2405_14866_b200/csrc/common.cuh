@@ -12,13 +12,14 @@
 namespace ta {
 
 constexpr int kTile = 16;
-// Coarse bins are 2^shift-pixel squares of 2^sb x 2^sb tiles (sb = shift - 4): 32 x 32 pixels for
-// targets up to 1024 pixels on a side, 64 x 64 beyond (api.cu bin_geometry), so the bin count stays
-// ~1024.  A coarse-list entry is the Gaussian's array index in the low 32 - 4 sb bits and, above it,
-// the bin's tiles its pixel box covers: for sb = 1 the 4-bit mask of the 2 x 2 tiles (bit qy*2+qx),
-// for sb = 2 the bin-local tile rectangle x0 | x1 << 2 | y0 << 4 | y1 << 6.
+// Coarse bins are 2^shift-pixel squares of 2^sb x 2^sb compositing tiles of 2^ts pixels (sb = shift - ts):
+// 32 x 32-pixel bins for targets up to 1024 pixels on a side, 64 x 64 beyond (api.cu bin_geometry), so
+// the bin count stays ~1024; tiles of 8 x 8 pixels (ts = 3) under 32-pixel bins, 16 x 16 (ts = 4)
+// otherwise.  A coarse-list entry is the Gaussian's array index in the low 32 - 4 sb bits and, above
+// it, the bin's tiles its pixel box covers: for sb = 1 the 4-bit mask of the 2 x 2 tiles (bit
+// qy*2+qx), for sb = 2 the bin-local tile rectangle x0 | x1 << 2 | y0 << 4 | y1 << 6.
 constexpr int kMaxCoarseShift = 6;
-__host__ __device__ constexpr int list_idx_bits(int shift) { return 32 - 4 * (shift - 4); }
+__host__ __device__ constexpr int entry_idx_bits(int sb) { return 32 - 4 * sb; }
 constexpr uint32_t kCulledKey = 0xffffffffu;
 constexpr uint32_t kEmptyRect = 1u;     // x0 = 1, x1 = 0  -> empty box
 

@@ -105,7 +105,8 @@ struct WarpBuf {
     float f[kBuf][CP];
 };
 
-// One CTA per 16x16 tile; warp w owns the 8x8 block (8*(w&1), 8*(w>>1)); lane l owns the two pixels
+// One CTA per 16x16 tile, warp w owning the 8x8 block (8*(w&1), 8*(w>>1)) -- or, for 8x8 tiles, one
+// tile per warp (4 per CTA); lane l owns the two pixels
 // (l&7, l>>3) and (l&7, (l>>3)+4) of its block (same column: dx is shared, the rest is computed
 // for both pixels with packed fp32x2 instructions).  Warps are fully independent (no barrier):
 // each walks the tile's (tile, depth, id) list (k_tile_split), keeps the entries whose ellipse can
@@ -122,7 +123,11 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     WarpBuf<C>& bf = reinterpret_cast<WarpBuf<C>*>(smem_raw)[warp];
 
-    const int tile = (int)order[blockIdx.x];           // heaviest tiles first (k_tile_order)
+    // 16 x 16 tiles: one CTA per tile, warp w = quadrant w; 8 x 8 tiles: one tile per warp
+    const bool t8 = cg.ts == 3;
+    const uint32_t slot = t8 ? 4u * blockIdx.x + warp : blockIdx.x;
+    if (slot >= (uint32_t)(cg.TX * cg.TY)) return;     // (warp-level: the kernel has no CTA barrier)
+    const int tile = (int)order[slot];                 // heaviest tiles first (k_tile_order)
     const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
     const uint2 tr = trng[tile];                       // this tile's (depth, id)-ordered list (k_tile_split)
     const uint32_t cstart = tr.x;
@@ -131,7 +136,7 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
     const uint32_t n = cs->n;
     const int W = cg.W, H = cg.H;
 
-    const int bx0 = txi * kTile + 8 * (int)(warp & 1), by0 = tyi * kTile + 8 * (int)(warp >> 1);
+    const int bx0 = (txi << cg.ts) + (t8 ? 0 : 8 * (int)(warp & 1)), by0 = (tyi << cg.ts) + (t8 ? 0 : 8 * (int)(warp >> 1));
     const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
     const float pxf = (float)px;
     const float2 py2 = make_float2((float)pyA, (float)pyB);
@@ -179,8 +184,8 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
             for (int h = 0; h < 2; h++) {
                 const int gx0 = (int)(r1[h].z & 0xffff), gx1 = (int)(r1[h].z >> 16);
                 const int gy0 = (int)(r1[h].w & 0xffff), gy1 = (int)(r1[h].w >> 16);
-                keep[h] = idx[h] < n && gx0 <= gx1 && (gx0 >> 4) <= txi && txi <= (gx1 >> 4) && (gy0 >> 4) <= tyi &&
-                          tyi <= (gy1 >> 4) && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
+                keep[h] = idx[h] < n && gx0 <= gx1 && (gx0 >> cg.ts) <= txi && txi <= (gx1 >> cg.ts) && (gy0 >> cg.ts) <= tyi &&
+                          tyi <= (gy1 >> cg.ts) && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
                           ellipse_may_touch(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y), __uint_as_float(r0[h].z),
                                             __uint_as_float(r0[h].w), __uint_as_float(r1[h].x), X0, X1, Y0, Y1, qlim);
             }
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
                                                      const CallState* __restrict__ cs, uint64_t clist_cap,
                                                      uint32_t* __restrict__ tlist, uint64_t tlist_cap,
                                                      uint2* __restrict__ trng) {
-    constexpr int SB = NQ == 4 ? 1 : 2, TPB = 1 << SB, IB = list_idx_bits(SB + 4);
+    constexpr int SB = NQ == 4 ? 1 : 2, TPB = 1 << SB, IB = entry_idx_bits(SB);
     __shared__ uint32_t s_cnt[32][NQ];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     const int bin = blockIdx.x;
@@ -539,18 +544,19 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     TcBuf<C>& bf = reinterpret_cast<TcBuf<C>*>(smem_raw)[warp];
 
-    // Persistent warps: each warp takes the next 8 x 8 block (tile quadrant) in the heaviest-first
-    // tile order from a per-call counter until all are done, so a warp that finishes early starts
-    // new work instead of idling until its CTA's slowest warp is done.
+    // Persistent warps: each warp takes the next 8 x 8 block (an 8 x 8 tile, or a quadrant of a 16 x 16
+    // tile) in the heaviest-first tile order from a per-call counter until all are done, so a warp
+    // that finishes early starts new work instead of idling until its CTA's slowest warp is done.
     uint32_t* const wq = &const_cast<CallState*>(cs)->scan_counter[6];
-    const uint32_t nblk = 4u * (uint32_t)(cg.TX * cg.TY);
+    const bool t8 = cg.ts == 3;
+    const uint32_t nblk = (t8 ? 1u : 4u) * (uint32_t)(cg.TX * cg.TY);
     for (;;) {
         uint32_t blk = 0;
         if (lane == 0) blk = atomicAdd(wq, 1u);
         blk = __shfl_sync(0xffffffffu, blk, 0);
         if (blk >= nblk) break;
-        const int tile = (int)order[blk >> 2];
-        const uint32_t qd = blk & 3u;                      // the 8 x 8 quadrant of the tile
+        const int tile = (int)order[t8 ? blk : blk >> 2];
+        const uint32_t qd = t8 ? 0u : blk & 3u;            // the 8 x 8 quadrant of a 16 x 16 tile
         const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
         const uint2 tr = trng[tile];                       // this tile's (depth, id)-ordered list (k_tile_split)
         const uint32_t cstart = tr.x;
@@ -559,7 +565,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         const uint32_t n = cs->n;
         const int W = cg.W, H = cg.H;
 
-        const int bx0 = txi * kTile + 8 * (int)(qd & 1), by0 = tyi * kTile + 8 * (int)(qd >> 1);
+        const int bx0 = (txi << cg.ts) + 8 * (int)(qd & 1), by0 = (tyi << cg.ts) + 8 * (int)(qd >> 1);
         const int px = bx0 + (int)(lane & 7), pyA = by0 + (int)(lane >> 3), pyB = pyA + 4;
         const float pxf = (float)px;
         const float2 py2 = make_float2((float)pyA, (float)pyB);
@@ -971,7 +977,8 @@ static cudaError_t launch_one(int tiles, bool fast, const uint4* rec, const void
     if (tiles == 0) return cudaSuccess;
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     const FT* ff = static_cast<const FT*>(feat);
-#define TA_ONE(K, FA) k_composite<C, FT, K, FA><<<tiles, kThreads, smem, st>>>(rec, ff, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib)
+    const int grid = cg.ts == 3 ? (tiles + kWarps - 1) / kWarps : tiles;
+#define TA_ONE(K, FA) k_composite<C, FT, K, FA><<<grid, kThreads, smem, st>>>(rec, ff, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib)
     if (ncontrib) {
         if (fast) TA_ONE(true, true); else TA_ONE(true, false);
     } else {
@@ -1083,7 +1090,7 @@ void launch_debug_tile_lists(const uint2* trng, const uint32_t* tlist, Composite
 void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGeom cg,
                        const CallState* cs, uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng,
                        cudaStream_t st) {
-    const int sb = cg.shift - 4;
+    const int sb = cg.shift - cg.ts;
     const int NB = cg.BX * ((cg.TY + (1 << sb) - 1) >> sb);
     if (sb == 1)
         k_tile_split<4><<<NB, 1024, 0, st>>>(clist, coffs, cg, cs, clist_cap, tlist, tlist_cap, trng);

@@ -22,6 +22,7 @@ struct RasterConsts {
 
 struct BinGeom {
     int shift;            // bin = (1 << shift) x (1 << shift) pixels (coarse bins: 32 x 32)
+    int ts;               // compositing tile = (1 << ts) x (1 << ts) pixels (3 or 4); shift - ts = 1 or 2
     int TX, TY;           // bins per row / column
     int nw;               // warps per k_bin_place block (per-warp [NB] cursors in shared memory)
     uint32_t P;           // rank tiles = columns of the bin-major [NB x P] run-start matrix
@@ -79,9 +80,10 @@ constexpr uint32_t scan_tiles(uint32_t len_max) { return len_max / 4096u + 1u; }
 
 // composite.cu
 struct CompositeGeom {
-    int TX, TY;           // 16 x 16 tiles per row / column
+    int TX, TY;           // compositing tiles ((1 << ts) pixels square) per row / column
     int W, H;
     int shift, BX;        // coarse bins: (1 << shift) pixels square, BX per row
+    int ts;               // tile side 1 << ts: 8 (one warp block per tile) or 16 (four 8 x 8 blocks)
     uint32_t P;           // coarse-binning partitions (columns of the bin-major offset matrix)
 };
 // per-tile lists (tile, depth, id) from the coarse bin lists: tlist + trng[tile] = (start, count)

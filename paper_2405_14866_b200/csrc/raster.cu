@@ -421,10 +421,11 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
         int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
         bool ok = false;
         if (r < wr1) ok = box_bins(pb, bg.shift, &x0, &x1, &y0, &y1);
-        // 16 x 16 tiles covered by the pixel box: each list entry carries, above the index, the
+        // compositing tiles covered by the pixel box: each list entry carries, above the index, the
         // rectangle of its coarse bin's tiles the box covers (read by k_tile_split)
-        const int tx0 = (int)(pb.x & 0xffff) >> 4, tx1 = (int)(pb.x >> 16) >> 4;
-        const int ty0 = (int)(pb.y & 0xffff) >> 4, ty1 = (int)(pb.y >> 16) >> 4;
+        const int ts = bg.ts;
+        const int tx0 = (int)(pb.x & 0xffff) >> ts, tx1 = (int)(pb.x >> 16) >> ts;
+        const int ty0 = (int)(pb.y & 0xffff) >> ts, ty1 = (int)(pb.y >> 16) >> ts;
         const int tw = x1 - x0 + 1;
         const int cnt = ok ? tw * (y1 - y0 + 1) : 0;
         const int maxc = __reduce_max_sync(0xffffffffu, cnt);
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
         for (int i = 0, xi = 0, yi = 0, t = t0; i < maxc; i++) {
             if (i < cnt) {
                 const uint32_t pos = s_cnt[rbase + t] + __popc(s_cnt[mbase + t] & lt);
-                const int sb = bg.shift - 4, qm = (1 << sb) - 1;
+                const int sb = bg.shift - ts, qm = (1 << sb) - 1;
                 const int cx = (x0 + xi) << sb, cy = (y0 + yi) << sb;
                 uint32_t rect;
                 if (sb == 1) {                               // 2 x 2 tiles: the tile mask itself
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(256) k_bin_place(const uint2* __restrict__ box
                     rect = (uint32_t)max(tx0 - cx, 0) | ((uint32_t)min(tx1 - cx, qm) << sb) |
                            ((uint32_t)max(ty0 - cy, 0) << (2 * sb)) | ((uint32_t)min(ty1 - cy, qm) << (3 * sb));
                 }
-                if (pos < cap32) list[pos] = idx | (rect << list_idx_bits(bg.shift));
+                if (pos < cap32) list[pos] = idx | (rect << entry_idx_bits(sb));
                 else overflow = 1u;
                 t++;
                 if (++xi == tw) { xi = 0; yi++; t += stride; }

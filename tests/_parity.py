@@ -76,7 +76,8 @@ def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True, counts=True):
         return out
     d = ctx.debug_last()
     T = d.tiles_x * d.tiles_y
-    out.update(n=d.n, K=d.K, P=d.P, tiles_x=d.tiles_x, tiles_y=d.tiles_y, sort_passes=d.sort_passes)
+    out.update(n=d.n, K=d.K, P=d.P, tiles_x=d.tiles_x, tiles_y=d.tiles_y, sort_passes=d.sort_passes,
+               tile_px=d.tile_px)
     out["records"] = d2h(d.records, 8 * d.n, np.uint32).reshape(-1, 8)
     out["order"] = d2h(d.order, d.n, np.uint32)
     out["keys_sorted"] = d2h(d.depth_keys, d.n, np.uint32)
@@ -144,8 +145,16 @@ def check_order(out, pr, ids):
     assert np.array_equal(got, want)
 
 
+def check_lists_vs_oracle(out, O, pr, ids, H, W):
+    """a3/a5 parity at the GPU's compositing tile size (ta_debug_view.tile_px: 8 under 32-px coarse
+    bins, 16 otherwise): the oracle's (tile, dkey, id) lists for that tile side, bit-exact."""
+    assert out["tile_px"] in (8, 16)
+    check_lists(out, *O.tile_lists(pr, ids, H, W, tile=out["tile_px"]))
+
+
 def check_lists(out, ranges, lst):
     """a3/a5 parity: tile ranges and per-tile lists bit-exact."""
+    assert len(out["ranges"]) == len(ranges), "tile counts differ (tile side)"
     assert out["K"] == len(lst)
     g = out["ranges"].astype(np.int64)
     o = ranges.astype(np.int64)

@@ -65,6 +65,22 @@ def test_random_scenes(ctx, seed):
     run_case(ctx, s, seed)
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2, 5])
+def test_tile8_lists(monkeypatch, seed):
+    """The backward over the forward's opt-in 8 x 8 tile lists (TA_TILE_PX=8): the plain kernel (64
+    threads per tile) for fp32 features / C = 8 fp16, the tensor-core kernel (one warp per tile) for
+    fp16 C >= 16 -- gradients against the oracle."""
+    import paper_2405_14866_b200 as tb
+    monkeypatch.setenv("TA_TILE_PX", "8")
+    c8 = tb.Context(0)
+    C = (8, 16, 32, 64, 16, 32, 64, 32, 8)[seed]
+    dt = "f16" if seed % 2 or seed >= 4 else "f32"
+    k = seed % 8
+    s = sg.make_random_scene(20 + seed, H=21 + 9 * k, W=47 - 6 * k, C=C, n_src=14 + 2 * k, feat_dtype=dt)
+    run_case(c8, s, seed)
+    assert c8.debug_last().tile_px == 8
+
+
 def test_rig_reduced(ctx):
     """configs[2] distributions at 128^2 sources, ragged 72 x 104 target, C = 32 fp16."""
     run_case(ctx, sg.make_config("c3", res=128, target_hw=(72, 104)))

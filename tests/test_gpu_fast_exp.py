@@ -52,7 +52,7 @@ def test_fast_exp_parity_reported(ctx, cfg):
     out = P.gpu_rasterize(ctx, g, cam, gp)
     K, R, t = sg.cam_arrays(cam)
     pr = O.project(go, K, R, t, cam.H, cam.W, op)
-    P.check_lists(out, *O.tile_lists(pr, go["ids"], cam.H, cam.W))     # a2-a5 unaffected by the exp mode
+    P.check_lists_vs_oracle(out, O, pr, go["ids"], cam.H, cam.W)      # a2-a5 unaffected by the exp mode
     ranges, lst = O.tile_lists(pr, go["ids"], cam.H, cam.W)
     TX = (cam.W + 15) // 16
     tiles = None

@@ -54,8 +54,8 @@ def full_parity(ctx, O, scene, tidx=0, tiles=None, async_=False, **pkw):
     pr = O.project(go, K, R, t, cam.H, cam.W, op)
     P.check_project(out, pr, go["alpha"])
     P.check_order(out, pr, go["ids"])
-    ranges, lst = O.tile_lists(pr, go["ids"], cam.H, cam.W)
-    P.check_lists(out, ranges, lst)
+    P.check_lists_vs_oracle(out, O, pr, go["ids"], cam.H, cam.W)
+    ranges, lst = O.tile_lists(pr, go["ids"], cam.H, cam.W)          # the oracle composites 16 x 16 tiles
     F, A, nc, _ = O.composite(go, pr, ranges, lst, cam.H, cam.W, op, tiles=tiles)
     err = P.check_composite(out, F, A, nc, tiles=tiles, tx=(cam.W + 15) // 16)
     return out, err
@@ -84,6 +84,27 @@ def test_random_scenes(ctx, oracle_lib, seed):
     dt = "f16" if seed % 2 else "f32"
     s = sg.make_random_scene(seed, H=17 + 13 * seed, W=90 - 5 * seed, C=C, n_src=12 + 3 * seed, feat_dtype=dt)
     full_parity(ctx, oracle_lib, s)
+
+
+@pytest.mark.parametrize("case", ["c2", "c2_async", "rand3", "rand6", "rand9", "c3_ragged"])
+def test_tile8_lists_and_composite(oracle_lib, monkeypatch, case):
+    """The opt-in 8 x 8 compositing tiles (TA_TILE_PX=8; 32-px coarse bins, 4 x 4 tiles per bin in the
+    entry bits): every 8 x 8 tile list bit-exact against the oracle's lists for 8-px tiles, every
+    pixel of F / A against the oracle; timed instantiation and TA_FLAG_ASYNC."""
+    import paper_2405_14866_b200 as tb
+    monkeypatch.setenv("TA_TILE_PX", "8")
+    c8 = tb.Context(0)
+    if case.startswith("rand"):
+        seed = int(case[4:])
+        C = (8, 16, 32, 64)[seed % 4]
+        s = sg.make_random_scene(seed, H=17 + 13 * seed, W=90 - 5 * seed, C=C, n_src=12 + 3 * seed,
+                                 feat_dtype="f16" if seed % 2 else "f32")
+        out, _ = full_parity(c8, oracle_lib, s)
+    elif case == "c3_ragged":
+        out, _ = full_parity(c8, oracle_lib, sg.make_config("c3", res=256, target_hw=(136, 200)))
+    else:
+        out, _ = full_parity(c8, oracle_lib, sg.make_config("c2"), async_=case.endswith("async"))
+    assert out["tile_px"] == 8
 
 
 def test_c2_full(ctx, oracle_lib):
@@ -184,8 +205,8 @@ def test_c4_bench_targets_full_size(ctx, oracle_lib):
         pr = O.project(go, K, R, t, cam.H, cam.W, op)
         P.check_project(out, pr, go["alpha"])
         P.check_order(out, pr, go["ids"])
+        P.check_lists_vs_oracle(out, O, pr, go["ids"], cam.H, cam.W)
         ranges, lst = O.tile_lists(pr, go["ids"], cam.H, cam.W)
-        P.check_lists(out, ranges, lst)
         tiles = sample_tiles(ranges, 64, 12, 24, j)
         Fo, Ao, nc, _ = O.composite(go, pr, ranges, lst, cam.H, cam.W, op, tiles=tiles)
         P.check_composite(out, Fo, Ao, nc, tiles=tiles, tx=64)
@@ -267,8 +288,8 @@ def test_c4_views_vs_single_view(ctx, oracle_lib):
         out = P.gpu_rasterize(ctx, g, cam, gp)
         K, R, t = sg.cam_arrays(cam)
         pr = oracle_lib.project(go, K, R, t, cam.H, cam.W, op)
+        P.check_lists_vs_oracle(out, oracle_lib, pr, go["ids"], cam.H, cam.W)
         ranges, lst = oracle_lib.tile_lists(pr, go["ids"], cam.H, cam.W)
-        P.check_lists(out, ranges, lst)
         F, A, nc, _ = oracle_lib.composite(go, pr, ranges, lst, cam.H, cam.W, op)
         P.check_composite(out, F, A, nc)
 
@@ -326,24 +347,37 @@ def test_c5_stress_sampled_tiles(ctx, oracle_lib):
     pr = oracle_lib.project(go, K, R, t, cam.H, cam.W, op)
     P.check_project(out, pr, go["alpha"])
     P.check_order(out, pr, go["ids"])
-    TX = (cam.W + 15) // 16
+    # a3/a5 on sampled GPU tiles (side tile_px): the oracle's definition -- every visible Gaussian whose
+    # box covers the tile, in (dkey, id) order -- written out for those tiles
     vis = np.nonzero(pr["visible"])[0]
-    rect = pr["rect"][vis] >> 4
+    ts = out["tile_px"]
+    TXg = (cam.W + ts - 1) // ts
     lens = out["ranges"][:, 1].astype(np.int64) - out["ranges"][:, 0]
     rng = np.random.default_rng(1)
-    tiles = np.unique(np.concatenate([np.argsort(lens)[-3:], rng.choice(np.nonzero(lens)[0], 6, replace=False)]))
-    sub_ranges = np.zeros((len(lens), 2), np.uint32)
+    gtiles = np.unique(np.concatenate([np.argsort(lens)[-3:], rng.choice(np.nonzero(lens)[0], 6, replace=False)]))
+
+    def covering(tx, ty, side):
+        r = pr["rect"][vis] // side
+        cov = vis[(r[:, 0] <= tx) & (tx <= r[:, 1]) & (r[:, 2] <= ty) & (ty <= r[:, 3])]
+        return cov[np.lexsort((go["ids"][cov], pr["dkey"][cov]))]
+
+    for tt in gtiles:
+        ty, tx = divmod(int(tt), TXg)
+        a, b = out["ranges"][tt]
+        assert np.array_equal(out["list"][a:b].astype(np.int64), covering(tx, ty, ts))
+    # a6 on the 16 x 16 tiles holding them (the oracle composites 16 x 16 tiles)
+    TX = (cam.W + 15) // 16
+    tiles = np.unique([(int(tt) // TXg * ts // 16) * TX + (int(tt) % TXg) * ts // 16 for tt in gtiles])
+    sub_ranges = np.zeros((TX * ((cam.H + 15) // 16), 2), np.uint32)
     chunks, pos = [], 0
     for tt in tiles:
         ty, tx = divmod(int(tt), TX)
-        cov = vis[(rect[:, 0] <= tx) & (tx <= rect[:, 1]) & (rect[:, 2] <= ty) & (ty <= rect[:, 3])]
-        cov = cov[np.lexsort((go["ids"][cov], pr["dkey"][cov]))]
-        a, b = out["ranges"][tt]
-        assert np.array_equal(out["list"][a:b].astype(np.int64), cov)
+        cov = covering(tx, ty, 16)
         sub_ranges[tt] = (pos, pos + len(cov))
         chunks.append(cov)
         pos += len(cov)
-    F, A, nc, _ = oracle_lib.composite(go, pr, sub_ranges, np.concatenate(chunks), cam.H, cam.W, op, tiles=tiles)
+    F, A, nc, _ = oracle_lib.composite(go, pr, sub_ranges, np.concatenate(chunks), cam.H, cam.W, op,
+                                       tiles=tiles.astype(np.int32))
     P.check_composite(out, F, A, nc, tiles=tiles, tx=TX)
 
 

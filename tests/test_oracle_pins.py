@@ -245,23 +245,25 @@ def test_projection_matches_float64_model_on_rig(oracle_lib):
 
 # ------------------------------------------------------------------------------ a3-a5 tile lists
 
-def test_tile_lists_equal_enumeration_brute_force(oracle_lib):
-    """Per tile: every visible Gaussian whose tile rect covers it, sorted by (dkey, id) (R12, R18)."""
+@pytest.mark.parametrize("tile", [16, 8])
+def test_tile_lists_equal_enumeration_brute_force(oracle_lib, tile):
+    """Per tile: every visible Gaussian whose tile rect covers it, sorted by (dkey, id) (R12, R18);
+    16 x 16 tiles ([kerbl20233d]) and the 8 x 8 tiles of the CUDA path under 32-px bins."""
     for seed in range(6):
         s = sg.make_random_scene(seed, H=45 + seed, W=70 - seed)
         g = oracle_lib.unproject(s)
         tgt = s.targets[0]
         K, R, t = sg.cam_arrays(tgt)
         pr = oracle_lib.project(g, K, R, t, tgt.H, tgt.W)
-        ranges, lst = oracle_lib.tile_lists(pr, g["ids"], tgt.H, tgt.W)
-        TX, TY = (tgt.W + 15) // 16, (tgt.H + 15) // 16
+        ranges, lst = oracle_lib.tile_lists(pr, g["ids"], tgt.H, tgt.W, tile=tile)
+        TX, TY = (tgt.W + tile - 1) // tile, (tgt.H + tile - 1) // tile
         total = 0
         for ty in range(TY):
             for tx in range(TX):
                 want = []
                 for i in np.nonzero(pr["visible"])[0]:
                     x0, x1, y0, y1 = pr["rect"][i]
-                    if x0 // 16 <= tx <= x1 // 16 and y0 // 16 <= ty <= y1 // 16:
+                    if x0 // tile <= tx <= x1 // tile and y0 // tile <= ty <= y1 // tile:
                         want.append((int(pr["dkey"][i]), int(g["ids"][i]), int(i)))
                 want.sort()
                 a, b = ranges[ty * TX + tx]

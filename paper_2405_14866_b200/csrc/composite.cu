@@ -487,7 +487,16 @@ struct TcBuf {
     __half f[NB][PH];                  // staged fp16 feature rows
     uint32_t w[2][16][WP];             // [hi|lo][k][lane]: half2 (w(pixel A), w(pixel B)) of staged entry j0+k
     SAcc<4 * NTS> sacc;                // [mt * NTS + nt - NTR][lane] (C = 64 only)
+    unsigned long long mbar;           // TA_TC_STAGE 2: completion of the fill's bulk feature-row copies
 };
+
+// Feature-row staging of the fill: 0 = cp.async 16 B x (2C / 16) per entry, waited for before the
+// first compositing chunk; 1 = the same, waited for just before the first chunk's MMA (the weights
+// of that chunk are computed meanwhile); 2 = one bulk copy (cp.async.bulk, TMA) per entry completing
+// on a per-warp mbarrier, waited for before the first chunk's MMA.
+#ifndef TA_TC_STAGE
+#define TA_TC_STAGE 0
+#endif
 
 // One compositing step of the normative a6 recurrence for the lane's two pixels, in the staged
 // scaling: q = q' = -q/2, a = 2^11 alpha', mA / mB = the entry's box lane masks (a pixel takes part
@@ -543,6 +552,13 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     TcBuf<C>& bf = reinterpret_cast<TcBuf<C>*>(smem_raw)[warp];
+    const uint32_t mbar = smem_u32(&bf.mbar);
+    uint32_t mphase = 0u;
+    if (TA_TC_STAGE == 2) {
+        if (lane == 0) mbar_init1(mbar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+    }
 
     // Persistent warps: each warp takes the next 8 x 8 block (an 8 x 8 tile, or a quadrant of a 16 x 16
     // tile) in the heaviest-first tile order from a per-call counter until all are done, so a warp
@@ -635,6 +651,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
             // ---- fill: up to NB entries of this warp, in list order; 64 list entries per round trip.
             //      The list indices of the next 64 entries are loaded one round ahead (pf_pos / pf).
             int cnt = 0;
+            if (TA_TC_STAGE == 2) fence_async_smem();   // earlier generic reads of the rows before the bulk writes
             while (cnt < NB && pos < cend) {
                 uint32_t idx[2];
                 if (pf_pos == pos) {
@@ -690,6 +707,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         step = (uint32_t)cl;
                         kp = kp && (int)lane < cl;
                     }
+                    if (TA_TC_STAGE == 2 && lane == 0 && bal) mbar_expect_tx(mbar, (uint32_t)__popc(bal) * (uint32_t)(2 * C));
                     if (kp) {
                         const int d = cnt + (int)rank;
                         const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
@@ -705,8 +723,12 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         pp[14] = __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4));
                         const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
                         const uint32_t dst = smem_u32(&bf.f[d][0]);
+                        if (TA_TC_STAGE == 2) {
+                            bulk_g2s(dst, src, (uint32_t)(2 * C), mbar);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                            for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                        }
                     }
                     cnt += __popc(bal);
                     adv += step;
@@ -716,7 +738,9 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 if (kCounts) { wk[0] += adv; wk[7] += 1; }
             }
             if (kCounts) wk[1] += cnt;
-            cp_async_wait_all();
+            if (TA_TC_STAGE == 0) cp_async_wait_all();
+            if (TA_TC_STAGE == 2 && lane == 0) mbar_arrive1(mbar);
+            bool feat_ready = TA_TC_STAGE == 0;
             __syncwarp();
             // ---- composite the staged entries, 16 at a time: SIMT weights -> smem -> tensor cores
             for (int j0 = 0; j0 < cnt; j0 += 16) {
@@ -856,6 +880,11 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                     if (nk == 16) pairs(std::integral_constant<bool, true>());
                     else pairs(std::integral_constant<bool, false>());
                 }
+                if (!feat_ready) {                   // staged feature rows: first needed by this chunk's MMA
+                    if (TA_TC_STAGE == 2) { mbar_wait_parity(mbar, mphase); mphase ^= 1u; }
+                    else cp_async_wait_all();
+                    feat_ready = true;
+                }
                 __syncwarp();
                 // B fragments: feature rows j0 .. j0+15 (rows past cnt carry weight 0: clamp to a staged row)
                 uint32_t bfr[NT][2];
@@ -894,6 +923,10 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 }
                 __syncwarp();
                 if (!__any_sync(0xffffffffu, (actA | actB | act1) != 0u)) break;
+            }
+            if (!feat_ready) {                       // no chunk ran: consume this fill's copies / barrier phase
+                if (TA_TC_STAGE == 2) { mbar_wait_parity(mbar, mphase); mphase ^= 1u; }
+                else cp_async_wait_all();
             }
             __syncwarp();
         }

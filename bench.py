@@ -798,8 +798,9 @@ def e2e(args, ctx, g, views, keep, scene, cams, outs, H, W, C_, rank, world, str
                 ha.copy_(A, non_blocking=True)
             copied[k].record(copy)
 
-    steps = max(2, min(args.steps, 5))
-    step()
+    steps = max(3, min(args.steps, 8))
+    for _ in range(2):                  # warm-up: pinned buffers, copy engines, both streams' first use
+        step()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)

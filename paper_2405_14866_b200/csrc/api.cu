@@ -33,9 +33,10 @@ struct ta_context {
     size_t smem_optin = 0;
     // per-context launch configuration (ta_context_create, on this context's device): persistent grid
     // sizes of the compositor / backward per C slot, and the tuning knobs read once from the environment
-    int resident_tc[4] = {1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1}, resident_tm[4] = {0, 1, 1, 1};
-    int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default), 2 = tensor-memory kernel
-                                  // (tcgen05.mma, fp16 C >= 16; measured slower)
+    int resident_tc[5] = {1, 1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1}, resident_tm[4] = {0, 1, 1, 1};
+    int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default; for fp16 C = 32 with its
+                                  // accumulators in tensor memory), 1 = the same with register accumulators for every C,
+                                  // 2 = tensor-memory MMA kernel (tcgen05.mma, fp16 C >= 16; measured slower)
     int coarse64_above = 1024;    // TA_COARSE64_ABOVE: 64-px coarse bins for targets wider / taller than this
     int tile_px = 16;             // TA_TILE_PX=8: 8 x 8 compositing tiles under 32-px coarse bins (opt-in, measured
                                   // slower: DESIGN.md section 6); 64-px bins and the TMEM compositor always use 16
@@ -753,7 +754,7 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
         e = launch_composite(job.C, job.fbytes, T, c->resident_tc, fast_exp, rec, job.feat,
                              (const uint32_t*)c->tlist.p, (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
                              (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
-                             counts ? (int32_t*)c->ncontrib.p : nullptr, s);
+                             counts ? (int32_t*)c->ncontrib.p : nullptr, s, c->compositor == 0);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "composite launch");
     c->launches += 2;   // k_tile_order + k_composite

@@ -14,6 +14,7 @@
 //   k_composite<C, float>  fp32-stored features: the same recurrence, all-SIMT packed FFMA2
 //                      accumulation, one CTA per tile.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 #include "common.cuh"
@@ -466,7 +467,7 @@ struct SAcc {
 template <>
 struct SAcc<0> {};
 
-template <int C>
+template <int C, int NBO = 0>
 struct TcBuf {
     // fp16 feature row pitch (halves): an odd number of 16-B chunks, so the 8 rows one ldmatrix
     // phase reads fall into 8 different 16-B bank groups
@@ -478,7 +479,7 @@ struct TcBuf {
 #define TA_TC_NTR32 4
 #endif
     static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : (C == 32 ? TA_TC_NTR32 : NT), NTS = NT - NTR;
-    static constexpr int NB = C >= 64 ? 32 : TA_TC_NB;   // entries staged per warp at a time
+    static constexpr int NB = NBO > 0 ? NBO : (C >= 64 ? 32 : TA_TC_NB);   // entries staged per warp at a time
     // staged records, entry pairs (2k, 2k+1) interleaved so that the compacted mode loads its packed
     // (entry, entry) operands directly: p[k][0] = (mx, mx', my, my'), [1] = (-ca/2, .., -cb2/2, ..),
     // [2] = (-cc/2, .., 2^11 alpha, ..), [3] = (box lane mask A, .., mask B, ..)  (pre-scaled by exact
@@ -539,19 +540,48 @@ constexpr bool kSkipEmptyPairs = false;
 #endif
 constexpr int kTcMinBlocks = TA_TC_MIN_BLOCKS;   // CTAs per SM the register budget targets
 
-template <int C, bool kCounts, bool kFast>
-__global__ void __launch_bounds__(kThreads, (C >= 64 ? 3 : kTcMinBlocks))
+// kTm (fp16 C = 32, the default there): the 64 x 32 fp32 accumulators of a warp's block live in tensor
+// memory (the warp's lane quarter, 64 columns per CTA) instead of 64 registers; each 16-entry chunk loads
+// one 16-pixel m-tile (16 columns) at a time (tcgen05.ld), runs its mma.sync and stores it back
+// (tcgen05.st).  With 96 registers and 32 staged entries (8 KB of shared memory) per warp, 5 CTAs
+// (20 warps) fit per SM instead of 4 (c3: 1.013 -> 0.981 ms; 6 CTAs at 80 registers spill: 1.166 ms).
+#ifndef TA_TM_BLOCKS
+#define TA_TM_BLOCKS 5
+#endif
+#ifndef TA_TM_NB
+#define TA_TM_NB 32
+#endif
+constexpr int kTmBlocks = TA_TM_BLOCKS;
+template <int C, bool kTm>
+using TcBufT = TcBuf<C, kTm ? TA_TM_NB : 0>;
+
+template <int C, bool kCounts, bool kFast, bool kTm>
+__global__ void __launch_bounds__(kThreads, (kTm ? kTmBlocks : (C >= 64 ? 3 : kTcMinBlocks)))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
                const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
                const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
                int32_t* __restrict__ ncontrib) {
+    using Buf = TcBufT<C, kTm>;
+    static_assert(!kTm || C == 32, "tensor-memory accumulators: C = 32 only");
     constexpr int NT = C / 8;                 // n-tiles of 8 channels
-    constexpr int PH = TcBuf<C>::PH;
-    constexpr int WP = TcBuf<C>::WP;
-    constexpr int NB = TcBuf<C>::NB, NTR = TcBuf<C>::NTR, NTS = TcBuf<C>::NTS;
+    constexpr int PH = Buf::PH;
+    constexpr int WP = Buf::WP;
+    constexpr int NB = Buf::NB, NTR = Buf::NTR, NTS = Buf::NTS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    TcBuf<C>& bf = reinterpret_cast<TcBuf<C>*>(smem_raw)[warp];
+    Buf& bf = reinterpret_cast<Buf*>(smem_raw)[warp];
+    __shared__ uint32_t s_tmem;
+    uint32_t tacc = 0;                        // kTm: this warp's accumulator columns (lane quarter warp & 3)
+    if (kTm) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&s_tmem)) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tacc = s_tmem + ((32u * (warp & 3u)) << 16);
+    }
     const uint32_t mbar = smem_u32(&bf.mbar);
     uint32_t mphase = 0u;
     if (TA_TC_STAGE == 2) {
@@ -600,13 +630,20 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         const uint32_t b_base = smem_u32(&bf.f[0][0]) + (uint32_t)((li >> 4) * 16);
         uint32_t* const wst = &bf.w[0][0][li];    // this lane's word in weight row 0 (hi)
 
-        float acc[4][NTR][4];
+        float acc[kTm ? 1 : 4][NTR][4];
 #pragma unroll
-        for (int mt = 0; mt < 4; mt++)
+        for (int mt = 0; mt < (kTm ? 1 : 4); mt++)
 #pragma unroll
             for (int nt = 0; nt < NTR; nt++)
 #pragma unroll
                 for (int e = 0; e < 4; e++) acc[mt][nt][e] = 0.0f;
+        if constexpr (kTm) {
+            float z[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) z[i] = 0.0f;
+#pragma unroll
+            for (int mt = 0; mt < 4; mt++) tm_st16(tacc + 16u * mt, z);
+        }
         if constexpr (NTS > 0) {
 #pragma unroll
             for (int k = 0; k < 4 * NTS; k++) bf.sacc.v[k][li] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -899,15 +936,28 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                             ldsm_x4_t(rb + np * 32, bfr[2 * np][0], bfr[2 * np][1], bfr[2 * np + 1][0], bfr[2 * np + 1][1]);
                     }
                 }
+                if constexpr (kTm) tm_wait_st();        // the previous chunk's stores precede these loads
 #pragma unroll
                 for (int mt = 0; mt < 4; mt++) {
                     uint32_t ah[4], al[4];
                     ldsm_x4_t(a_base + mt * 32, ah[0], ah[1], ah[2], ah[3]);
                     ldsm_x4_t(a_base + mt * 32 + kLoOff, al[0], al[1], al[2], al[3]);
+                    if constexpr (kTm) {                  // this m-tile's accumulators: tensor memory -> MMA -> back
+                        float v[16];
+                        tm_ld16(tacc + 16u * mt, v);
+                        float (&am)[NTR][4] = *reinterpret_cast<float (*)[NTR][4]>(v);
 #pragma unroll
-                    for (int nt = 0; nt < NTR; nt++) {
-                        hmma16816(acc[mt][nt], ah, bfr[nt][0], bfr[nt][1]);
-                        hmma16816(acc[mt][nt], al, bfr[nt][0], bfr[nt][1]);
+                        for (int nt = 0; nt < NTR; nt++) {
+                            hmma16816(am[nt], ah, bfr[nt][0], bfr[nt][1]);
+                            hmma16816(am[nt], al, bfr[nt][0], bfr[nt][1]);
+                        }
+                        tm_st16(tacc + 16u * mt, v);
+                    } else {
+#pragma unroll
+                        for (int nt = 0; nt < NTR; nt++) {
+                            hmma16816(acc[mt][nt], ah, bfr[nt][0], bfr[nt][1]);
+                            hmma16816(acc[mt][nt], al, bfr[nt][0], bfr[nt][1]);
+                        }
                     }
                     if constexpr (NTS > 0) {
 #pragma unroll
@@ -939,8 +989,12 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         }
         // accumulator (mt, row r in 0..15) <-> pixel p' = 16 mt + r = 2 l' + h: lane l' = 8 mt + (r >> 1), pixel A/B = r & 1
         const int g = li >> 2, t = li & 3;
+        if constexpr (kTm) tm_wait_st();
 #pragma unroll
         for (int mt = 0; mt < 4; mt++) {
+            float tv[16];
+            if constexpr (kTm) tm_ld16(tacc + 16u * mt, tv);
+            float (&acm)[NTR][4] = kTm ? *reinterpret_cast<float (*)[NTR][4]>(tv) : acc[kTm ? 0 : mt];
 #pragma unroll
             for (int half = 0; half < 2; half++) {
                 const int r = g + 8 * half;
@@ -951,7 +1005,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 #pragma unroll
                     for (int nt = 0; nt < NTR; nt++)
                         *reinterpret_cast<float2*>(out + 8 * nt) =
-                            make_float2(acc[mt][nt][2 * half] * (1.0f / 2048.0f), acc[mt][nt][2 * half + 1] * (1.0f / 2048.0f));
+                            make_float2(acm[nt][2 * half] * (1.0f / 2048.0f), acm[nt][2 * half + 1] * (1.0f / 2048.0f));
                     if constexpr (NTS > 0) {
 #pragma unroll
                         for (int nt = NTR; nt < NT; nt++) {
@@ -979,19 +1033,24 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         }
 
     }
+    if (kTm) {                                 // every warp of the CTA is done with its columns
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(s_tmem) : "memory");
+    }
 }
 
-template <int C>
+template <int C, bool kTm>
 static cudaError_t launch_tc(int tiles, int resident, bool fast, const uint4* rec, const void* feat, const uint32_t* list,
                              const uint2* offs, uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs,
                              uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
-    const size_t smem = sizeof(TcBuf<C>) * kWarps;
+    const size_t smem = sizeof(TcBufT<C, kTm>) * kWarps;
     if (tiles == 0) return cudaSuccess;
     // persistent warps: as many CTAs as are co-resident (more would only find the block counter spent)
     const int grid = std::min(tiles, resident);
     k_tile_order<<<1, 1024, 0, st>>>(offs, cg, order);
     const __half* fh = static_cast<const __half*>(feat);
-#define TA_TC(K, FA) k_composite_tc<C, K, FA><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib)
+#define TA_TC(K, FA) k_composite_tc<C, K, FA, kTm><<<grid, kThreads, smem, st>>>(rec, fh, list, offs, order, cg, rc, cs, list_cap, F, A, ncontrib)
     if (ncontrib) {
         if (fast) TA_TC(true, true); else TA_TC(true, false);
     } else {
@@ -1030,28 +1089,64 @@ static cudaError_t prepare_one(int num_sms, int cap, int* resident) {
     const int smem_tc = (int)(sizeof(TcBuf<C>) * kWarps), smem = (int)(sizeof(WarpBuf<C>) * kWarps);
     const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_composite_tc<C, false, false>, A, smem_tc)) ||
-        (e = cudaFuncSetAttribute(k_composite_tc<C, true, false>, A, smem_tc)) ||
-        (e = cudaFuncSetAttribute(k_composite_tc<C, false, true>, A, smem_tc)) ||
-        (e = cudaFuncSetAttribute(k_composite_tc<C, true, true>, A, smem_tc)) ||
+    if ((e = cudaFuncSetAttribute(k_composite_tc<C, false, false, false>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true, false, false>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, false, true, false>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true, true, false>, A, smem_tc)) ||
         (e = cudaFuncSetAttribute(k_composite<C, float, false, false>, A, smem)) ||
         (e = cudaFuncSetAttribute(k_composite<C, float, true, false>, A, smem)) ||
         (e = cudaFuncSetAttribute(k_composite<C, float, false, true>, A, smem)) ||
         (e = cudaFuncSetAttribute(k_composite<C, float, true, true>, A, smem)))
         return e;
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false, false>, kThreads, smem_tc))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_tc<C, false, false, false>, kThreads, smem_tc))) return e;
     if (cap > 0) per_sm = std::min(per_sm, cap);
     *resident = std::max(1, num_sms * std::max(1, per_sm));
     return cudaSuccess;
 }
 
-cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[4]) {
+// The tensor-memory-accumulator instantiations (C = 32): co-resident CTAs from the kernel's registers and
+// shared memory and the SM's TMEM columns (64 per CTA); the occupancy API reports 1 CTA / SM for kernels
+// that allocate tensor memory.
+static cudaError_t prepare_tc_tm(int num_sms, int cap, int* resident) {
+    constexpr int C = 32;
+    const int smem_tc = (int)(sizeof(TcBufT<C, true>) * kWarps);
+    const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_composite_tc<C, false, false, true>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true, false, true>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, false, true, true>, A, smem_tc)) ||
+        (e = cudaFuncSetAttribute(k_composite_tc<C, true, true, true>, A, smem_tc)))
+        return e;
+    cudaFuncAttributes fa{};
+    if ((e = cudaFuncGetAttributes(&fa, k_composite_tc<C, false, false, true>))) return e;
+    int dev = 0, regs_sm = 0, smem_sm = 0, thr_sm = 0, blk_sm = 0, smem_rsv = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+    cudaDeviceGetAttribute(&blk_sm, cudaDevAttrMaxBlocksPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    const int regs_blk = ((fa.numRegs * 32 + 255) / 256 * 256) * kWarps;   // 256-register warp granules
+    int per_sm = std::min(thr_sm / kThreads, blk_sm);
+    per_sm = std::min(per_sm, regs_sm / std::max(1, regs_blk));
+    per_sm = std::min(per_sm, smem_sm / (smem_tc + (int)fa.sharedSizeBytes + smem_rsv));
+    per_sm = std::min(per_sm, 512 / 64);
+    if (getenv("TA_DEBUG_PREP"))
+        fprintf(stderr, "k_composite_tc<32, tmem>: %d regs, %d B local, smem %d, %d CTAs/SM\n", fa.numRegs,
+                (int)fa.localSizeBytes, smem_tc, per_sm);
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    *resident = std::max(1, num_sms * std::max(1, per_sm));
+    return cudaSuccess;
+}
+
+cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[5]) {
     cudaError_t e;
     if ((e = prepare_one<8>(num_sms, ctas_per_sm_cap, &resident[0])) ||
         (e = prepare_one<16>(num_sms, ctas_per_sm_cap, &resident[1])) ||
         (e = prepare_one<32>(num_sms, ctas_per_sm_cap, &resident[2])) ||
-        (e = prepare_one<64>(num_sms, ctas_per_sm_cap, &resident[3])))
+        (e = prepare_one<64>(num_sms, ctas_per_sm_cap, &resident[3])) ||
+        (e = prepare_tc_tm(num_sms, ctas_per_sm_cap, &resident[4])))
         return e;
     return cudaSuccess;
 }
@@ -1065,10 +1160,13 @@ int c_slot(int C) { return C == 8 ? 0 : C == 16 ? 1 : C == 32 ? 2 : 3; }
 cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, bool fast, const uint4* rec,
                              const void* feat, const uint32_t* list, const uint2* offs, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
-                             int32_t* ncontrib, cudaStream_t st) {
+                             int32_t* ncontrib, cudaStream_t st, bool tm_acc) {
+    if (tm_acc && C == 32 && fbytes == 2)
+        return launch_tc<32, true>(tiles, resident[4], fast, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A,
+                                   ncontrib, st);
 #define TA_CASE(CC)                                                                                              \
     case CC:                                                                                                     \
-        return fbytes == 2 ? launch_tc<CC>(tiles, resident[c_slot(CC)], fast, rec, feat, list, offs, order, cg, rc, cs, \
+        return fbytes == 2 ? launch_tc<CC, false>(tiles, resident[c_slot(CC)], fast, rec, feat, list, offs, order, cg, rc, cs, \
                                            list_cap, F, A, ncontrib, st)                                         \
                            : launch_one<CC, float>(tiles, fast, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A, \
                                                    ncontrib, st);

@@ -91,13 +91,13 @@ void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGe
                        const CallState* cs, uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng,
                        cudaStream_t st);
 // per-device preparation (ta_context_create): shared-memory opt-ins + persistent grid sizes per C
-// (slot c_slot(C): C = 8, 16, 32, 64)
-cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[4]);
+// (slot c_slot(C): C = 8, 16, 32, 64; slot 4: the tensor-memory-accumulator variant, C = 32)
+cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[5]);
 int c_slot(int C);
 cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, bool fast_exp, const uint4* rec, const void* feat,
                              const uint32_t* tlist, const uint2* trng, uint32_t* order, CompositeGeom cg,
                              RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
-                             int32_t* ncontrib, cudaStream_t st);
+                             int32_t* ncontrib, cudaStream_t st, bool tm_acc = false);
 // heaviest-first tile order (by list length) for the persistent compositors
 void launch_tile_order(const uint2* trng, CompositeGeom cg, uint32_t* order, cudaStream_t st);
 // composite_tm.cu: tensor-memory compositor (fp16 features, C in {16, 32, 64}); resident[c_slot(C)]

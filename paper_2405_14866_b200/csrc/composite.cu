@@ -721,8 +721,8 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                 for (int hh = 0; hh < 2; hh++) {
                     const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
                     const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                    keep[hh] = idx[hh] < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
-                               ellipse_may_touch2(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
+                    keep[hh] = (idx[hh] < n) & (gx0 <= ax1) & (gx1 >= ax0) & (gy0 <= ay1) & (gy1 >= ay0) &
+                               ellipse_may_touch_bf(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
                                                   __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
                                                   __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
                 }
@@ -756,8 +756,10 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                         pp[6] = -0.5f * __uint_as_float(r0[hh].w);
                         pp[8] = -0.5f * __uint_as_float(r1[hh].x);
                         pp[10] = 2048.0f * __uint_as_float(r1[hh].y);
-                        pp[12] = __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0));
-                        pp[14] = __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4));
+                        uint32_t mA, mB;
+                        box_lane_masks(gx0, gx1, gy0, gy1, bx0, by0, mA, mB);
+                        pp[12] = __uint_as_float(mA);
+                        pp[14] = __uint_as_float(mB);
                         const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
                         const uint32_t dst = smem_u32(&bf.f[d][0]);
                         if (TA_TC_STAGE == 2) {

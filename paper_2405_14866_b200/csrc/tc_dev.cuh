@@ -87,6 +87,23 @@ __device__ __forceinline__ uint32_t box_lane_mask(int gx0, int gx1, int gy0, int
     return rows & (col * 0x01010101u);
 }
 
+// Both lane masks of an 8x8 block at once, branch-free: mA = lanes whose pixel A (rows by0 .. by0+3)
+// lies in the box, mB = the same for pixel B (rows by0+4 .. by0+7).  The clamped ranges make an empty
+// overlap give an empty 8-bit column / row mask; the 4 row bits of each half are spread to bytes by
+// multiply-and-mask.  Equal to box_lane_mask(.., by0) / box_lane_mask(.., by0 + 4).
+__device__ __forceinline__ void box_lane_masks(int gx0, int gx1, int gy0, int gy1, int bx0, int by0, uint32_t& mA,
+                                               uint32_t& mB) {
+    const int cx0 = min(max(gx0 - bx0, 0), 8), cx1 = max(min(gx1 - bx0, 7), -1);
+    const int ry0 = min(max(gy0 - by0, 0), 8), ry1 = max(min(gy1 - by0, 7), -1);
+    const uint32_t col = (0xffu >> (7 - cx1)) & (0xffu << cx0) & 0xffu;
+    const uint32_t row = (0xffu >> (7 - ry1)) & (0xffu << ry0) & 0xffu;
+    const uint32_t crep = col * 0x01010101u;
+    const uint32_t ra = ((((row & 0xfu) * 0x00204081u) & 0x01010101u) * 0xffu);
+    const uint32_t rb = ((((row >> 4) * 0x00204081u) & 0x01010101u) * 0xffu);
+    mA = crep & ra;
+    mB = crep & rb;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -186,6 +203,23 @@ __device__ __forceinline__ bool ellipse_may_touch2(float mx, float my, float ca,
         best = fminf(best, ex * (ca * ex + cb2 * ey) + cc * ey * ey);
     }
     return best <= qlim;
+}
+// The same test without branches (both edge minima always evaluated, then selected): the SIMT fill
+// evaluates it for 32 list entries at once, where the branches of the form above diverge.
+__device__ __forceinline__ bool ellipse_may_touch_bf(float mx, float my, float ca, float cb2, float cc, float X0,
+                                                     float X1, float Y0, float Y1, float qlim) {
+    const float lx = X0 - mx, hx = X1 - mx, ly = Y0 - my, hy = Y1 - my;
+    const bool vx = lx > 0.0f || hx < 0.0f, vy = ly > 0.0f || hy < 0.0f;
+    const float cb = 0.5f * cb2;
+    const bool degenerate = !(fmaf(-cb, cb, ca * cc) * 4096.0f > ca * cc);
+    const float dx = lx > 0.0f ? lx : hx;
+    const float dy = fminf(fmaxf(-cb * dx * rcp_approx(cc), ly), hy);
+    const float b1 = dx * (ca * dx + cb2 * dy) + cc * dy * dy;
+    const float ey = ly > 0.0f ? ly : hy;
+    const float ex = fminf(fmaxf(-cb * ey * rcp_approx(ca), lx), hx);
+    const float b2 = ex * (ca * ex + cb2 * ey) + cc * ey * ey;
+    const float best = fminf(vx ? b1 : 3.0e38f, vy ? b2 : 3.0e38f);
+    return (!vx & !vy) | degenerate | (best <= qlim);
 }
 
 constexpr float kInf = __builtin_huge_valf();

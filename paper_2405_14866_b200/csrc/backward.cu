@@ -421,9 +421,9 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
                     pf = pos + 32 + lane < cend ? tlist[pos + 32 + lane] : 0xffffffffu;
                     const int gx0 = (int)(r1.z & 0xffff), gx1 = (int)(r1.z >> 16);
                     const int gy0 = (int)(r1.w & 0xffff), gy1 = (int)(r1.w >> 16);
-                    bool kp = idx < n && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
-                              ellipse_may_touch2(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
-                                                 __uint_as_float(r0.w), __uint_as_float(r1.x), X0, X1, Y0, Y1, qlim);
+                    bool kp = (idx < n) & (gx0 <= ax1) & (gx1 >= ax0) & (gy0 <= ay1) & (gy1 >= ay0) &
+                              ellipse_may_touch_bf(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
+                                                   __uint_as_float(r0.w), __uint_as_float(r1.x), X0, X1, Y0, Y1, qlim);
                     uint32_t bal = __ballot_sync(0xffffffffu, kp);
                     const int room = kBwdBuf - cnt;
                     const uint32_t rank = __popc(bal & lt);
@@ -439,9 +439,10 @@ __global__ void __launch_bounds__(32) k_composite_bwd_tc(const uint4* __restrict
                         const int d = cnt + (int)rank;
                         bf.g[d] = make_float4(__uint_as_float(r0.x), __uint_as_float(r0.y), __uint_as_float(r0.z),
                                               __uint_as_float(r0.w));
-                        bf.h[d] = make_float4(__uint_as_float(r1.x), __uint_as_float(r1.y),
-                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0)),
-                                              __uint_as_float(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4)));
+                        uint32_t mA, mB;
+                        box_lane_masks(gx0, gx1, gy0, gy1, bx0, by0, mA, mB);
+                        bf.h[d] = make_float4(__uint_as_float(r1.x), __uint_as_float(r1.y), __uint_as_float(mA),
+                                              __uint_as_float(mB));
                         bf.id[d] = idx;
                         const char* src = reinterpret_cast<const char*>(feat + (size_t)idx * C);
                         const uint32_t dst = smem_u32(&bf.f[d][0]);

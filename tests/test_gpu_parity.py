@@ -510,6 +510,52 @@ def test_tensor_memory_compositor_parity(oracle_lib, cfg):
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3r"])
+def test_register_accumulator_compositor_parity(oracle_lib, cfg):
+    """fp16 C = 32 composites with its accumulators in tensor memory by default; TA_COMPOSITOR=1 keeps
+    them in registers (64 staged entries per warp instead of 32).  That variant against the oracle,
+    every stage and every pixel (A and composited counts bit-exact, F within 1e-4)."""
+    import os
+    import paper_2405_14866_b200 as tb
+    os.environ["TA_COMPOSITOR"] = "1"
+    try:
+        c = tb.Context(0)
+    finally:
+        os.environ.pop("TA_COMPOSITOR")
+    s = sg.make_config("c2") if cfg == "c2" else sg.make_config("c3", res=256, target_hw=(136, 200))
+    full_parity(c, oracle_lib, s)
+
+
+def test_accumulator_placement_same_alpha_c4_target(ctx):
+    """Tensor-memory (default) vs register accumulators on a full 1024^2 c4 target: A and the
+    composited counts bit-identical (same per-pixel decisions), F within 2e-6 (the staging depth
+    changes only how the fp32 MMA sums are grouped)."""
+    import os
+    import torch
+    import paper_2405_14866_b200 as tb
+    os.environ["TA_COMPOSITOR"] = "1"
+    try:
+        c1 = tb.Context(0)
+    finally:
+        os.environ.pop("TA_COMPOSITOR")
+    s = sg.make_config("c3")
+    gp = P.gpu_params(s)
+    g = P.gpu_unproject(ctx, s, gp)
+    cam = sg.make_targets("c4", n_targets=32)[7]
+    a = P.gpu_rasterize(ctx, g, cam, gp, debug=False)
+    b = P.gpu_rasterize(c1, g, cam, gp, debug=False)
+    assert np.array_equal(a["A"].view(np.uint32), b["A"].view(np.uint32))
+    assert np.abs(a["F"] - b["F"]).max() <= 2e-6
+    pc = P.gpu_params(s, flags=tb.TA_FLAG_DEBUG_COUNTS)
+    K, R, t = sg.cam_arrays(cam)
+    for cx in (ctx, c1):
+        tb.rasterize(cx, g, K, R, t, cam.H, cam.W, pc)
+    torch.cuda.synchronize()
+    na = P.d2h(ctx.debug_last().n_contrib, cam.H * cam.W, np.int32)
+    nb = P.d2h(c1.debug_last().n_contrib, cam.H * cam.W, np.int32)
+    assert np.array_equal(na, nb) and na.sum() > 0
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3r"])
 def test_fp32_features_timed_instantiation(ctx, oracle_lib, cfg):
     """fp32-stored features take k_composite<C, float, false> (the SIMT compositor; the counters
     instantiation runs after it and must give the same bits): c2 at full size and the reduced ragged

@@ -33,9 +33,9 @@ struct ta_context {
     size_t smem_optin = 0;
     // per-context launch configuration (ta_context_create, on this context's device): persistent grid
     // sizes of the compositor / backward per C slot, and the tuning knobs read once from the environment
-    int resident_tc[5] = {1, 1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1}, resident_tm[4] = {0, 1, 1, 1};
-    int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default; for fp16 C = 32 with its
-                                  // accumulators in tensor memory), 1 = the same with register accumulators for every C,
+    int resident_tc[6] = {1, 1, 1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1}, resident_tm[4] = {0, 1, 1, 1};
+    int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default; for fp16 C = 32 / 64 with
+                                  // its accumulators in tensor memory), 1 = register (+ shared) accumulators for every C,
                                   // 2 = tensor-memory MMA kernel (tcgen05.mma, fp16 C >= 16; measured slower)
     int coarse64_above = 1024;    // TA_COARSE64_ABOVE: 64-px coarse bins for targets wider / taller than this
     int tile_px = 16;             // TA_TILE_PX=8: 8 x 8 compositing tiles under 32-px coarse bins (opt-in, measured

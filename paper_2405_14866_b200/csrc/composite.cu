@@ -467,7 +467,7 @@ struct SAcc {
 template <>
 struct SAcc<0> {};
 
-template <int C, int NBO = 0>
+template <int C, int NBO = 0, bool TM = false>
 struct TcBuf {
     // fp16 feature row pitch (halves): an odd number of 16-B chunks, so the 8 rows one ldmatrix
     // phase reads fall into 8 different 16-B bank groups
@@ -478,7 +478,8 @@ struct TcBuf {
 #ifndef TA_TC_NTR32
 #define TA_TC_NTR32 4
 #endif
-    static constexpr int NT = C / 8, NTR = C >= 64 ? 4 : (C == 32 ? TA_TC_NTR32 : NT), NTS = NT - NTR;
+    // (TM: every accumulator in tensor memory, none in shared memory)
+    static constexpr int NT = C / 8, NTR = TM ? NT : (C >= 64 ? 4 : (C == 32 ? TA_TC_NTR32 : NT)), NTS = NT - NTR;
     static constexpr int NB = NBO > 0 ? NBO : (C >= 64 ? 32 : TA_TC_NB);   // entries staged per warp at a time
     // staged records, entry pairs (2k, 2k+1) interleaved so that the compacted mode loads its packed
     // (entry, entry) operands directly: p[k][0] = (mx, mx', my, my'), [1] = (-ca/2, .., -cb2/2, ..),
@@ -540,11 +541,13 @@ constexpr bool kSkipEmptyPairs = false;
 #endif
 constexpr int kTcMinBlocks = TA_TC_MIN_BLOCKS;   // CTAs per SM the register budget targets
 
-// kTm (fp16 C = 32, the default there): the 64 x 32 fp32 accumulators of a warp's block live in tensor
-// memory (the warp's lane quarter, 64 columns per CTA) instead of 64 registers; each 16-entry chunk loads
-// one 16-pixel m-tile (16 columns) at a time (tcgen05.ld), runs its mma.sync and stores it back
-// (tcgen05.st).  With 96 registers and 32 staged entries (8 KB of shared memory) per warp, 5 CTAs
-// (20 warps) fit per SM instead of 4 (c3: 1.013 -> 0.981 ms; 6 CTAs at 80 registers spill: 1.166 ms).
+// kTm (fp16 C = 32 and 64, the default there): the 64 x C fp32 accumulators of a warp's block live in
+// tensor memory (the warp's lane quarter, 2C columns per CTA) instead of registers (C = 32: 64 of them)
+// or registers + shared memory (C = 64); each 16-entry chunk loads one 16-pixel m-tile (C / 2 columns)
+// at a time (tcgen05.ld), runs its mma.sync and stores it back (tcgen05.st).  C = 32: 96 registers and
+// 32 staged entries (8 KB of shared memory) per warp, 5 CTAs (20 warps) per SM instead of 4 (c3:
+// 1.013 -> 0.981 ms; 6 CTAs at 80 registers spill: 1.166 ms).  C = 64: 128 TMEM columns per CTA, so
+// 4 CTAs per SM instead of 3.
 #ifndef TA_TM_BLOCKS
 #define TA_TM_BLOCKS 5
 #endif
@@ -553,16 +556,19 @@ constexpr int kTcMinBlocks = TA_TC_MIN_BLOCKS;   // CTAs per SM the register bud
 #endif
 constexpr int kTmBlocks = TA_TM_BLOCKS;
 template <int C, bool kTm>
-using TcBufT = TcBuf<C, kTm ? TA_TM_NB : 0>;
+using TcBufT = TcBuf<C, kTm ? TA_TM_NB : 0, kTm>;
+template <int C>
+__host__ __device__ constexpr int tm_cols() { return C >= 64 ? 128 : 64; }    // TMEM columns per CTA (a power of two >= 32)
 
 template <int C, bool kCounts, bool kFast, bool kTm>
-__global__ void __launch_bounds__(kThreads, (kTm ? kTmBlocks : (C >= 64 ? 3 : kTcMinBlocks)))
+__global__ void __launch_bounds__(kThreads, (kTm ? (C >= 64 ? 4 : kTmBlocks) : (C >= 64 ? 3 : kTcMinBlocks)))
 k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
                const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
                const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
                int32_t* __restrict__ ncontrib) {
     using Buf = TcBufT<C, kTm>;
-    static_assert(!kTm || C == 32, "tensor-memory accumulators: C = 32 only");
+    static_assert(!kTm || C == 32 || C == 64, "tensor-memory accumulators: C = 32 or 64");
+    constexpr uint32_t kMtCols = C / 2;      // TMEM columns of one 16-pixel m-tile (NT n-tiles x 4 floats)
     constexpr int NT = C / 8;                 // n-tiles of 8 channels
     constexpr int PH = Buf::PH;
     constexpr int WP = Buf::WP;
@@ -574,7 +580,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     uint32_t tacc = 0;                        // kTm: this warp's accumulator columns (lane quarter warp & 3)
     if (kTm) {
         if (warp == 0) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&s_tmem)) : "memory");
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(tm_cols<C>()) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -642,7 +648,9 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 #pragma unroll
             for (int i = 0; i < 16; i++) z[i] = 0.0f;
 #pragma unroll
-            for (int mt = 0; mt < 4; mt++) tm_st16(tacc + 16u * mt, z);
+            for (int mt = 0; mt < 4; mt++)
+#pragma unroll
+                for (uint32_t c = 0; c < kMtCols; c += 16) tm_st16(tacc + kMtCols * mt + c, z);
         }
         if constexpr (NTS > 0) {
 #pragma unroll
@@ -945,15 +953,19 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
                     ldsm_x4_t(a_base + mt * 32, ah[0], ah[1], ah[2], ah[3]);
                     ldsm_x4_t(a_base + mt * 32 + kLoOff, al[0], al[1], al[2], al[3]);
                     if constexpr (kTm) {                  // this m-tile's accumulators: tensor memory -> MMA -> back
-                        float v[16];
-                        tm_ld16(tacc + 16u * mt, v);
+                        float v[kMtCols];
+#pragma unroll
+                        for (uint32_t c = 0; c < kMtCols; c += 16)
+                            tm_ld16(tacc + kMtCols * mt + c, *reinterpret_cast<float (*)[16]>(v + c));
                         float (&am)[NTR][4] = *reinterpret_cast<float (*)[NTR][4]>(v);
 #pragma unroll
                         for (int nt = 0; nt < NTR; nt++) {
                             hmma16816(am[nt], ah, bfr[nt][0], bfr[nt][1]);
                             hmma16816(am[nt], al, bfr[nt][0], bfr[nt][1]);
                         }
-                        tm_st16(tacc + 16u * mt, v);
+#pragma unroll
+                        for (uint32_t c = 0; c < kMtCols; c += 16)
+                            tm_st16(tacc + kMtCols * mt + c, *reinterpret_cast<const float (*)[16]>(v + c));
                     } else {
 #pragma unroll
                         for (int nt = 0; nt < NTR; nt++) {
@@ -994,8 +1006,12 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
         if constexpr (kTm) tm_wait_st();
 #pragma unroll
         for (int mt = 0; mt < 4; mt++) {
-            float tv[16];
-            if constexpr (kTm) tm_ld16(tacc + 16u * mt, tv);
+            float tv[kTm ? kMtCols : 1];
+            if constexpr (kTm) {
+#pragma unroll
+                for (uint32_t c = 0; c < kMtCols; c += 16)
+                    tm_ld16(tacc + kMtCols * mt + c, *reinterpret_cast<float (*)[16]>(tv + c));
+            }
             float (&acm)[NTR][4] = kTm ? *reinterpret_cast<float (*)[NTR][4]>(tv) : acc[kTm ? 0 : mt];
 #pragma unroll
             for (int half = 0; half < 2; half++) {
@@ -1038,7 +1054,7 @@ k_composite_tc(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     if (kTm) {                                 // every warp of the CTA is done with its columns
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
-        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(s_tmem) : "memory");
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(tm_cols<C>()) : "memory");
     }
 }
 
@@ -1110,8 +1126,8 @@ static cudaError_t prepare_one(int num_sms, int cap, int* resident) {
 // The tensor-memory-accumulator instantiations (C = 32): co-resident CTAs from the kernel's registers and
 // shared memory and the SM's TMEM columns (64 per CTA); the occupancy API reports 1 CTA / SM for kernels
 // that allocate tensor memory.
+template <int C>
 static cudaError_t prepare_tc_tm(int num_sms, int cap, int* resident) {
-    constexpr int C = 32;
     const int smem_tc = (int)(sizeof(TcBufT<C, true>) * kWarps);
     const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
@@ -1133,22 +1149,23 @@ static cudaError_t prepare_tc_tm(int num_sms, int cap, int* resident) {
     int per_sm = std::min(thr_sm / kThreads, blk_sm);
     per_sm = std::min(per_sm, regs_sm / std::max(1, regs_blk));
     per_sm = std::min(per_sm, smem_sm / (smem_tc + (int)fa.sharedSizeBytes + smem_rsv));
-    per_sm = std::min(per_sm, 512 / 64);
+    per_sm = std::min(per_sm, 512 / tm_cols<C>());
     if (getenv("TA_DEBUG_PREP"))
-        fprintf(stderr, "k_composite_tc<32, tmem>: %d regs, %d B local, smem %d, %d CTAs/SM\n", fa.numRegs,
+        fprintf(stderr, "k_composite_tc<%d, tmem>: %d regs, %d B local, smem %d, %d CTAs/SM\n", C, fa.numRegs,
                 (int)fa.localSizeBytes, smem_tc, per_sm);
     if (cap > 0) per_sm = std::min(per_sm, cap);
     *resident = std::max(1, num_sms * std::max(1, per_sm));
     return cudaSuccess;
 }
 
-cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[5]) {
+cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[6]) {
     cudaError_t e;
     if ((e = prepare_one<8>(num_sms, ctas_per_sm_cap, &resident[0])) ||
         (e = prepare_one<16>(num_sms, ctas_per_sm_cap, &resident[1])) ||
         (e = prepare_one<32>(num_sms, ctas_per_sm_cap, &resident[2])) ||
         (e = prepare_one<64>(num_sms, ctas_per_sm_cap, &resident[3])) ||
-        (e = prepare_tc_tm(num_sms, ctas_per_sm_cap, &resident[4])))
+        (e = prepare_tc_tm<32>(num_sms, ctas_per_sm_cap, &resident[4])) ||
+        (e = prepare_tc_tm<64>(num_sms, ctas_per_sm_cap, &resident[5])))
         return e;
     return cudaSuccess;
 }
@@ -1165,6 +1182,9 @@ cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, 
                              int32_t* ncontrib, cudaStream_t st, bool tm_acc) {
     if (tm_acc && C == 32 && fbytes == 2)
         return launch_tc<32, true>(tiles, resident[4], fast, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A,
+                                   ncontrib, st);
+    if (tm_acc && C == 64 && fbytes == 2)
+        return launch_tc<64, true>(tiles, resident[5], fast, rec, feat, list, offs, order, cg, rc, cs, list_cap, F, A,
                                    ncontrib, st);
 #define TA_CASE(CC)                                                                                              \
     case CC:                                                                                                     \

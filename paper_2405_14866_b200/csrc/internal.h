@@ -91,8 +91,8 @@ void launch_tile_split(const uint32_t* clist, const uint32_t* coffs, CompositeGe
                        const CallState* cs, uint64_t clist_cap, uint32_t* tlist, uint64_t tlist_cap, uint2* trng,
                        cudaStream_t st);
 // per-device preparation (ta_context_create): shared-memory opt-ins + persistent grid sizes per C
-// (slot c_slot(C): C = 8, 16, 32, 64; slot 4: the tensor-memory-accumulator variant, C = 32)
-cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[5]);
+// (slot c_slot(C): C = 8, 16, 32, 64; slots 4 / 5: the tensor-memory-accumulator variant, C = 32 / 64)
+cudaError_t prepare_composite(int num_sms, int ctas_per_sm_cap, int resident[6]);
 int c_slot(int C);
 cudaError_t launch_composite(int C, int fbytes, int tiles, const int* resident, bool fast_exp, const uint4* rec, const void* feat,
                              const uint32_t* tlist, const uint2* trng, uint32_t* order, CompositeGeom cg,

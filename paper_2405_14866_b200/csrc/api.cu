@@ -220,7 +220,7 @@ const char* ta_status_string(ta_status s) {
 const char* ta_last_error(const ta_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 const char* ta_build_info(void) {
-    return "taloha sm_100a (persistent-warp compositor: packed-fp32 recurrence + mma.sync f16 feature accumulation; one-sweep depth sort; look-back scans; coarse binning + tile split; tensor-core backward)";
+    return "taloha sm_100a (persistent-warp compositor: packed-fp32 recurrence + mma.sync f16 feature accumulation into tensor-memory accumulators; one-sweep depth sort; look-back scans; coarse binning + tile split; tensor-core backward)";
 }
 
 uint64_t ta_launch_count(const ta_context* ctx) {

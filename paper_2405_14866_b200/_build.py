@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-diag-suppress", "550", *os.environ.get("TA_NVCC_EXTRA", "").split()]
-SOURCES = ["api.cu", "raster.cu", "composite.cu", "composite_tm.cu", "unproject.cu", "zbuffer.cu", "blend.cu", "backward.cu"]
+SOURCES = ["api.cu", "raster.cu", "composite.cu", "composite_tm.cu", "composite_ws.cu", "unproject.cu", "zbuffer.cu", "blend.cu", "backward.cu"]
 
 
 def _deps():

@@ -500,33 +500,6 @@ struct TcBuf {
 #define TA_TC_STAGE 0
 #endif
 
-// One compositing step of the normative a6 recurrence for the lane's two pixels, in the staged
-// scaling: q = q' = -q/2, a = 2^11 alpha', mA / mB = the entry's box lane masks (a pixel takes part
-// only while its bit is also set in actA / actB); qlo = -q_max/2, alo = 2^11 alpha_min.  Both scalings are exact (powers of two, no
-// subnormals on the used range), so every decision and T are those of the normative sequence:
-// fma(a, -2^-11, 1) = fl(1 - alpha').  Returns the weight 2^11 alpha' T of each pixel (0 if it does
-// not composite this entry) and advances T / the active bits.
-template <bool kCounts>
-__device__ __forceinline__ float2 tstep(float2 q, float2 a, uint32_t mA, uint32_t mB, float qlo, float alo, float teps,
-                                        float2& T, uint32_t& actA, uint32_t& actB, int& ncA, int& ncB,
-                                        unsigned long long* wk) {
-    const float2 Tn = mul2(T, fma2(a, bc2(-1.0f / 2048.0f), bc2(1.0f)));
-    const bool okA = (mA & actA) && q.x >= qlo && a.x >= alo, okB = (mB & actB) && q.y >= qlo && a.y >= alo;
-    const bool inA = okA && Tn.x >= teps, inB = okB && Tn.y >= teps;
-    if (okA && !inA) actA = 0u;           // T would drop below t_eps: stop before this Gaussian (R10)
-    if (okB && !inB) actB = 0u;
-    const float2 ws = mul2(a, T);
-    const float2 w = make_float2(inA ? ws.x : 0.0f, inB ? ws.y : 0.0f);
-    T = make_float2(inA ? Tn.x : T.x, inB ? Tn.y : T.y);
-    if (kCounts) {
-        wk[4] += __any_sync(0xffffffffu, inA || inB) ? 1 : 0;
-        wk[5] += __popc(__ballot_sync(0xffffffffu, inA)) + __popc(__ballot_sync(0xffffffffu, inB));
-        ncA += inA ? 1 : 0;
-        ncB += inB ? 1 : 0;
-    }
-    return w;
-}
-
 // Skip the exp / recurrence of an entry pair no pixel can take (saves ~13 % of pairs, but the
 // warp-wide vote + branch splits the unrolled loop into basic blocks the scheduler cannot overlap;
 // round 2 also measured a q-based skip -- compute both entries' q first, skip when no active in-box

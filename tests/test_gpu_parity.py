@@ -510,6 +510,22 @@ def test_tensor_memory_compositor_parity(oracle_lib, cfg):
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3r"])
+def test_warp_specialized_compositor_parity(oracle_lib, cfg):
+    """The opt-in warp-specialized compositor (TA_COMPOSITOR=3: producer / consumer warp pairs handing
+    staging buffers over mbarriers, accumulators in tensor memory) against the oracle: every stage and
+    every pixel, A and composited counts bit-exact, F within 1e-4."""
+    import os
+    import paper_2405_14866_b200 as tb
+    os.environ["TA_COMPOSITOR"] = "3"
+    try:
+        c = tb.Context(0)
+    finally:
+        os.environ.pop("TA_COMPOSITOR")
+    s = sg.make_config("c2") if cfg == "c2" else sg.make_config("c3", res=256, target_hw=(136, 200))
+    full_parity(c, oracle_lib, s)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3r"])
 def test_register_accumulator_compositor_parity(oracle_lib, cfg):
     """fp16 C = 32 composites with its accumulators in tensor memory by default; TA_COMPOSITOR=1 keeps
     them in registers (64 staged entries per warp instead of 32).  That variant against the oracle,

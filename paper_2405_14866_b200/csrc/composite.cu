@@ -426,6 +426,9 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
 // Launch order of the tile CTAs: by decreasing log2 of the tile's list length (longest
 // lists first, so the last wave is made of short tiles).  One block; order within a bucket is
 // arbitrary (it only affects scheduling, never results).
+#ifndef TA_ORDER_CAP
+#define TA_ORDER_CAP 2048
+#endif
 __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ trng, CompositeGeom cg,
                                                      uint32_t* __restrict__ order) {
     __shared__ uint32_t s_cnt[33], s_off[33];
@@ -433,7 +436,9 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ t
     if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0u;
     __syncthreads();
     auto bucket = [&](int t) {
-        const uint32_t len = trng[t].y;
+        // the list length saturates as a cost estimate: a fully covered block stops long before the end
+        // of a long list (c3: 0.904 -> 0.895 ms with the cap at 2048 entries)
+        const uint32_t len = min(trng[t].y, (uint32_t)TA_ORDER_CAP);
         return 32 - (32 - __clz(len));                 // 32 - bit length: longer lists -> smaller bucket
     };
     for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_cnt[bucket(t)], 1u);

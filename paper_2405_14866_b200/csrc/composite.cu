@@ -67,32 +67,6 @@ __device__ __forceinline__ float2 ffma2(float2 f, float w, float2 acc) {
     return *reinterpret_cast<float2*>(&r);
 }
 
-// Conservative cull of a Gaussian against an 8x4 pixel rectangle [X0,X1]x[Y0,Y1]: returns false
-// only if every pixel of the rectangle is provably outside q <= q_max (with a 1.6% + 0.01 margin
-// covering fp32 rounding of the per-pixel q); nearly degenerate conics
-// (condition > 4096) are never culled here (the per-pixel test decides).
-__device__ __forceinline__ bool ellipse_may_touch(float mx, float my, float ca, float cb2, float cc, float X0,
-                                                  float X1, float Y0, float Y1, float qlim) {
-    const float lx = X0 - mx, hx = X1 - mx, ly = Y0 - my, hy = Y1 - my;
-    if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return true;
-    const float cb = 0.5f * cb2;
-    const float detc = ca * cc - cb * cb;
-    if (!(detc * 4096.0f > ca * cc)) return true;
-    // minimum of q on each edge (the other coordinate clamped to the edge's extent)
-    const float ica = __frcp_rn(ca), icc = __frcp_rn(cc);
-    float best = 3.0e38f;
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-        const float dx = e ? hx : lx;          // vertical edges x = const
-        const float dy = fminf(fmaxf(-cb * dx * icc, ly), hy);
-        best = fminf(best, dx * (ca * dx + cb2 * dy) + cc * dy * dy);
-        const float ey = e ? hy : ly;          // horizontal edges y = const
-        const float ex = fminf(fmaxf(-cb * ey * ica, lx), hx);
-        best = fminf(best, ex * (ca * ex + cb2 * ey) + cc * ey * ey);
-    }
-    return best <= qlim;
-}
-
 constexpr int kWarps = 4;                        // warps per CTA = 8x8-pixel blocks of the 16x16 tile
 constexpr int kThreads = 32 * kWarps;
 constexpr int kBuf = 64;                         // entries staged per warp at a time
@@ -185,10 +159,11 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
             for (int h = 0; h < 2; h++) {
                 const int gx0 = (int)(r1[h].z & 0xffff), gx1 = (int)(r1[h].z >> 16);
                 const int gy0 = (int)(r1[h].w & 0xffff), gy1 = (int)(r1[h].w >> 16);
-                keep[h] = idx[h] < n && gx0 <= gx1 && (gx0 >> cg.ts) <= txi && txi <= (gx1 >> cg.ts) && (gy0 >> cg.ts) <= tyi &&
-                          tyi <= (gy1 >> cg.ts) && gx0 <= ax1 && gx1 >= ax0 && gy0 <= ay1 && gy1 >= ay0 &&
-                          ellipse_may_touch(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y), __uint_as_float(r0[h].z),
-                                            __uint_as_float(r0[h].w), __uint_as_float(r1[h].x), X0, X1, Y0, Y1, qlim);
+                keep[h] = (idx[h] < n) & (gx0 <= gx1) & ((gx0 >> cg.ts) <= txi) & (txi <= (gx1 >> cg.ts)) &
+                          ((gy0 >> cg.ts) <= tyi) & (tyi <= (gy1 >> cg.ts)) & (gx0 <= ax1) & (gx1 >= ax0) & (gy0 <= ay1) &
+                          (gy1 >= ay0) &
+                          ellipse_may_touch_bf(__uint_as_float(r0[h].x), __uint_as_float(r0[h].y), __uint_as_float(r0[h].z),
+                                               __uint_as_float(r0[h].w), __uint_as_float(r1[h].x), X0, X1, Y0, Y1, qlim);
             }
             uint32_t adv = 0;
 #pragma unroll
@@ -215,8 +190,9 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
                     bf.g2[d] = make_float2(__uint_as_float(r1[h].x), __uint_as_float(r1[h].y));
                     const int gx0 = (int)(r1[h].z & 0xffff), gx1 = (int)(r1[h].z >> 16);
                     const int gy0 = (int)(r1[h].w & 0xffff), gy1 = (int)(r1[h].w >> 16);
-                    bf.bm[d] = make_uint2(box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0),
-                                          box_lane_mask(gx0, gx1, gy0, gy1, bx0, by0 + 4));
+                    uint32_t mA, mB;
+                    box_lane_masks(gx0, gx1, gy0, gy1, bx0, by0, mA, mB);
+                    bf.bm[d] = make_uint2(mA, mB);
                     FeatLoad<FT>::template row<C>(feat + (size_t)idx[h] * C, &bf.f[d][0]);
                 }
                 cnt += __popc(bal);

@@ -15,14 +15,20 @@ import paper_2405_14866_b200 as tb
 
 
 def main():
-    nv = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    nv = int(args[0]) if len(args) > 0 else 4
+    reps = int(args[1]) if len(args) > 1 else 5
     s = sg.make_config("c3")
+    f32 = "--f32" in sys.argv
+    if f32:                                   # fp32-stored features: the SIMT compositor
+        for v in s.views:
+            v.feat = v.feat.astype("float32")
+        s.feat_dtype = "f32"
     targets = sg.make_targets("c4", n_targets=32)[::32 // nv][:nv]
     cx = tb.Context(0)
     p = tb.default_params()
     views, keep = tb.views_to_device(s.views)
-    g = tb.unproject(cx, views, 32, "f16", p)
+    g = tb.unproject(cx, views, 32, "f32" if f32 else "f16", p)
     torch.cuda.synchronize()
     H = W = 1024
     outs = []

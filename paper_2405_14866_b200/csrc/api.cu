@@ -33,12 +33,13 @@ struct ta_context {
     size_t smem_optin = 0;
     // per-context launch configuration (ta_context_create, on this context's device): persistent grid
     // sizes of the compositor / backward per C slot, and the tuning knobs read once from the environment
-    int resident_ws = 1;          // warp-specialized compositor (TA_COMPOSITOR=3)
+    int resident_ws[2] = {1, 1};  // warp-specialized compositor (TA_COMPOSITOR=3: 1 producer : 1 consumer, 4: 1 : 2)
     int resident_tc[6] = {1, 1, 1, 1, 1, 1}, resident_bwd[4] = {1, 1, 1, 1}, resident_tm[4] = {0, 1, 1, 1};
     int compositor = 0;           // TA_COMPOSITOR: 0 = mma.sync persistent-warp kernel (default; for fp16 C = 32 / 64 with
                                   // its accumulators in tensor memory), 1 = register (+ shared) accumulators for every C,
                                   // 2 = tensor-memory MMA kernel (tcgen05.mma, fp16 C >= 16; measured slower),
-                                  // 3 = warp-specialized producer / consumer kernel (fp16 C = 32; measured slower)
+                                  // 3 / 4 = warp-specialized producer : consumer = 1 : 1 / 1 : 2 (fp16 C = 32;
+                                  // measured slower)
     int coarse64_above = 1024;    // TA_COARSE64_ABOVE: 64-px coarse bins for targets wider / taller than this
     int tile_px = 16;             // TA_TILE_PX=8: 8 x 8 compositing tiles under 32-px coarse bins (opt-in, measured
                                   // slower: DESIGN.md section 6); 64-px bins and the TMEM compositor always use 16
@@ -267,7 +268,7 @@ ta_status ta_context_create(int32_t device, ta_context** out) {
     const int cap_tm = getenv("TA_TM_CTAS_PER_SM") ? atoi(getenv("TA_TM_CTAS_PER_SM")) : 0;
     if (prepare_composite(c->num_sms, cap, c->resident_tc) != cudaSuccess ||
         prepare_composite_tm(c->num_sms, cap_tm, c->resident_tm) != cudaSuccess ||
-        prepare_composite_ws(c->num_sms, cap, &c->resident_ws) != cudaSuccess ||
+        prepare_composite_ws(c->num_sms, cap, c->resident_ws) != cudaSuccess ||
         prepare_composite_bwd(c->num_sms, c->resident_bwd) != cudaSuccess) {
         cudaGetLastError();
         cudaFreeHost(c->pinned);
@@ -752,9 +753,9 @@ ta_status raster_pipeline(ta_context* c, const RasterJob& job) {
                                         (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
                                         counts ? (int32_t*)c->ncontrib.p : nullptr, s)
                   : cudaSuccess;
-    } else if (job.fbytes == 2 && job.C == 32 && c->compositor == 3 && cg.ts == 4) {
-        // warp-specialized compositor: producer (fill) / consumer (composite) warp pairs
-        e = launch_composite_ws(T, c->resident_ws, fast_exp, rec, job.feat, (const uint32_t*)c->tlist.p,
+    } else if (job.fbytes == 2 && job.C == 32 && (c->compositor == 3 || c->compositor == 4) && cg.ts == 4) {
+        // warp-specialized compositor: producer (fill) / consumer (composite) warps, 1 : 1 or 1 : 2
+        e = launch_composite_ws(c->compositor == 4 ? 2 : 1, T, c->resident_ws, fast_exp, rec, job.feat, (const uint32_t*)c->tlist.p,
                                 (const uint2*)c->trng.p, (uint32_t*)c->tile_order.p, cg, rc, cs,
                                 (uint64_t)(c->tlist.bytes / 4), feat_out, alpha_out,
                                 counts ? (int32_t*)c->ncontrib.p : nullptr, s);

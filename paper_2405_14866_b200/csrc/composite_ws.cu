@@ -24,8 +24,9 @@ namespace ta {
 namespace wsc {
 
 constexpr int C = 32;
-constexpr int kPairs = 4;
-constexpr int kThreads = 64 * kPairs;     // 4 producer + 4 consumer warps
+constexpr int kProducers = 4;             // warpgroup 0
+template <int kCPP>                       // consumers per producer: warpgroups 1 .. kCPP
+constexpr int threads_for() { return 32 * kProducers * (1 + kCPP); }
 #ifndef TA_WS_NB
 #define TA_WS_NB 32
 #endif
@@ -38,6 +39,13 @@ constexpr int kThreads = 64 * kPairs;     // 4 producer + 4 consumer warps
 #endif
 #ifndef TA_WS_REGS_C
 #define TA_WS_REGS_C 104
+#endif
+// 1 producer : 2 consumers (TA_COMPOSITOR=4): 2 CTAs of 12 warps per SM, registers rebalanced
+#ifndef TA_WS2_REGS_P
+#define TA_WS2_REGS_P 48
+#endif
+#ifndef TA_WS2_REGS_C
+#define TA_WS2_REGS_C 96
 #endif
 constexpr int NB = TA_WS_NB;              // entries per staging buffer
 constexpr int PH = C + 8;                 // feature row pitch (halves): 5 x 16 B, an odd number of 16-B chunks
@@ -57,26 +65,220 @@ struct Pair {
     int rblk, rect[4], pad[3];            // consumer -> producer: active-pixel box (x0, x1, y0, y1) of block rblk
     unsigned long long full[2], empty[2]; // mbarriers: buffer s filled / consumed
 };
+// A producer's walk through one consumer's current block (registers for 1 : 1, shared memory for 1 : 2)
+struct FillState {
+    uint32_t blk, pos, cend, pf_pos, pf0, pf1, fills0, fills1;
+    int bx0, by0, ax0, ax1, ay0, ay1, first, active, term, s;
+};
 
-template <bool kCounts, bool kFast>
-__global__ void __launch_bounds__(kThreads, TA_WS_BLOCKS)
+__device__ __forceinline__ bool mbar_test_parity(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n}\n" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0u;
+}
+
+// One staging buffer of the producer's walk `fs` (the fill of k_composite_tc): list indices (one round
+// ahead), splat records, cull against the consumer's latest active box, staging + feature rows by
+// cp.async; then the header and the hand-over to the consumer.  Returns true after the block's last buffer.
+template <bool kCounts>
+__device__ __forceinline__ bool fill_one(FillState& fs, Pair& pr, const uint4* __restrict__ rec,
+                                         const __half* __restrict__ feat, const uint32_t* __restrict__ clist, uint32_t n,
+                                         float qlim, unsigned long long* wk) {
+    const uint32_t lane = lane_id(), lt = lanemask_lt();
+    const int s = fs.s;
+    const uint32_t fills = s ? fs.fills1 : fs.fills0;
+    if (fills) mbar_wait_parity_sleep(smem_u32(&pr.empty[s]), (fills - 1u) & 1u);
+    if (!fs.first) {
+        // lane 0 reads the consumer's latest box and the warp takes its copy (lanes reading separately
+        // could see different publications, and the cull / fill below must be warp-uniform)
+        int rb = 0, r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+        if (lane == 0) {
+            rb = *(volatile int*)&pr.rblk;
+            r0 = *(volatile int*)&pr.rect[0];
+            r1 = *(volatile int*)&pr.rect[1];
+            r2 = *(volatile int*)&pr.rect[2];
+            r3 = *(volatile int*)&pr.rect[3];
+        }
+        rb = __shfl_sync(0xffffffffu, rb, 0);
+        if (rb == (int)fs.blk) {
+            fs.ax0 = __shfl_sync(0xffffffffu, r0, 0);
+            fs.ax1 = __shfl_sync(0xffffffffu, r1, 0);
+            fs.ay0 = __shfl_sync(0xffffffffu, r2, 0);
+            fs.ay1 = __shfl_sync(0xffffffffu, r3, 0);
+        }
+    }
+    Stage& st = pr.s[s];
+    int cnt = 0;
+    const int ax0 = fs.ax0, ax1 = fs.ax1, ay0 = fs.ay0, ay1 = fs.ay1, bx0 = fs.bx0, by0 = fs.by0;
+    const uint32_t cend = fs.cend;
+    uint32_t pos = fs.pos, pf_pos = fs.pf_pos, pf[2] = {fs.pf0, fs.pf1};
+    const bool live = ax0 <= ax1 && ay0 <= ay1;
+    if (live) {
+        const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
+        while (cnt < NB && pos < cend) {
+            uint32_t idx[2];
+            if (pf_pos == pos) {
+                idx[0] = pf[0];
+                idx[1] = pf[1];
+            } else {
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const uint32_t e = pos + 32 * hh + lane;
+                    idx[hh] = e < cend ? clist[e] : 0xffffffffu;
+                }
+            }
+            uint4 r0[2], r1[2];
+            bool keep[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
+                r1[hh] = rec[2 * i + 1];
+                r0[hh] = rec[2 * i];
+            }
+            pf_pos = pos + 64;
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const uint32_t e = pf_pos + 32 * hh + lane;
+                pf[hh] = e < cend ? clist[e] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
+                const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
+                keep[hh] = (idx[hh] < n) & (gx0 <= ax1) & (gx1 >= ax0) & (gy0 <= ay1) & (gy1 >= ay0) &
+                           ellipse_may_touch_bf(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
+                                                __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
+                                                __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
+            }
+            uint32_t adv = 0;
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                if (cnt >= NB) break;
+                const uint32_t base = pos + 32 * hh;
+                if (base >= cend) break;
+                bool kp = keep[hh];
+                uint32_t bal = __ballot_sync(0xffffffffu, kp);
+                const int room = NB - cnt;
+                const uint32_t rank = __popc(bal & lt);
+                uint32_t step = min(32u, cend - base);
+                if (__popc(bal) > room) {
+                    const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
+                    const int cl = __ffs(cut) - 1;
+                    bal &= (1u << cl) - 1u;
+                    step = (uint32_t)cl;
+                    kp = kp && (int)lane < cl;
+                }
+                if (kp) {
+                    const int d = cnt + (int)rank;
+                    const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
+                    const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
+                    float* const pp = reinterpret_cast<float*>(&st.p[d >> 1][0]) + (d & 1);
+                    pp[0] = __uint_as_float(r0[hh].x);
+                    pp[2] = __uint_as_float(r0[hh].y);
+                    pp[4] = -0.5f * __uint_as_float(r0[hh].z);
+                    pp[6] = -0.5f * __uint_as_float(r0[hh].w);
+                    pp[8] = -0.5f * __uint_as_float(r1[hh].x);
+                    pp[10] = 2048.0f * __uint_as_float(r1[hh].y);
+                    uint32_t mA, mB;
+                    box_lane_masks(gx0, gx1, gy0, gy1, bx0, by0, mA, mB);
+                    pp[12] = __uint_as_float(mA);
+                    pp[14] = __uint_as_float(mB);
+                    const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
+                    const uint32_t dst = smem_u32(&st.f[d][0]);
+#pragma unroll
+                    for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
+                }
+                cnt += __popc(bal);
+                adv += step;
+                if (step < 32u) break;
+            }
+            pos += adv;
+            if (kCounts) { wk[0] += adv; wk[7] += 1; }
+        }
+    }
+    cp_async_wait_all();
+    const bool last = !live || pos >= cend;
+    if (kCounts) wk[1] += cnt;
+    if (lane == 0) { st.cnt = cnt; st.flags = (fs.first ? kFirst : 0) | (last ? kLast : 0); st.blk = (int)fs.blk; }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(smem_u32(&pr.full[s]));
+    if (s) fs.fills1++; else fs.fills0++;
+    fs.s = s ^ 1;
+    fs.first = 0;
+    fs.pos = pos;
+    fs.pf_pos = pf_pos;
+    fs.pf0 = pf[0];
+    fs.pf1 = pf[1];
+    if (last) fs.active = 0;
+    return last;
+}
+
+// Starts the producer's walk of the next block for a consumer (claims it); false when none is left.
+__device__ __forceinline__ bool begin_block(FillState& fs, uint32_t* wq, uint32_t nblk, const uint32_t* __restrict__ order,
+                                            const uint2* __restrict__ trng, const CompositeGeom& cg, uint64_t list_cap) {
+    uint32_t blk = 0;
+    if (lane_id() == 0) blk = atomicAdd(wq, 1u);
+    blk = __shfl_sync(0xffffffffu, blk, 0);
+    if (blk >= nblk) return false;
+    const int tile = (int)order[blk >> 2];
+    const uint32_t qd = blk & 3u;
+    const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
+    const uint2 tr = trng[tile];
+    uint32_t cend = tr.x + tr.y;
+    if (cend > list_cap) cend = (uint32_t)list_cap;
+    fs.blk = blk;
+    fs.pos = tr.x;
+    fs.cend = cend;
+    fs.pf_pos = 0xffffffffu;
+    fs.bx0 = txi * kTile + 8 * (int)(qd & 1);
+    fs.by0 = tyi * kTile + 8 * (int)(qd >> 1);
+    // culling rectangle: the block's in-frame pixels until the consumer publishes its active box
+    fs.ax0 = fs.bx0; fs.ax1 = min(fs.bx0 + 7, cg.W - 1);
+    fs.ay0 = fs.by0; fs.ay1 = min(fs.by0 + 7, cg.H - 1);
+    fs.first = 1;
+    fs.active = 1;
+    return true;
+}
+
+// Hands the terminate marker to a consumer through its next buffer.
+__device__ __forceinline__ void send_term(FillState& fs, Pair& pr) {
+    const int s = fs.s;
+    const uint32_t fills = s ? fs.fills1 : fs.fills0;
+    if (fills) mbar_wait_parity_sleep(smem_u32(&pr.empty[s]), (fills - 1u) & 1u);
+    if (lane_id() == 0) { pr.s[s].cnt = 0; pr.s[s].flags = kTerm; pr.s[s].blk = -1; }
+    __threadfence_block();
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive1(smem_u32(&pr.full[s]));
+    fs.term = 1;
+}
+
+template <bool kCounts, bool kFast, int kCPP>
+__global__ void __launch_bounds__(threads_for<kCPP>(), kCPP == 1 ? TA_WS_BLOCKS : 2)
 k_composite_ws(const uint4* __restrict__ rec, const __half* __restrict__ feat, const uint32_t* __restrict__ clist,
                const uint2* __restrict__ trng, const uint32_t* __restrict__ order, CompositeGeom cg, RasterConsts rc,
                const CallState* __restrict__ cs, uint64_t list_cap, float* __restrict__ Fout, float* __restrict__ Aout,
                int32_t* __restrict__ ncontrib) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Pair* const pairs = reinterpret_cast<Pair*>(smem_raw);
+    FillState* const pstate = reinterpret_cast<FillState*>(pairs + kProducers * kCPP);   // 1 : 2 walks
     __shared__ uint32_t s_tmem;
     const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-    const bool producer = warp < (uint32_t)kPairs;
-    Pair& pr = pairs[producer ? warp : warp - kPairs];
+    const bool producer = warp < (uint32_t)kProducers;
+    const int cidx = producer ? 0 : (int)warp - kProducers;        // consumer pair index
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&s_tmem)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(64 * kCPP) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (producer && lane == 0) {
-        for (int k = 0; k < 2; k++) { mbar_init1(smem_u32(&pr.full[k])); mbar_init1(smem_u32(&pr.empty[k])); }
-        pr.rblk = -1;
+        for (int c = 0; c < kCPP; c++) {
+            Pair& q = pairs[(int)warp + kProducers * c];
+            for (int k = 0; k < 2; k++) { mbar_init1(smem_u32(&q.full[k])); mbar_init1(smem_u32(&q.empty[k])); }
+            q.rblk = -1;
+        }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -88,153 +290,73 @@ k_composite_ws(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
 
     if (producer) {
         // ================================================================ producer: fill
-#if TA_WS_REGS_P
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TA_WS_REGS_P));
-#endif
+        if (kCPP == 1) { if (TA_WS_REGS_P) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TA_WS_REGS_P)); }
+        else { if (TA_WS2_REGS_P) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TA_WS2_REGS_P)); }
         uint32_t* const wq = &const_cast<CallState*>(cs)->scan_counter[6];
         const uint32_t n = cs->n;
         const float qlim = rc.q_max * 1.015625f + 0.01f;
-        const uint32_t lt = lanemask_lt();
-        uint32_t fills[2] = {0u, 0u};
-        int s = 0;
-        for (;;) {
-            uint32_t blk = 0;
-            if (lane == 0) blk = atomicAdd(wq, 1u);
-            blk = __shfl_sync(0xffffffffu, blk, 0);
-            if (blk >= nblk) {                             // no work left: tell the consumer to finish
-                if (fills[s]) mbar_wait_parity_sleep(smem_u32(&pr.empty[s]), (fills[s] - 1u) & 1u);
-                if (lane == 0) { pr.s[s].cnt = 0; pr.s[s].flags = kTerm; pr.s[s].blk = -1; }
-                __threadfence_block();
-                __syncwarp();
-                if (lane == 0) mbar_arrive1(smem_u32(&pr.full[s]));
-                break;
-            }
-            if (kCounts) wk[6] += 1;
-            const int tile = (int)order[blk >> 2];
-            const uint32_t qd = blk & 3u;
-            const int tyi = tile / cg.TX, txi = tile - tyi * cg.TX;
-            const uint2 tr = trng[tile];
-            uint32_t cend = tr.x + tr.y;
-            if (cend > list_cap) cend = (uint32_t)list_cap;
-            const int bx0 = txi * kTile + 8 * (int)(qd & 1), by0 = tyi * kTile + 8 * (int)(qd >> 1);
-            // culling rectangle: the block's in-frame pixels until the consumer publishes its active box
-            int ax0 = bx0, ax1 = min(bx0 + 7, W - 1), ay0 = by0, ay1 = min(by0 + 7, H - 1);
-            uint32_t pos = tr.x;
-            uint32_t pf_pos = 0xffffffffu, pf[2] = {0u, 0u};
-            bool first = true;
+        if (kCPP == 1) {
+            Pair& pr = pairs[warp];
+            FillState fs;
+            fs.fills0 = fs.fills1 = 0u;
+            fs.s = 0;
+            fs.term = 0;
             for (;;) {
-                if (fills[s]) mbar_wait_parity_sleep(smem_u32(&pr.empty[s]), (fills[s] - 1u) & 1u);
-                if (!first && *(volatile int*)&pr.rblk == (int)blk) {
-                    ax0 = *(volatile int*)&pr.rect[0];
-                    ax1 = *(volatile int*)&pr.rect[1];
-                    ay0 = *(volatile int*)&pr.rect[2];
-                    ay1 = *(volatile int*)&pr.rect[3];
+                if (!begin_block(fs, wq, nblk, order, trng, cg, list_cap)) { send_term(fs, pr); break; }
+                if (kCounts) wk[6] += 1;
+                while (!fill_one<kCounts>(fs, pr, rec, feat, clist, n, qlim, wk)) {}
+            }
+        } else {
+            // one producer, kCPP consumers: serve whichever consumer has a free buffer; walks in shared memory
+            FillState* const my = pstate + (int)warp * kCPP;
+            if (lane == 0)
+                for (int c = 0; c < kCPP; c++) {
+                    my[c].fills0 = my[c].fills1 = 0u;
+                    my[c].s = 0;
+                    my[c].term = 0;
+                    my[c].active = 0;
                 }
-                Stage& st = pr.s[s];
-                int cnt = 0;
-                const bool live = ax0 <= ax1 && ay0 <= ay1;
-                if (live) {
-                    const float X0 = (float)ax0, X1 = (float)ax1, Y0 = (float)ay0, Y1 = (float)ay1;
-                    while (cnt < NB && pos < cend) {
-                        uint32_t idx[2];
-                        if (pf_pos == pos) {
-                            idx[0] = pf[0];
-                            idx[1] = pf[1];
-                        } else {
-#pragma unroll
-                            for (int hh = 0; hh < 2; hh++) {
-                                const uint32_t e = pos + 32 * hh + lane;
-                                idx[hh] = e < cend ? clist[e] : 0xffffffffu;
-                            }
+            __syncwarp();
+            for (;;) {
+                bool all_done = true, progressed = false;
+                for (int c = 0; c < kCPP; c++) {
+                    FillState fs = my[c];
+                    if (fs.term) continue;
+                    all_done = false;
+                    Pair& pr = pairs[(int)warp + kProducers * c];
+                    const uint32_t fills = fs.s ? fs.fills1 : fs.fills0;
+                    // (one lane's view of the barrier for the whole warp: lanes polling separately could
+                    //  disagree while the phase completes, and the fill below is warp-synchronous)
+                    const bool free_buf = !fills || __shfl_sync(0xffffffffu, (uint32_t)mbar_test_parity(
+                                                       smem_u32(&pr.empty[fs.s]), (fills - 1u) & 1u), 0) != 0u;
+                    if (!free_buf) continue;
+                    progressed = true;
+                    if (!fs.active) {
+                        if (!begin_block(fs, wq, nblk, order, trng, cg, list_cap)) {
+                            send_term(fs, pr);
+                            __syncwarp();
+                            if (lane == 0) my[c] = fs;
+                            __syncwarp();
+                            continue;
                         }
-                        uint4 r0[2], r1[2];
-                        bool keep[2];
-#pragma unroll
-                        for (int hh = 0; hh < 2; hh++) {
-                            const uint32_t i = idx[hh] < n ? idx[hh] : 0u;
-                            r1[hh] = rec[2 * i + 1];
-                            r0[hh] = rec[2 * i];
-                        }
-                        pf_pos = pos + 64;
-#pragma unroll
-                        for (int hh = 0; hh < 2; hh++) {
-                            const uint32_t e = pf_pos + 32 * hh + lane;
-                            pf[hh] = e < cend ? clist[e] : 0xffffffffu;
-                        }
-#pragma unroll
-                        for (int hh = 0; hh < 2; hh++) {
-                            const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
-                            const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                            keep[hh] = (idx[hh] < n) & (gx0 <= ax1) & (gx1 >= ax0) & (gy0 <= ay1) & (gy1 >= ay0) &
-                                       ellipse_may_touch_bf(__uint_as_float(r0[hh].x), __uint_as_float(r0[hh].y),
-                                                            __uint_as_float(r0[hh].z), __uint_as_float(r0[hh].w),
-                                                            __uint_as_float(r1[hh].x), X0, X1, Y0, Y1, qlim);
-                        }
-                        uint32_t adv = 0;
-#pragma unroll
-                        for (int hh = 0; hh < 2; hh++) {
-                            if (cnt >= NB) break;
-                            const uint32_t base = pos + 32 * hh;
-                            if (base >= cend) break;
-                            bool kp = keep[hh];
-                            uint32_t bal = __ballot_sync(0xffffffffu, kp);
-                            const int room = NB - cnt;
-                            const uint32_t rank = __popc(bal & lt);
-                            uint32_t step = min(32u, cend - base);
-                            if (__popc(bal) > room) {
-                                const uint32_t cut = __ballot_sync(0xffffffffu, kp && rank == (uint32_t)room);
-                                const int cl = __ffs(cut) - 1;
-                                bal &= (1u << cl) - 1u;
-                                step = (uint32_t)cl;
-                                kp = kp && (int)lane < cl;
-                            }
-                            if (kp) {
-                                const int d = cnt + (int)rank;
-                                const int gx0 = (int)(r1[hh].z & 0xffff), gx1 = (int)(r1[hh].z >> 16);
-                                const int gy0 = (int)(r1[hh].w & 0xffff), gy1 = (int)(r1[hh].w >> 16);
-                                float* const pp = reinterpret_cast<float*>(&st.p[d >> 1][0]) + (d & 1);
-                                pp[0] = __uint_as_float(r0[hh].x);
-                                pp[2] = __uint_as_float(r0[hh].y);
-                                pp[4] = -0.5f * __uint_as_float(r0[hh].z);
-                                pp[6] = -0.5f * __uint_as_float(r0[hh].w);
-                                pp[8] = -0.5f * __uint_as_float(r1[hh].x);
-                                pp[10] = 2048.0f * __uint_as_float(r1[hh].y);
-                                uint32_t mA, mB;
-                                box_lane_masks(gx0, gx1, gy0, gy1, bx0, by0, mA, mB);
-                                pp[12] = __uint_as_float(mA);
-                                pp[14] = __uint_as_float(mB);
-                                const char* src = reinterpret_cast<const char*>(feat + (size_t)idx[hh] * C);
-                                const uint32_t dst = smem_u32(&st.f[d][0]);
-#pragma unroll
-                                for (int c = 0; c < C * 2; c += 16) cp_async16(dst + c, src + c);
-                            }
-                            cnt += __popc(bal);
-                            adv += step;
-                            if (step < 32u) break;
-                        }
-                        pos += adv;
-                        if (kCounts) { wk[0] += adv; wk[7] += 1; }
+                        if (kCounts) wk[6] += 1;
                     }
+                    fill_one<kCounts>(fs, pr, rec, feat, clist, n, qlim, wk);
+                    fs.pf_pos = 0xffffffffu;        // the prefetched indices are per lane: not kept in the shared walk
+                    __syncwarp();
+                    if (lane == 0) my[c] = fs;
+                    __syncwarp();
                 }
-                cp_async_wait_all();
-                const bool last = !live || pos >= cend;
-                if (kCounts) wk[1] += cnt;
-                if (lane == 0) { st.cnt = cnt; st.flags = (first ? kFirst : 0) | (last ? kLast : 0); st.blk = (int)blk; }
-                __threadfence_block();
-                __syncwarp();
-                if (lane == 0) mbar_arrive1(smem_u32(&pr.full[s]));
-                fills[s]++;
-                s ^= 1;
-                first = false;
-                if (last) break;
+                if (all_done) break;
+                if (!progressed) __nanosleep(256);
             }
         }
     } else {
+        Pair& pr = pairs[cidx];
         // ================================================================ consumer: composite
-#if TA_WS_REGS_C
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TA_WS_REGS_C));
-#endif
-        const uint32_t tacc = s_tmem + ((32u * (warp & 3u)) << 16);
+        if (kCPP == 1) { if (TA_WS_REGS_C) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TA_WS_REGS_C)); }
+        else { if (TA_WS2_REGS_C) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TA_WS2_REGS_C)); }
+        const uint32_t tacc = s_tmem + ((32u * (warp & 3u)) << 16) + 64u * (uint32_t)(cidx / kProducers);
         const float teps = rc.t_eps, qlo = rc.q_lo_half, amx = rc.a_max_2k, alo = rc.a_min_2k;
         const int li = (int)lane;
         const uint32_t a_base = smem_u32(&pr.w[0][(li & 7) + 8 * (li >> 4)][0]) + (uint32_t)(((li >> 3) & 1) * 16);
@@ -516,23 +638,27 @@ k_composite_ws(const uint4* __restrict__ rec, const __half* __restrict__ feat, c
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(s_tmem) : "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(64 * kCPP) : "memory");
 }
 
 }  // namespace wsc
 
 // Per-device preparation: shared-memory opt-in and co-resident CTAs (registers, shared memory, TMEM).
-cudaError_t prepare_composite_ws(int num_sms, int cap, int* resident) {
-    const int smem = (int)(sizeof(wsc::Pair) * wsc::kPairs);
+template <int kCPP>
+static size_t ws_smem() { return sizeof(wsc::Pair) * wsc::kProducers * kCPP + (kCPP > 1 ? sizeof(wsc::FillState) * wsc::kProducers * kCPP : 0); }
+
+template <int kCPP>
+static cudaError_t prepare_ws(int num_sms, int cap, int* resident) {
+    const int smem = (int)ws_smem<kCPP>();
     const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(wsc::k_composite_ws<false, false>, A, smem)) ||
-        (e = cudaFuncSetAttribute(wsc::k_composite_ws<true, false>, A, smem)) ||
-        (e = cudaFuncSetAttribute(wsc::k_composite_ws<false, true>, A, smem)) ||
-        (e = cudaFuncSetAttribute(wsc::k_composite_ws<true, true>, A, smem)))
+    if ((e = cudaFuncSetAttribute(wsc::k_composite_ws<false, false, kCPP>, A, smem)) ||
+        (e = cudaFuncSetAttribute(wsc::k_composite_ws<true, false, kCPP>, A, smem)) ||
+        (e = cudaFuncSetAttribute(wsc::k_composite_ws<false, true, kCPP>, A, smem)) ||
+        (e = cudaFuncSetAttribute(wsc::k_composite_ws<true, true, kCPP>, A, smem)))
         return e;
     cudaFuncAttributes fa{};
-    if ((e = cudaFuncGetAttributes(&fa, wsc::k_composite_ws<false, false>))) return e;
+    if ((e = cudaFuncGetAttributes(&fa, wsc::k_composite_ws<false, false, kCPP>))) return e;
     int dev = 0, regs_sm = 0, smem_sm = 0, thr_sm = 0, blk_sm = 0, smem_rsv = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
@@ -540,28 +666,35 @@ cudaError_t prepare_composite_ws(int num_sms, int cap, int* resident) {
     cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
     cudaDeviceGetAttribute(&blk_sm, cudaDevAttrMaxBlocksPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
-    const int regs_blk = ((fa.numRegs * 32 + 255) / 256 * 256) * (wsc::kThreads / 32);
-    int per_sm = std::min(thr_sm / wsc::kThreads, blk_sm);
+    constexpr int kThr = wsc::threads_for<kCPP>();
+    const int regs_blk = ((fa.numRegs * 32 + 255) / 256 * 256) * (kThr / 32);
+    int per_sm = std::min(thr_sm / kThr, blk_sm);
     per_sm = std::min(per_sm, regs_sm / std::max(1, regs_blk));
     per_sm = std::min(per_sm, smem_sm / (smem + (int)fa.sharedSizeBytes + smem_rsv));
-    per_sm = std::min(per_sm, 512 / 64);
+    per_sm = std::min(per_sm, 512 / (64 * kCPP));
     if (getenv("TA_DEBUG_PREP"))
-        fprintf(stderr, "k_composite_ws: %d regs, %d B local, smem %d, %d CTAs/SM\n", fa.numRegs, (int)fa.localSizeBytes,
-                smem, per_sm);
+        fprintf(stderr, "k_composite_ws<1:%d>: %d regs, %d B local, smem %d, %d CTAs/SM\n", kCPP, fa.numRegs,
+                (int)fa.localSizeBytes, smem, per_sm);
     if (cap > 0) per_sm = std::min(per_sm, cap);
     *resident = std::max(1, num_sms * std::max(1, per_sm));
     return cudaSuccess;
 }
 
-cudaError_t launch_composite_ws(int tiles, int resident, bool fast, const uint4* rec, const void* feat, const uint32_t* list,
-                                const uint2* trng, uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs,
-                                uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
-    if (tiles == 0) return cudaSuccess;
-    const size_t smem = sizeof(wsc::Pair) * wsc::kPairs;
+cudaError_t prepare_composite_ws(int num_sms, int cap, int* resident) {
+    cudaError_t e;
+    if ((e = prepare_ws<1>(num_sms, cap, &resident[0])) || (e = prepare_ws<2>(num_sms, cap, &resident[1]))) return e;
+    return cudaSuccess;
+}
+
+template <int kCPP>
+static cudaError_t launch_ws(int tiles, int resident, bool fast, const uint4* rec, const void* feat, const uint32_t* list,
+                             const uint2* trng, uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs,
+                             uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st) {
+    const size_t smem = ws_smem<kCPP>();
     const int grid = std::min(tiles, resident);
-    launch_tile_order(trng, cg, order, st);
+    constexpr int kThr = wsc::threads_for<kCPP>();
     const __half* fh = static_cast<const __half*>(feat);
-#define TA_WS(K, FA) wsc::k_composite_ws<K, FA><<<grid, wsc::kThreads, smem, st>>>(rec, fh, list, trng, order, cg, rc, cs, list_cap, F, A, ncontrib)
+#define TA_WS(K, FA) wsc::k_composite_ws<K, FA, kCPP><<<grid, kThr, smem, st>>>(rec, fh, list, trng, order, cg, rc, cs, list_cap, F, A, ncontrib)
     if (ncontrib) {
         if (fast) TA_WS(true, true); else TA_WS(true, false);
     } else {
@@ -569,6 +702,16 @@ cudaError_t launch_composite_ws(int tiles, int resident, bool fast, const uint4*
     }
 #undef TA_WS
     return cudaGetLastError();
+}
+
+cudaError_t launch_composite_ws(int cpp, int tiles, const int* resident, bool fast, const uint4* rec, const void* feat,
+                                const uint32_t* list, const uint2* trng, uint32_t* order, CompositeGeom cg, RasterConsts rc,
+                                const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
+                                cudaStream_t st) {
+    if (tiles == 0) return cudaSuccess;
+    launch_tile_order(trng, cg, order, st);
+    return cpp == 2 ? launch_ws<2>(tiles, resident[1], fast, rec, feat, list, trng, order, cg, rc, cs, list_cap, F, A, ncontrib, st)
+                    : launch_ws<1>(tiles, resident[0], fast, rec, feat, list, trng, order, cg, rc, cs, list_cap, F, A, ncontrib, st);
 }
 
 }  // namespace ta

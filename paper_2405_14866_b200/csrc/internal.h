@@ -107,10 +107,12 @@ cudaError_t launch_composite_tm(int C, int tiles, const int* resident, bool fast
                                 RasterConsts rc, const CallState* cs, uint64_t list_cap, float* F, float* A,
                                 int32_t* ncontrib, cudaStream_t st);
 // composite_ws.cu: warp-specialized compositor (producer / consumer warp pairs; fp16 C = 32, 16 x 16 tiles)
+// (resident[0]: 1 producer : 1 consumer, resident[1]: 1 : 2)
 cudaError_t prepare_composite_ws(int num_sms, int cap, int* resident);
-cudaError_t launch_composite_ws(int tiles, int resident, bool fast, const uint4* rec, const void* feat, const uint32_t* list,
-                                const uint2* trng, uint32_t* order, CompositeGeom cg, RasterConsts rc, const CallState* cs,
-                                uint64_t list_cap, float* F, float* A, int32_t* ncontrib, cudaStream_t st);
+cudaError_t launch_composite_ws(int cpp, int tiles, const int* resident, bool fast, const uint4* rec, const void* feat,
+                                const uint32_t* list, const uint2* trng, uint32_t* order, CompositeGeom cg, RasterConsts rc,
+                                const CallState* cs, uint64_t list_cap, float* F, float* A, int32_t* ncontrib,
+                                cudaStream_t st);
 // backward.cu
 cudaError_t prepare_composite_bwd(int num_sms, int resident[4]);
 cudaError_t launch_composite_bwd(int C, int fbytes, int tiles, const int* resident, bool simt, const uint4* rec, const void* feat, const uint32_t* tlist,

@@ -60,7 +60,7 @@ def gaussians_to_host(g):
                 feat=g.feat[:n].cpu().numpy())
 
 
-def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True, counts=True):
+def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True, counts=True, same_f_bits=True):
     """Rasterize with `params` as given -- by default flags = 0, the compositor instantiation bench.py
     times -- and pull every stage's output back to the host.  With `counts`, the same call is
     repeated with TA_FLAG_DEBUG_COUNTS added (the counters instantiation): its F and A must be
@@ -93,7 +93,8 @@ def gpu_rasterize(ctx, g, cam, params, n=-1, debug=True, counts=True):
         pc.flags = params.flags | tb.TA_FLAG_DEBUG_COUNTS
         F2, A2 = tb.rasterize(ctx, g, K, R, t, cam.H, cam.W, pc, n=n)
         torch.cuda.synchronize()
-        assert torch.equal(F2.view(torch.int32), F.view(torch.int32)), "counters instantiation changed F"
+        if same_f_bits:   # (the warp-specialized variants group their fp32 MMA sums by timing: A only)
+            assert torch.equal(F2.view(torch.int32), F.view(torch.int32)), "counters instantiation changed F"
         assert torch.equal(A2.view(torch.int32), A.view(torch.int32)), "counters instantiation changed A"
         d2 = ctx.debug_last()
         out["n_contrib"] = d2h(d2.n_contrib, cam.H * cam.W, np.int32).reshape(cam.H, cam.W)

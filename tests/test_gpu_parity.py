@@ -28,7 +28,7 @@ def oracle_lib():
     return oracle
 
 
-def full_parity(ctx, O, scene, tidx=0, tiles=None, async_=False, **pkw):
+def full_parity(ctx, O, scene, tidx=0, tiles=None, async_=False, same_f_bits=True, **pkw):
     """Every stage of the CUDA path against the oracle on one scene and target.  The rasterize call
     runs the instantiation bench.py times (flags = 0; with async_, TA_FLAG_ASYNC on a context sized
     by ta_reserve as in bench.py), then again with TA_FLAG_DEBUG_COUNTS, which must give the same bits
@@ -47,7 +47,7 @@ def full_parity(ctx, O, scene, tidx=0, tiles=None, async_=False, **pkw):
         rctx = tb.Context(0)
         rctx.reserve(g.capacity, max(int(sizing["Kc"] * 1.05), 1) + 1024, cam.H, cam.W)
         gp = P.gpu_params(scene, flags=tb.TA_FLAG_ASYNC, **pkw)
-    out = P.gpu_rasterize(rctx, g, cam, gp)
+    out = P.gpu_rasterize(rctx, g, cam, gp, same_f_bits=same_f_bits)
     if async_:
         assert not rctx.check_overflow()
     K, R, t = sg.cam_arrays(cam)
@@ -509,20 +509,25 @@ def test_tensor_memory_compositor_parity(oracle_lib, cfg):
     full_parity(c, oracle_lib, s)
 
 
+@pytest.mark.parametrize("comp", ["3", "4"])
 @pytest.mark.parametrize("cfg", ["c2", "c3r"])
-def test_warp_specialized_compositor_parity(oracle_lib, cfg):
-    """The opt-in warp-specialized compositor (TA_COMPOSITOR=3: producer / consumer warp pairs handing
-    staging buffers over mbarriers, accumulators in tensor memory) against the oracle: every stage and
-    every pixel, A and composited counts bit-exact, F within 1e-4."""
+def test_warp_specialized_compositor_parity(oracle_lib, cfg, comp):
+    """The opt-in warp-specialized compositors (TA_COMPOSITOR=3: one producer warp per consumer warp,
+    4: one producer for two consumers; staging buffers handed over mbarriers, accumulators in tensor
+    memory) against the oracle: every stage and every pixel, A and composited counts bit-exact, F within
+    1e-4."""
     import os
     import paper_2405_14866_b200 as tb
-    os.environ["TA_COMPOSITOR"] = "3"
+    os.environ["TA_COMPOSITOR"] = comp
     try:
         c = tb.Context(0)
     finally:
         os.environ.pop("TA_COMPOSITOR")
     s = sg.make_config("c2") if cfg == "c2" else sg.make_config("c3", res=256, target_hw=(136, 200))
-    full_parity(c, oracle_lib, s)
+    # the producer culls against the consumer's active box as last published, so which entries are staged
+    # (and with them the grouping of the fp32 MMA sums) depends on timing: F can differ between runs in
+    # its last bits, the decisions (A, counts) cannot
+    full_parity(c, oracle_lib, s, same_f_bits=False)
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3r"])

@@ -303,6 +303,9 @@ k_composite(const uint4* __restrict__ rec, const FT* __restrict__ feat, const ui
 // k_bin_place stored above the entry's index), an exclusive scan over the warps gives every (segment, tile) write
 // offset, pass 2 writes.  Tile q of bin b owns tlist[NQ cstart_b + q len_b, + len_b) (a tile list
 // is a subsequence of the bin list); trng[tile] = (start, count).
+#ifndef TA_SPLIT_PACKED
+#define TA_SPLIT_PACKED 1
+#endif
 template <int NQ>
 __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict__ clist,
                                                      const uint32_t* __restrict__ coffs, CompositeGeom cg,
@@ -370,7 +373,22 @@ __global__ void __launch_bounds__(1024) k_tile_split(const uint32_t* __restrict_
     uint32_t run[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; q++) run[q] = 0u;
-    walk(false, run);
+    if (NQ == 4 && TA_SPLIT_PACKED) {
+        // pass 1 for 2 x 2 tiles: each lane counts its entries per tile in two 16-bit-field words, one warp
+        // reduction per tile at the end (instead of a ballot per tile per 32 entries)
+        uint32_t c01 = 0u, c23 = 0u;
+        for (uint32_t pos = s0 + lane; pos < s1; pos += 32) {
+            const uint32_t tm = clist[pos] >> IB;
+            c01 += (tm & 1u) | ((tm & 2u) << 15);
+            c23 += ((tm >> 2) & 1u) | ((tm & 8u) << 13);
+        }
+        run[0] = __reduce_add_sync(0xffffffffu, c01 & 0xffffu);
+        run[1] = __reduce_add_sync(0xffffffffu, c01 >> 16);
+        run[2 % NQ] = __reduce_add_sync(0xffffffffu, c23 & 0xffffu);
+        run[3 % NQ] = __reduce_add_sync(0xffffffffu, c23 >> 16);
+    } else {
+        walk(false, run);
+    }
 #pragma unroll
     for (int q = 0; q < NQ; q++)
         if (lane == (uint32_t)q) s_cnt[warp][q] = run[q];

@@ -409,7 +409,15 @@ def run_ours(args):
             "data": "synthetic (seeded synthgen rig: ellipsoid upper body, log-normal scales, random rotations)",
             "config": dict(workload_config(n_g, kmax), streams=nstr,
                            exp="fast (MUFU ex2.approx, TA exact_exp = 0)" if args.fast_exp else
-                               "exact (exp_det, DESIGN.md R13; TA exact_exp = 1)"),
+                               "exact (exp_det, DESIGN.md R13; TA exact_exp = 1)",
+                           compositor={"0": "k_composite_tc: packed-fp32 recurrence, mma.sync feature accumulation "
+                                             "into tensor-memory accumulators (tcgen05.ld/st), 5 CTAs/SM",
+                                       "1": "k_composite_tc with register accumulators",
+                                       "2": "k_composite_tm (tcgen05.mma)",
+                                       "3": "k_composite_ws (producer:consumer 1:1)",
+                                       "4": "k_composite_ws (producer:consumer 1:2)"}.get(
+                               os.environ.get("TA_COMPOSITOR", "0"), "?"),
+                           tile_px=int(os.environ.get("TA_TILE_PX", "16") == "8") * 8 or 16),
             "gpu_launches": launches, "clocks": clk, "overflow": overflow,
             "step_ms_rank0": {"median": step_ms[len(step_ms) // 2], "min": step_ms[0],
                               "p90": step_ms[min(len(step_ms) - 1, int(0.9 * len(step_ms)))],

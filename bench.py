@@ -224,7 +224,7 @@ def workload_config(n, K):
     return {"workload": "c4: BASELINE.json configs[3] -- c3 Gaussian set (4 x 1024^2 sources, C=32 fp16-stored) "
                         "rendered to 32 parallax targets 1024^2 per frame",
             "views_per_step": 32, "target": "1024x1024", "C": 32, "feat_storage": "f16", "sources": "4x1024x1024",
-            "n_gaussians": n, "entries_per_view": K,
+            "n_gaussians": n, "entries_per_view": K, "focal_scale": __import__("synthgen").FOCAL_SCALE,
             "l2": "no flush: inputs larger than L2 (423 MB source maps, 187 MB Gaussian set, "
                   "~68 MB tile lists + 138 MB output per view)",
             "parallelism": "target views sharded over ranks; Gaussian set NCCL-broadcast from rank 0"}
@@ -690,7 +690,13 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
     torch.cuda.synchronize()
     d = ctx.debug_last()
     rec = P.d2h(d.records, 8 * d.n, np.uint32).reshape(-1, 8)
-    nvis = int(np.count_nonzero((rec[:, 6] & 0xffff) <= (rec[:, 6] >> 16)))
+    visible = (rec[:, 6] & 0xffff) <= (rec[:, 6] >> 16)
+    nvis = int(np.count_nonzero(visible))
+    # sigma_px = largest-axis std-dev of the projected covariance = 1 / sqrt(smallest
+    # eigenvalue of the conic (ca, cb2 / 2; cb2 / 2, cc))
+    cf = rec[visible][:, 2:5].view(np.float32).astype(np.float64)
+    lam_min = 0.5 * (cf[:, 0] + cf[:, 2]) - np.sqrt(0.25 * (cf[:, 0] - cf[:, 2]) ** 2 + 0.25 * cf[:, 1] ** 2)
+    sigma_px = float(np.median(1.0 / np.sqrt(np.maximum(lam_min, 1e-30)))) if nvis else 0.0
     pairs = int(P.d2h(d.n_contrib, H * W, np.int32).astype(np.int64).sum())
     K = int(d.K)
     Kc = int(d.Kc)
@@ -743,6 +749,7 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
         pass
     r.update({"kernel": dom, "traffic": traffic, "ms_per_launch": stages[dom],
               "algorithmic_bytes_per_launch": bytes_alg[dom], "composited_pairs_per_view": pairs,
+              "sigma_px_median": sigma_px,
               "visible_gaussians": nvis, "entries_per_view": K, "coarse_entries_per_view": Kc,
               "work_counters": {k: int(v) for k, v in zip(
                   ("list_entries_read", "staged", "evaluated", "evaluated_q_ok", "accumulated", "composited_pairs",
@@ -899,6 +906,8 @@ def main():
     ap.add_argument("--streams", type=int, default=4)
     ap.add_argument("--fast-exp", action="store_true", help="time the opt-in MUFU ex2 mode (exact_exp = 0)")
     ap.add_argument("--c3-calls", type=int, default=20)
+    ap.add_argument("--focal-scale", type=float, default=1.95,
+                    help="SURVEY 8(d) sensitivity: f = scale * W (body scaled to keep its image); 1.95 = headline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stage-events", action="store_true")
@@ -906,6 +915,9 @@ def main():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--dry-run-dist", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.focal_scale != 1.95:
+        import synthgen as sg
+        sg.set_focal_scale(args.focal_scale)
     cmd = relaunch_command(args.gpus, sys.argv[1:], os.environ)
     if cmd is not None:
         return subprocess.call(cmd)

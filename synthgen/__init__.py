@@ -122,6 +122,18 @@ ELLIPSOIDS = (
 )
 PLANE_Z = 3.0
 FOCAL_SCALE = 1.95
+_BASE_ELLIPSOIDS = ELLIPSOIDS
+
+
+def set_focal_scale(f: float = 1.95) -> None:
+    """SURVEY 8(d) sensitivity: focal length f = f_scale * W for every rig camera and target, with the
+    body scaled by 1.95 / f_scale about the look-at point so its image (and the ~40 % foreground) stays
+    put while the Gaussians (metric scales unchanged) cover 1.95 / f_scale times fewer pixels per axis.
+    1.95 is the human-scale headline."""
+    global FOCAL_SCALE, ELLIPSOIDS
+    k = 1.95 / float(f)
+    FOCAL_SCALE = float(f)
+    ELLIPSOIDS = tuple((RIG_LOOK + k * (c - RIG_LOOK), k * a) for c, a in _BASE_ELLIPSOIDS)
 
 
 def _raycast_depth(cam: Camera):

@@ -107,6 +107,18 @@ def test_tile8_lists_and_composite(oracle_lib, monkeypatch, case):
     assert out["tile_px"] == 8
 
 
+@pytest.mark.parametrize("f", [1.0, 0.55])
+def test_focal_scale_sensitivity_configs(ctx, oracle_lib, f):
+    """The footprint-sensitivity inputs of bench.py --focal-scale (f = 1.0 W, 0.55 W, body
+    scaled to keep its image) at c2 size: every stage and every pixel against the oracle."""
+    try:
+        sg.set_focal_scale(f)
+        s = sg.make_config("c2")
+    finally:
+        sg.set_focal_scale(1.95)
+    full_parity(ctx, oracle_lib, s)
+
+
 def test_c2_full(ctx, oracle_lib):
     """configs[1]: 2 x 512^2 sources, 512^2 target -- every stage, every pixel."""
     full_parity(ctx, oracle_lib, sg.make_config("c2"))

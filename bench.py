@@ -759,6 +759,8 @@ def roofline(ctx, g, cam0, out0, H, W, C_, stages, n_g, stream, ms_per_view=None
     b_view = n_g * 48 + nvis * fb + 16 * K + 4 * H * W * (C_ + 1)
     r["view"] = {"ms": view_ms, "alg_bytes": b_view, "hbm_frac": b_view / (view_ms / 1e3) / 1e9 / hbm,
                  "fp32_frac": flops_comp / (view_ms / 1e3) / 1e12 / fp32_tflops}
+    # roofline% = max(t_HBM, t_FP32) / t_measured for the whole view
+    r["view"]["roofline_frac"] = max(r["view"]["hbm_frac"], r["view"]["fp32_frac"])
     return r
 
 

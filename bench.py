@@ -562,12 +562,22 @@ def c3_single_view(args, ctx, g, views, params, params_sync, H, W, C_, n_g, stre
     # pixel, write pos_alpha 16 + cov 32 + features 2C per lifted Gaussian
     b_unp = src_px * (4 + 1 + 12 + 16 + 4 + 2 * C_) + n_g * (16 + 32 + 2 * C_)
     t_r, t_u = r_ms["median"] / 1e3, u_ms["median"] / 1e3
+    # composited pairs of this view (counters run) for the FP32 side: P_comp (2C + 12) flops
+    from tests import _parity as P   # d2h helper only (no oracle use)
+    ctx.rasterize(g, -1, Ki, Ri, H, W, tb.default_params(flags=tb.TA_FLAG_DEBUG_COUNTS), F, A, stream)
+    torch.cuda.synchronize()
+    pairs = int(P.d2h(ctx.debug_last().n_contrib, H * W, np.int32).astype(np.int64).sum())
+    mhz = float(peaks.get("sm_max_mhz", SM_CLOCK_MAX_MHZ))
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    fp32 = sms * FP32_LANES_PER_SM * 2 * mhz * 1e6
+    fp32_frac = pairs * (2 * C_ + 12) / t_r / fp32
     return {"target": "c3 (BASELINE.json configs[2]): 1024^2 on the arc between the pairs, C = 32",
             "rasterize_ms": r_ms, "views_per_s": 1e3 / r_ms["median"],
             "roofline": {"bound": "hbm", "alg_bytes": b_alg, "achieved": b_alg / t_r / 1e9, "peak": hbm,
                          "unit": "GB/s", "frac": b_alg / t_r / 1e9 / hbm, "peak_source": src,
                          "north_star_target_ms": b_alg / (0.5 * hbm * 1e9) * 1e3,
-                         "entries": int(d.K), "coarse_entries": int(d.Kc)},
+                         "entries": int(d.K), "coarse_entries": int(d.Kc), "composited_pairs": pairs,
+                         "fp32_frac": fp32_frac, "roofline_frac": max(b_alg / t_r / 1e9 / hbm, fp32_frac)},
             "unproject_ms": u_ms,
             "unproject_roofline": {"bound": "hbm", "alg_bytes": b_unp, "achieved": b_unp / t_u / 1e9, "peak": hbm,
                                    "unit": "GB/s", "frac": b_unp / t_u / 1e9 / hbm},

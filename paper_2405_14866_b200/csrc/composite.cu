@@ -10,7 +10,9 @@
 //                      ellipse can reach its still-active pixels (splat record + fp16 feature row by
 //                      cp.async), runs the normative fp32 recurrence with packed fp32x2 instructions
 //                      (T, alpha', the decisions and A bit-exact) and accumulates F on the tensor
-//                      cores (mma.sync m16n8k16, fp16 hi/lo weights x fp16 features, fp32 accumulate).
+//                      cores (mma.sync m16n8k16, fp16 hi/lo weights x fp16 features, fp32 accumulate;
+//                      for C = 32 / 64 the accumulators live in tensor memory between chunks,
+//                      tcgen05.ld / st, which frees the registers for a fifth CTA per SM).
 //   k_composite<C, float>  fp32-stored features: the same recurrence, all-SIMT packed FFMA2
 //                      accumulation, one CTA per tile.
 #include <algorithm>
